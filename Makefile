@@ -1,0 +1,35 @@
+# Build the B200 (sm_100a) decoder library and the host-side C helpers.
+#   make            -> paper_1802_08483_b200/libbsidmap.so, oracle/libbsid_oracle.so, bsidgen/libbsidgen.so
+#   make ptxas      -> register / spill report of every kernel
+NVCC    ?= /usr/local/cuda/bin/nvcc
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O2 --expt-relaxed-constexpr
+CSRC    := paper_1802_08483_b200/csrc
+OBJDIR  := build/obj
+CU      := $(wildcard $(CSRC)/*.cu)
+OBJS    := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(CU))
+HDRS    := $(wildcard $(CSRC)/*.cuh) include/bsidmap.h
+LIB     := paper_1802_08483_b200/libbsidmap.so
+
+all: $(LIB) oracle/libbsid_oracle.so bsidgen/libbsidgen.so
+
+$(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+
+oracle/libbsid_oracle.so: oracle/bsid_oracle.c
+	gcc -O2 -std=c11 -fPIC -shared -fno-fast-math -ffp-contract=off -o $@ $< -lm
+
+bsidgen/libbsidgen.so: bsidgen/bsidgen.c
+	gcc -O2 -std=c11 -fPIC -shared -o $@ $< -lm
+
+ptxas:
+	@for f in $(CU); do $(NVCC) $(NVFLAGS) -Xptxas -v -c $$f -o /dev/null 2>&1 | grep -E "Compiling|registers|spill" ; done
+
+clean:
+	rm -rf build $(LIB) oracle/libbsid_oracle.so bsidgen/libbsidgen.so
+
+.PHONY: all clean ptxas

@@ -1,0 +1,170 @@
+/*
+ * bsidmap.h -- C ABI of the B200 batched BSID MAP (forward-backward) decoder,
+ * arXiv 1802.08483.  "P:n" cites line n of the paper's LaTeX;
+ * equations are cited by label.
+ *
+ * The decoder computes, for every frame of a batch, the a-posteriori symbol
+ * probabilities L_i(D) of eqn:L:
+ *
+ *   L_i(D) = 1/lambda_N(rho - tau) * sum_{m',m} alpha_i(m') gamma_i(m',m,D) beta_{i+1}(m)
+ *
+ * with gamma from the corridor-constrained receiver-metric lattice
+ * (eqn:gamma P:156-161, eqn:F P:197-204, eqn:F_lastrow P:228-235, corridor
+ * P:250-254), alpha/beta from the normalised recursions (eqn:alpha,
+ * eqn:beta, eqn:alpha_norm P:257-271), the receiver metric in single and the
+ * states in double precision.  Boundary priors are point masses:
+ * alpha_0 = delta(0), beta_N = delta(rho - tau) (reading R1).
+ *
+ * Bit conventions: bit t (LSB = bit 0) of a codeword word is the t-th
+ * transmitted bit x_{t+1}; received sequences are packed LSB-first into
+ * 32-bit words, y_1 = bit 0 of the frame's first word (reading R15).
+ *
+ * Every function returns BSIDMAP_OK (0) or a negative error code; the
+ * message of the last failure is available from bsidmap_last_error().
+ * Per-frame conditions are reported in frame_status[], never as errors.
+ * A decoder is used by one host thread at a time; decoders on different
+ * devices are independent (one process per GPU).
+ */
+#ifndef BSIDMAP_H
+#define BSIDMAP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bsidmap_decoder bsidmap_decoder; /* opaque; owns the device codebook and workspace */
+
+/* return codes */
+#define BSIDMAP_OK 0
+#define BSIDMAP_EINVAL (-1)         /* invalid argument (see bsidmap_last_error) */
+#define BSIDMAP_ENOTINJECTIVE (-2)  /* some C_i maps two symbols to one codeword */
+#define BSIDMAP_ENOMEM (-3)         /* device allocation failed */
+#define BSIDMAP_EPLAN (-4)          /* no feasible launch plan (e.g. corridor wider than 32) */
+#define BSIDMAP_ECUDA (-5)          /* a CUDA call failed */
+
+/* per-frame status */
+#define BSIDMAP_FRAME_OK 0
+#define BSIDMAP_FRAME_DRIFT_OUT_OF_RANGE 1 /* rho - tau outside [m_tau^-, m_tau^+]; L rows = 0 */
+#define BSIDMAP_FRAME_UNDERFLOW 2          /* an all-zero alpha/beta/L row: Y impossible under the limits; L rows = 0 */
+
+/* storage schedule */
+#define BSIDMAP_MODE_AUTO 0      /* planner choice */
+#define BSIDMAP_MODE_STORED 1    /* paper's global storage: every gamma stored in HBM, read back for L */
+#define BSIDMAP_MODE_RECOMPUTE 2 /* memory-reduced: gamma recomputed in the L pass; only Gamma = sum_D gamma,
+                                    alpha, beta kept (the paper's local storage trade) */
+
+/*
+ * Create a decoder on CUDA device `device`.
+ *   q, n, N        : alphabet size, codeword length, symbols per frame; 2 <= q <= 2^n,
+ *                    1 <= n <= 32, N >= 1.
+ *   codebook_host  : HOST pointer, N*q words, C[i*q + D] = C_i(D); copied, caller keeps ownership.
+ *                    Each C_i must be injective (else BSIDMAP_ENOTINJECTIVE).
+ *   Pi, Pd, Ps     : BSID channel; Pi, Pd, Ps >= 0, Ps <= 1, Pi + Pd < 1.
+ *   mn_lo, mn_hi   : per-codeword drift limits m_n^-, m_n^+ (corridor, M_n = mn_hi - mn_lo + 1 <= 32),
+ *                    mn_lo <= 0 <= mn_hi, n + mn_hi <= 64.
+ *   mt_lo, mt_hi   : trellis drift limits m_tau^-, m_tau^+ (M_tau states), mt_lo <= mn_lo, mt_hi >= mn_hi.
+ *   mode           : BSIDMAP_MODE_*.
+ * On success *out receives the decoder.  Allocates only the codebook (N*q*4 bytes);
+ * the workspace is allocated lazily by the first decode of a given size.
+ */
+int bsidmap_create(bsidmap_decoder **out, int q, int n, int N, const uint32_t *codebook_host,
+                   double Pi, double Pd, double Ps, int mn_lo, int mn_hi, int mt_lo, int mt_hi,
+                   int mode, int device);
+
+/*
+ * Decode num_frames frames.  All pointers are DEVICE pointers on the decoder's device,
+ * caller-owned, and must stay valid until `cuda_stream` (a cudaStream_t; NULL = legacy
+ * default stream) reaches the end of the call.  The call is asynchronous: it only
+ * enqueues work (it may block once to grow the workspace).
+ *   rx_words        : packed received bits (LSB-first); frame f starts at word rx_word_offset[f]
+ *                     and owns ceil(rho[f]/32) words.
+ *   rx_word_offset  : [num_frames] int64.
+ *   rho             : [num_frames] int32 received lengths.
+ *   priors          : [num_frames][N][q] FP32 P(D_i = D) weights, or NULL for uniform 1/q
+ *                     (P:166-170); rows need not sum to 1; entries >= 0.
+ *   L_out           : [num_frames][N][q] FP32 APPs L_i(D); each row sums to 1 (0 for failed frames).
+ *   frame_status    : [num_frames] int32 BSIDMAP_FRAME_*.
+ */
+int bsidmap_decode_batch(bsidmap_decoder *d, int num_frames, const uint32_t *rx_words,
+                         const int64_t *rx_word_offset, const int32_t *rho, const float *priors,
+                         float *L_out, int32_t *frame_status, void *cuda_stream);
+
+/*
+ * Same computation with HOST buffers (end-to-end path): copies the inputs to the
+ * device (pinned memory gives async copies), decodes, copies L and the status back and
+ * synchronises `cuda_stream` before returning.  rx_words_total = number of words in rx_words.
+ */
+int bsidmap_decode_batch_host(bsidmap_decoder *d, int num_frames, const uint32_t *rx_words,
+                              size_t rx_words_total, const int64_t *rx_word_offset, const int32_t *rho,
+                              const float *priors, float *L_out, int32_t *frame_status, void *cuda_stream);
+
+/* Release the decoder and all its device memory (synchronises its device). NULL is a no-op. */
+void bsidmap_destroy(bsidmap_decoder *d);
+
+/* Message of the last failure on this decoder ("" if none); valid until the next call. NULL d: global message. */
+const char *bsidmap_last_error(const bsidmap_decoder *d);
+
+/* Device workspace bytes needed to decode num_frames frames in `mode` without chunking
+   (the paper's memory estimate).  Returns 0 for an invalid mode. */
+size_t bsidmap_workspace_bytes(const bsidmap_decoder *d, int num_frames, int mode);
+
+/* Cap the workspace (bytes; 0 = automatic, 85% of free memory); larger batches are chunked. */
+int bsidmap_set_workspace_limit(bsidmap_decoder *d, size_t bytes);
+
+/* Override the storage schedule of subsequent decodes (BSIDMAP_MODE_*). */
+int bsidmap_set_mode(bsidmap_decoder *d, int mode);
+
+/*
+ * Per-phase device timing of the next decodes (CUDA events on the decode stream).
+ * bsidmap_phase_times writes up to n_max entries of the LAST decode_batch, in ms:
+ *   [0] status init + accumulator clear, [1] lattice pass 1 (gamma / Gamma),
+ *   [2] alpha/beta recursions, [3] lattice pass 2 / stored APP, [4] finalize.
+ * and returns the number written.  It synchronises the decode stream.
+ */
+int bsidmap_set_timing(bsidmap_decoder *d, int enable);
+int bsidmap_phase_times(bsidmap_decoder *d, float *ms, int n_max);
+
+/* Kernel launches issued by the last decode_batch call. */
+long bsidmap_last_launch_count(const bsidmap_decoder *d);
+
+/*
+ * Human/JSON-readable launch plan for num_frames frames (mode, chunking, grid and block
+ * sizes, lattice core: "spec" fully unrolled or "generic"), written to buf (NUL-terminated).
+ * Returns the length, or a negative error code.
+ */
+int bsidmap_plan_info(bsidmap_decoder *d, int num_frames, char *buf, size_t buf_len);
+
+/*
+ * Corridor nodes per lattice of this decoder's shape, n M_n - m_n^-(m_n^- - 1)/2,
+ * and the number of lattices with a valid window (0 <= n i + m' <= rho) for the given
+ * host rho[] -- the algorithmic work counters used by the roofline.
+ */
+long bsidmap_lattice_nodes(const bsidmap_decoder *d);
+long long bsidmap_valid_lattices(const bsidmap_decoder *d, int num_frames, const int32_t *rho_host);
+
+/*
+ * Debug/parity: gamma_i(m', m, D) of symbol index i for every frame, true scale, FP64,
+ * gamma_out[f][m' - m_tau^-][m - m' - m_n^-][D] (DEVICE pointer, num_frames*M_tau*M_n*q
+ * doubles).  Uses the same lattice core as the decode.  Inputs as in decode_batch.
+ * Synchronous.
+ */
+int bsidmap_debug_gamma(bsidmap_decoder *d, int num_frames, const uint32_t *rx_words,
+                        const int64_t *rx_word_offset, const int32_t *rho, const float *priors, int i,
+                        double *gamma_out, void *cuda_stream);
+
+/*
+ * Debug/parity: after a decode_batch whose workspace held all frames (no chunking), copy
+ * the normalised FP64 alpha and beta rows [num_frames][N+1][M_tau] to DEVICE pointers.
+ * Synchronous.  Returns BSIDMAP_EINVAL if the last decode was chunked or smaller.
+ */
+int bsidmap_debug_states(bsidmap_decoder *d, int num_frames, double *alpha_out, double *beta_out,
+                         void *cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BSIDMAP_H */

@@ -1,0 +1,512 @@
+// api.cu -- the C ABI (include/bsidmap.h): argument validation, the launch
+// planner (row a6: storage schedule from the memory estimate, chunking,
+// grid/block geometry for 148 SMs) and the launch sequence of one decode.
+//
+// Launch sequence per chunk of frames (all on the caller's stream):
+//   k_frame_init -> memset(Lacc) -> lattice pass 1 (Gamma; STORED: + gamma)
+//   -> k_alpha_beta -> lattice pass 2 (RECOMPUTE) | k_app_stored (STORED)
+//   -> k_finalize
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/bsidmap.h"
+#include "k_lattice.cuh"
+
+namespace bsidmap {
+__global__ void k_frame_init(const DecodeParams p);
+__global__ void k_alpha_beta(const DecodeParams p);
+__global__ void k_finalize(const DecodeParams p);
+}  // namespace bsidmap
+
+using namespace bsidmap;
+
+namespace {
+constexpr int kPhases = 5;
+std::string g_err;  // failures without a decoder (create)
+}  // namespace
+
+struct bsidmap_decoder {
+  int device = 0;
+  int q = 0, n = 0, N = 0, mn_lo = 0, mn_hi = 0, mt_lo = 0, mt_hi = 0, Mn = 0, Mt = 0;
+  double Pi = 0, Pd = 0, Ps = 0;
+  int mode = BSIDMAP_MODE_AUTO;
+  uint32_t* d_C = nullptr;
+  CoreKernels kern{};
+  bool spec = false;
+  LatticeConst lc{};
+  // workspace
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  size_t ws_limit = 0;
+  int last_chunk = 0, last_frames = 0, last_mode = 0;
+  // host-path staging
+  void* hs = nullptr;
+  size_t hs_bytes = 0;
+  // timing
+  bool timing = false;
+  cudaEvent_t ev[kPhases + 1] = {};
+  cudaStream_t ev_stream = nullptr;
+  bool ev_valid = false;
+  long launches = 0;
+  std::string err;
+};
+
+namespace {
+
+int fail(bsidmap_decoder* d, int code, const std::string& msg) {
+  if (d) d->err = msg; else g_err = msg;
+  return code;
+}
+
+int cuda_fail(bsidmap_decoder* d, cudaError_t e, const char* what) {
+  return fail(d, BSIDMAP_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Layout {
+  size_t gsum, gamma, alpha, beta, lacc, total;
+};
+
+// Bytes per frame of each workspace array (the paper's memory estimate).
+Layout layout(const bsidmap_decoder* d, long F, int mode) {
+  Layout l{};
+  l.gsum = align_up((size_t)F * d->N * d->Mn * d->Mt * sizeof(float));
+  l.gamma = mode == BSIDMAP_MODE_STORED ? align_up((size_t)F * d->N * d->q * d->Mn * d->Mt * sizeof(float)) : 0;
+  l.alpha = align_up((size_t)F * (d->N + 1) * d->Mt * sizeof(double));
+  l.beta = l.alpha;
+  l.lacc = align_up((size_t)F * d->N * d->q * sizeof(double));
+  l.total = l.gsum + l.gamma + l.alpha + l.beta + l.lacc;
+  return l;
+}
+
+struct Plan {
+  int mode;
+  int chunk;        // frames per chunk
+  int nchunks;
+  int ab_threads;   // k_alpha_beta block size
+  size_t ab_smem, app_smem, l1_smem;
+};
+
+size_t budget(const bsidmap_decoder* d) {
+  if (d->ws_limit) return d->ws_limit;
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return 0;
+  return (size_t)((double)(fr + d->ws_bytes) * 0.85);
+}
+
+int make_plan(bsidmap_decoder* d, int F, Plan* P) {
+  int mode = d->mode;
+  const size_t bud = budget(d);
+  const size_t per_rc = layout(d, 1, BSIDMAP_MODE_RECOMPUTE).total;
+  const size_t per_st = layout(d, 1, BSIDMAP_MODE_STORED).total;
+  if (mode == BSIDMAP_MODE_AUTO) {
+    // Stored gamma costs 8 B of HBM traffic per gamma value against ~5n FP32 flops to
+    // recompute it; on B200 recomputing is the faster side of the ridge,
+    // and it is the only one whose batches fit for long frames.  RECOMPUTE by default.
+    mode = BSIDMAP_MODE_RECOMPUTE;
+  }
+  const size_t per = mode == BSIDMAP_MODE_STORED ? per_st : per_rc;
+  long chunk = per ? (long)(bud / per) : F;
+  if (chunk < 1) return fail(d, BSIDMAP_ENOMEM, "workspace for one frame (" + std::to_string(per) +
+                                                    " B) exceeds the budget (" + std::to_string(bud) + " B)");
+  chunk = std::min<long>(chunk, F);
+  P->mode = mode;
+  P->chunk = (int)chunk;
+  P->nchunks = (int)((F + chunk - 1) / chunk);
+  P->ab_threads = std::min(1024, ((d->Mt + 31) / 32) * 32);
+  P->ab_smem = (2 * (size_t)d->Mt + 33) * sizeof(double);
+  P->app_smem = kLatticeThreads * sizeof(double) + (size_t)std::min(d->q, kAppDChunk) * kLatticeThreads * 4 +
+                (size_t)d->q * 4;
+  P->l1_smem = (size_t)d->q * 4;
+  return BSIDMAP_OK;
+}
+
+int ensure_ws(bsidmap_decoder* d, size_t bytes) {
+  if (bytes <= d->ws_bytes) return BSIDMAP_OK;
+  if (d->ws) {
+    cudaDeviceSynchronize();
+    cudaFree(d->ws);
+    d->ws = nullptr;
+    d->ws_bytes = 0;
+  }
+  cudaError_t e = cudaMalloc(&d->ws, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(d, BSIDMAP_ENOMEM, "cudaMalloc(" + std::to_string(bytes) + ") failed: " + cudaGetErrorString(e));
+  }
+  d->ws_bytes = bytes;
+  return BSIDMAP_OK;
+}
+
+int set_smem(bsidmap_decoder* d, const void* fn, size_t bytes) {
+  if (bytes <= 48 * 1024) return BSIDMAP_OK;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return cuda_fail(d, e, "cudaFuncSetAttribute(smem)");
+  return BSIDMAP_OK;
+}
+
+void fill_params(const bsidmap_decoder* d, DecodeParams* p) {
+  std::memset(p, 0, sizeof(*p));
+  p->q = d->q; p->n = d->n; p->N = d->N;
+  p->mn_lo = d->mn_lo; p->mn_hi = d->mn_hi; p->Mn = d->Mn;
+  p->mt_lo = d->mt_lo; p->mt_hi = d->mt_hi; p->Mt = d->Mt;
+  p->C = d->d_C;
+  p->lc = d->lc;
+}
+
+void bind_ws(const bsidmap_decoder* d, const Layout& l, DecodeParams* p) {
+  char* b = static_cast<char*>(d->ws);
+  p->Gsum = reinterpret_cast<float*>(b);
+  b += l.gsum;
+  p->gamma = l.gamma ? reinterpret_cast<float*>(b) : nullptr;
+  b += l.gamma;
+  p->alpha = reinterpret_cast<double*>(b);
+  b += l.alpha;
+  p->beta = reinterpret_cast<double*>(b);
+  b += l.beta;
+  p->Lacc = reinterpret_cast<double*>(b);
+}
+
+void record(bsidmap_decoder* d, int k, cudaStream_t s) {
+  if (d->timing) cudaEventRecord(d->ev[k], s);
+}
+
+// Lattice-pass launches over i in slices of <= 65535 (gridDim.y limit).
+template <class Fn>
+void for_i_slices(int N, Fn fn) {
+  for (int i0 = 0; i0 < N; i0 += 65535) fn(i0, std::min(65535, N - i0));
+}
+
+int run_chunk(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s, bool first_chunk, bool last_chunk) {
+  const long lanes = (long)p.F * d->Mt;
+  const unsigned gx = (unsigned)((lanes + kLatticeThreads - 1) / kLatticeThreads);
+  if (first_chunk) record(d, 0, s);
+  k_frame_init<<<(p.F + 255) / 256, 256, 0, s>>>(p);
+  cudaMemsetAsync(p.Lacc, 0, (size_t)p.F * d->N * d->q * sizeof(double), s);
+  d->launches += 1;
+  if (first_chunk) record(d, 1, s);
+  auto l1 = P.mode == BSIDMAP_MODE_STORED ? d->kern.gamma_store : d->kern.gamma_sum;
+  for_i_slices(d->N, [&](int i0, int ni) {
+    p.i_base = i0;
+    l1<<<dim3(gx, ni), kLatticeThreads, P.l1_smem, s>>>(p);
+    d->launches++;
+  });
+  p.i_base = 0;
+  if (first_chunk) record(d, 2, s);
+  k_alpha_beta<<<dim3(p.F, 2), P.ab_threads, P.ab_smem, s>>>(p);
+  d->launches++;
+  if (first_chunk) record(d, 3, s);
+  auto l2 = P.mode == BSIDMAP_MODE_STORED ? d->kern.app_stored : d->kern.app;
+  for_i_slices(d->N, [&](int i0, int ni) {
+    p.i_base = i0;
+    l2<<<dim3(gx, ni), kLatticeThreads, P.app_smem, s>>>(p);
+    d->launches++;
+  });
+  p.i_base = 0;
+  if (first_chunk) record(d, 4, s);
+  const long rows = (long)p.F * d->N;
+  k_finalize<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(p);
+  d->launches++;
+  if (last_chunk) record(d, 5, s);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(d, e, "kernel launch");
+  return BSIDMAP_OK;
+}
+
+int check_inputs(bsidmap_decoder* d, int F, const void* rx, const void* off, const void* rho, const void* L,
+                 const void* st) {
+  if (!d) return fail(nullptr, BSIDMAP_EINVAL, "decoder is NULL");
+  if (F < 0) return fail(d, BSIDMAP_EINVAL, "num_frames < 0");
+  if (F > 0 && (!rx || !off || !rho || !L || !st))
+    return fail(d, BSIDMAP_EINVAL, "rx_words, rx_word_offset, rho, L_out and frame_status must be non-NULL");
+  return BSIDMAP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bsidmap_create(bsidmap_decoder** out, int q, int n, int N, const uint32_t* codebook_host, double Pi, double Pd,
+                   double Ps, int mn_lo, int mn_hi, int mt_lo, int mt_hi, int mode, int device) {
+  if (!out) return fail(nullptr, BSIDMAP_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n < 1 || n > 32) return fail(nullptr, BSIDMAP_EINVAL, "need 1 <= n <= 32");
+  if (q < 2 || (n < 32 && (uint64_t)q > (1ull << n))) return fail(nullptr, BSIDMAP_EINVAL, "need 2 <= q <= 2^n");
+  if (N < 1) return fail(nullptr, BSIDMAP_EINVAL, "need N >= 1");
+  if (!codebook_host) return fail(nullptr, BSIDMAP_EINVAL, "codebook is NULL");
+  if (!(Pi >= 0 && Pd >= 0 && Ps >= 0 && Ps <= 1 && Pi + Pd < 1))
+    return fail(nullptr, BSIDMAP_EINVAL, "need Pi, Pd, Ps >= 0, Ps <= 1, Pi + Pd < 1");
+  if (!(mn_lo <= 0 && 0 <= mn_hi)) return fail(nullptr, BSIDMAP_EINVAL, "need m_n^- <= 0 <= m_n^+");
+  if (!(mt_lo <= mn_lo && mt_hi >= mn_hi)) return fail(nullptr, BSIDMAP_EINVAL, "need m_tau^- <= m_n^-, m_tau^+ >= m_n^+");
+  if (n + mn_hi > kMaxWindow) return fail(nullptr, BSIDMAP_EINVAL, "need n + m_n^+ <= 64");
+  if (mode < 0 || mode > 2) return fail(nullptr, BSIDMAP_EINVAL, "unknown mode");
+  const int Mn = mn_hi - mn_lo + 1;
+  if (Mn > kMaxMn) return fail(nullptr, BSIDMAP_EPLAN, "corridor width M_n > 32 is not supported");
+  if ((long)(mt_hi - mt_lo + 1) * (N + 1) > (1l << 40)) return fail(nullptr, BSIDMAP_EINVAL, "state space too large");
+  const uint32_t mask = n == 32 ? 0xffffffffu : ((1u << n) - 1u);
+  for (int i = 0; i < N; i++) {
+    std::set<uint32_t> seen;
+    for (int D = 0; D < q; D++) {
+      const uint32_t w = codebook_host[(size_t)i * q + D];
+      if (w & ~mask) return fail(nullptr, BSIDMAP_EINVAL, "codeword has bits above n");
+      if (!seen.insert(w).second)
+        return fail(nullptr, BSIDMAP_ENOTINJECTIVE, "C_" + std::to_string(i) + " is not injective");
+    }
+  }
+  bsidmap_decoder* d = new bsidmap_decoder();
+  d->device = device;
+  d->q = q; d->n = n; d->N = N;
+  d->mn_lo = mn_lo; d->mn_hi = mn_hi; d->Mn = Mn;
+  d->mt_lo = mt_lo; d->mt_hi = mt_hi; d->Mt = mt_hi - mt_lo + 1;
+  d->Pi = Pi; d->Pd = Pd; d->Ps = Ps;
+  d->mode = mode;
+  // lattice constants (eqn:F, Q-dot); row 0 = insertions only, F_{0,j} = 2^80 (Pi/2)^j
+  const double Pt = 1.0 - Pi - Pd;
+  d->lc.a = (float)(0.5 * Pi);
+  d->lc.b = (float)Pd;
+  d->lc.qm = (float)(Pt * (1.0 - Ps));
+  d->lc.qs = (float)(Pt * Ps);
+  for (int e = 0; e < kMaxMn; e++) {
+    const int j = mn_lo + e;
+    d->lc.row0[e] = (e < Mn && j >= 0) ? (float)std::ldexp(std::pow(0.5 * Pi, j), kLatticeSeedLog2) : 0.f;
+  }
+  d->spec = find_spec_kernels(n, mn_lo, Mn, &d->kern);
+  if (!d->spec && !find_generic_kernels(Mn, &d->kern)) {
+    delete d;
+    return fail(nullptr, BSIDMAP_EPLAN, "no lattice core for M_n = " + std::to_string(Mn));
+  }
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaMalloc(&d->d_C, sizeof(uint32_t) * (size_t)N * q);
+  if (e == cudaSuccess) e = cudaMemcpy(d->d_C, codebook_host, sizeof(uint32_t) * (size_t)N * q, cudaMemcpyHostToDevice);
+  for (int k = 0; e == cudaSuccess && k <= kPhases; k++) e = cudaEventCreate(&d->ev[k]);
+  if (e != cudaSuccess) {
+    std::string m = std::string("device setup: ") + cudaGetErrorString(e);
+    bsidmap_destroy(d);
+    return fail(nullptr, BSIDMAP_ECUDA, m);
+  }
+  *out = d;
+  return BSIDMAP_OK;
+}
+
+int bsidmap_decode_batch(bsidmap_decoder* d, int F, const uint32_t* rx, const int64_t* off, const int32_t* rho,
+                         const float* priors, float* L, int32_t* status, void* stream) {
+  int rc = check_inputs(d, F, rx, off, rho, L, status);
+  if (rc) return rc;
+  d->launches = 0;
+  d->ev_valid = false;
+  if (F == 0) return BSIDMAP_OK;
+  cudaSetDevice(d->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Plan P;
+  if ((rc = make_plan(d, F, &P))) return rc;
+  const Layout l = layout(d, P.chunk, P.mode);
+  if ((rc = ensure_ws(d, l.total))) return rc;
+  if ((rc = set_smem(d, (const void*)k_alpha_beta, P.ab_smem))) return rc;
+  if ((rc = set_smem(d, (const void*)(P.mode == BSIDMAP_MODE_STORED ? d->kern.app_stored : d->kern.app), P.app_smem)))
+    return rc;
+  for (int c = 0; c < P.nchunks; c++) {
+    const int f0 = c * P.chunk;
+    DecodeParams p;
+    fill_params(d, &p);
+    bind_ws(d, l, &p);
+    p.F = std::min(P.chunk, F - f0);
+    p.rx = rx;
+    p.rx_off = off + f0;
+    p.rho = rho + f0;
+    p.priors = priors ? priors + (size_t)f0 * d->N * d->q : nullptr;
+    p.status = status + f0;
+    p.L = L + (size_t)f0 * d->N * d->q;
+    if ((rc = run_chunk(d, P, p, s, c == 0, c == P.nchunks - 1))) return rc;
+  }
+  d->last_chunk = P.chunk;
+  d->last_frames = F;
+  d->last_mode = P.mode;
+  d->ev_stream = s;
+  d->ev_valid = d->timing;
+  return BSIDMAP_OK;
+}
+
+int bsidmap_decode_batch_host(bsidmap_decoder* d, int F, const uint32_t* rx, size_t rx_words_total,
+                              const int64_t* off, const int32_t* rho, const float* priors, float* L, int32_t* status,
+                              void* stream) {
+  int rc = check_inputs(d, F, rx, off, rho, L, status);
+  if (rc) return rc;
+  if (F == 0) return BSIDMAP_OK;
+  cudaSetDevice(d->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t nL = (size_t)F * d->N * d->q;
+  const size_t b_rx = align_up(rx_words_total * 4), b_off = align_up((size_t)F * 8), b_rho = align_up((size_t)F * 4);
+  const size_t b_pri = priors ? align_up(nL * 4) : 0, b_L = align_up(nL * 4), b_st = align_up((size_t)F * 4);
+  const size_t need = b_rx + b_off + b_rho + b_pri + b_L + b_st;
+  if (need > d->hs_bytes) {
+    if (d->hs) {
+      cudaStreamSynchronize(s);
+      cudaFree(d->hs);
+    }
+    d->hs = nullptr;
+    d->hs_bytes = 0;
+    cudaError_t e = cudaMalloc(&d->hs, need);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(d, BSIDMAP_ENOMEM, "staging cudaMalloc failed");
+    }
+    d->hs_bytes = need;
+  }
+  char* b = static_cast<char*>(d->hs);
+  uint32_t* d_rx = reinterpret_cast<uint32_t*>(b); b += b_rx;
+  int64_t* d_off = reinterpret_cast<int64_t*>(b); b += b_off;
+  int32_t* d_rho = reinterpret_cast<int32_t*>(b); b += b_rho;
+  float* d_pri = priors ? reinterpret_cast<float*>(b) : nullptr; b += b_pri;
+  float* d_L = reinterpret_cast<float*>(b); b += b_L;
+  int32_t* d_st = reinterpret_cast<int32_t*>(b);
+  cudaMemcpyAsync(d_rx, rx, rx_words_total * 4, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(d_off, off, (size_t)F * 8, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(d_rho, rho, (size_t)F * 4, cudaMemcpyHostToDevice, s);
+  if (priors) cudaMemcpyAsync(d_pri, priors, nL * 4, cudaMemcpyHostToDevice, s);
+  if ((rc = bsidmap_decode_batch(d, F, d_rx, d_off, d_rho, d_pri, d_L, d_st, stream))) return rc;
+  cudaMemcpyAsync(L, d_L, nL * 4, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(status, d_st, (size_t)F * 4, cudaMemcpyDeviceToHost, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(d, e, "decode_batch_host");
+  return BSIDMAP_OK;
+}
+
+void bsidmap_destroy(bsidmap_decoder* d) {
+  if (!d) return;
+  cudaSetDevice(d->device);
+  cudaDeviceSynchronize();
+  if (d->ws) cudaFree(d->ws);
+  if (d->hs) cudaFree(d->hs);
+  if (d->d_C) cudaFree(d->d_C);
+  for (int k = 0; k <= kPhases; k++)
+    if (d->ev[k]) cudaEventDestroy(d->ev[k]);
+  delete d;
+}
+
+const char* bsidmap_last_error(const bsidmap_decoder* d) { return d ? d->err.c_str() : g_err.c_str(); }
+
+size_t bsidmap_workspace_bytes(const bsidmap_decoder* d, int F, int mode) {
+  if (!d || F < 0) return 0;
+  if (mode == BSIDMAP_MODE_AUTO) mode = BSIDMAP_MODE_RECOMPUTE;
+  if (mode != BSIDMAP_MODE_STORED && mode != BSIDMAP_MODE_RECOMPUTE) return 0;
+  return layout(d, F, mode).total;
+}
+
+int bsidmap_set_workspace_limit(bsidmap_decoder* d, size_t bytes) {
+  if (!d) return fail(nullptr, BSIDMAP_EINVAL, "decoder is NULL");
+  d->ws_limit = bytes;
+  return BSIDMAP_OK;
+}
+
+int bsidmap_set_mode(bsidmap_decoder* d, int mode) {
+  if (!d) return fail(nullptr, BSIDMAP_EINVAL, "decoder is NULL");
+  if (mode < 0 || mode > 2) return fail(d, BSIDMAP_EINVAL, "unknown mode");
+  d->mode = mode;
+  return BSIDMAP_OK;
+}
+
+int bsidmap_set_timing(bsidmap_decoder* d, int enable) {
+  if (!d) return fail(nullptr, BSIDMAP_EINVAL, "decoder is NULL");
+  d->timing = enable != 0;
+  return BSIDMAP_OK;
+}
+
+int bsidmap_phase_times(bsidmap_decoder* d, float* ms, int n_max) {
+  if (!d || !ms) return fail(d, BSIDMAP_EINVAL, "bad arguments");
+  if (!d->ev_valid) return fail(d, BSIDMAP_EINVAL, "no timed decode (enable bsidmap_set_timing first)");
+  cudaError_t e = cudaEventSynchronize(d->ev[kPhases]);
+  if (e != cudaSuccess) return cuda_fail(d, e, "cudaEventSynchronize");
+  int k = 0;
+  for (; k < kPhases && k < n_max; k++) {
+    // phases 0-3 are the first chunk; the last phase runs to the end of the last chunk
+    cudaEventElapsedTime(&ms[k], d->ev[k], d->ev[k + 1]);
+  }
+  return k;
+}
+
+long bsidmap_last_launch_count(const bsidmap_decoder* d) { return d ? d->launches : 0; }
+
+int bsidmap_plan_info(bsidmap_decoder* d, int F, char* buf, size_t len) {
+  if (!d || !buf || F < 1) return fail(d, BSIDMAP_EINVAL, "bad arguments");
+  Plan P;
+  int rc = make_plan(d, F, &P);
+  if (rc) return rc;
+  const long lanes = (long)P.chunk * d->Mt;
+  int nb = std::snprintf(
+      buf, len,
+      "{\"mode\": \"%s\", \"frames\": %d, \"chunk\": %d, \"chunks\": %d, \"core\": \"%s\", "
+      "\"lattice_grid\": [%ld, %d], \"lattice_block\": %d, \"alpha_beta_grid\": [%d, 2], \"alpha_beta_block\": %d, "
+      "\"workspace_bytes\": %zu, \"q\": %d, \"n\": %d, \"N\": %d, \"Mn\": %d, \"Mtau\": %d}",
+      P.mode == BSIDMAP_MODE_STORED ? "stored" : "recompute", F, P.chunk, P.nchunks, d->spec ? "spec" : "generic",
+      (lanes + kLatticeThreads - 1) / kLatticeThreads, d->N, kLatticeThreads, P.chunk, P.ab_threads,
+      layout(d, P.chunk, P.mode).total, d->q, d->n, d->N, d->Mn, d->Mt);
+  return nb;
+}
+
+long bsidmap_lattice_nodes(const bsidmap_decoder* d) {
+  if (!d) return 0;
+  return (long)d->n * d->Mn - (long)d->mn_lo * (d->mn_lo - 1) / 2;
+}
+
+long long bsidmap_valid_lattices(const bsidmap_decoder* d, int F, const int32_t* rho) {
+  if (!d || !rho) return 0;
+  long long tot = 0;
+  for (int f = 0; f < F; f++) {
+    const int drift = rho[f] - d->n * d->N;
+    if (drift < d->mt_lo || drift > d->mt_hi) continue;
+    for (int i = 0; i < d->N; i++) {
+      // m' in [mt_lo, mt_hi] with 0 <= n i + m' <= rho
+      const int lo = std::max(d->mt_lo, -d->n * i), hi = std::min(d->mt_hi, rho[f] - d->n * i);
+      if (hi >= lo) tot += hi - lo + 1;
+    }
+  }
+  return tot * d->q;
+}
+
+int bsidmap_debug_gamma(bsidmap_decoder* d, int F, const uint32_t* rx, const int64_t* off, const int32_t* rho,
+                        const float* priors, int i, double* gamma_out, void* stream) {
+  if (!d || F < 1 || !rx || !off || !rho || !gamma_out || i < 0 || i >= d->N)
+    return fail(d, BSIDMAP_EINVAL, "bad arguments");
+  cudaSetDevice(d->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int32_t* st = nullptr;
+  cudaError_t e = cudaMalloc(&st, sizeof(int32_t) * F);
+  if (e != cudaSuccess) return cuda_fail(d, e, "cudaMalloc");
+  DecodeParams p;
+  fill_params(d, &p);
+  p.F = F; p.rx = rx; p.rx_off = off; p.rho = rho; p.priors = priors; p.status = st;
+  p.dbg_gamma = gamma_out; p.dbg_i = i;
+  k_frame_init<<<(F + 255) / 256, 256, 0, s>>>(p);
+  const long lanes = (long)F * d->Mt;
+  d->kern.gamma_dump<<<(unsigned)((lanes + kLatticeThreads - 1) / kLatticeThreads), kLatticeThreads, d->q * 4, s>>>(p);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(st);
+  if (e != cudaSuccess) return cuda_fail(d, e, "debug_gamma");
+  return BSIDMAP_OK;
+}
+
+int bsidmap_debug_states(bsidmap_decoder* d, int F, double* alpha_out, double* beta_out, void* stream) {
+  if (!d || !alpha_out || !beta_out) return fail(d, BSIDMAP_EINVAL, "bad arguments");
+  if (F != d->last_frames || d->last_chunk < F || !d->ws)
+    return fail(d, BSIDMAP_EINVAL, "last decode was chunked or of a different size");
+  cudaSetDevice(d->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const Layout l = layout(d, d->last_chunk, d->last_mode);
+  DecodeParams p;
+  bind_ws(d, l, &p);
+  const size_t bytes = (size_t)F * (d->N + 1) * d->Mt * sizeof(double);
+  cudaMemcpyAsync(alpha_out, p.alpha, bytes, cudaMemcpyDeviceToDevice, s);
+  cudaMemcpyAsync(beta_out, p.beta, bytes, cudaMemcpyDeviceToDevice, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(d, e, "debug_states");
+  return BSIDMAP_OK;
+}
+
+}  // extern "C"

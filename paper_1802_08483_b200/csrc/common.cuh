@@ -1,0 +1,65 @@
+// common.cuh -- parameters shared by the bsidmap kernels (sm_100a).
+//
+// Notation follows arXiv 1802.08483 (P:n = PAPER.md line n): q, n, N,
+// drift limits m_n^-/m_n^+ (corridor, M_n) and m_tau^-/m_tau^+ (trellis
+// states, M_tau), channel Pi, Pd, Ps.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bsidmap {
+
+constexpr int kMaxMn = 32;        // corridor width held in registers
+constexpr int kMaxWindow = 64;    // n + m_n^+ received bits per lattice window
+constexpr int kLatticeSeedLog2 = 80;  // F_{0,0} = 2^80: exact range extension of the FP32 lattice
+
+enum FrameStatus : int32_t { kFrameOk = 0, kFrameDriftOutOfRange = 1, kFrameUnderflow = 2 };
+
+// Channel constants of the FP32 lattice (eqn:F, eqn:F_lastrow, Q-dot P:207-215).
+struct LatticeConst {
+  float a;                 // 1/2 Pi   (insertion of a matching random bit)
+  float b;                 // Pd       (deletion)
+  float qm;                // Pt (1 - Ps)  Q-dot for y == x
+  float qs;                // Pt Ps        Q-dot for y != x
+  float row0[kMaxMn];      // row 0 of the lattice, F_{0,j} = 2^80 (1/2 Pi)^j, indexed by e = j - m_n^-
+};
+
+// Everything one decode launch needs, passed by value (lives in the constant bank).
+struct DecodeParams {
+  int q, n, N;
+  int mn_lo, mn_hi, Mn;
+  int mt_lo, mt_hi, Mt;
+  int F;                      // frames in this chunk
+  const uint32_t* C;          // [N][q] codebook, decoder-owned (bit t = t-th transmitted bit)
+  const uint32_t* rx;         // packed received words, caller-owned
+  const int64_t* rx_off;      // [F] word offset of each frame in rx
+  const int32_t* rho;         // [F] received length
+  const float* priors;        // [F][N][q] or nullptr (uniform 1/q)
+  int32_t* status;            // [F]
+  float* Gsum;                // [F][N][M_n][M_tau]  Gamma_i(m', k) = sum_D gamma_i(m', m'+k, D), scaled 2^80
+  float* gamma;               // stored variant: [F][N][q][M_n][M_tau] gamma, scaled 2^80
+  double* alpha;              // [F][N+1][M_tau] normalised alpha rows
+  double* beta;               // [F][N+1][M_tau] normalised beta rows
+  double* Lacc;               // [F][N][q] un-normalised APP accumulators
+  float* L;                   // [F][N][q] output APP, rows sum to 1
+  double* dbg_gamma;          // debug dump [F][M_tau][M_n][q] (true scale) or nullptr
+  int dbg_i;                  // symbol index of the debug dump
+  int i_base;                 // first symbol index of this launch (blockIdx.y offset)
+  LatticeConst lc;
+};
+
+// 64 received bits starting at bit `s` of frame f (LSB-first); bits at or
+// beyond rho read as 0 (they only feed lattice columns that are masked).
+__device__ __forceinline__ uint64_t load_window(const DecodeParams& p, int f, int s, int rho) {
+  const uint32_t* w = p.rx + p.rx_off[f];
+  const int nwords = (rho + 31) >> 5;
+  const int w0 = s >> 5, sh = s & 31;
+  const uint32_t a = (w0 < nwords) ? __ldg(w + w0) : 0u;
+  const uint32_t b = (w0 + 1 < nwords) ? __ldg(w + w0 + 1) : 0u;
+  const uint32_t c = (w0 + 2 < nwords) ? __ldg(w + w0 + 2) : 0u;
+  const uint32_t lo = __funnelshift_r(a, b, sh);
+  const uint32_t hi = __funnelshift_r(b, c, sh);
+  return (uint64_t)lo | ((uint64_t)hi << 32);
+}
+
+}  // namespace bsidmap

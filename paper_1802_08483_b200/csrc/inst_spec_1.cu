@@ -1,0 +1,3 @@
+// Fully unrolled lattice core for (n, m_n^-, M_n) = (10,-6,14).
+#include "inst.cuh"
+BSIDMAP_SPEC_UNIT(1, 10,-6,14)

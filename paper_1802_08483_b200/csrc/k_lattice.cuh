@@ -1,0 +1,266 @@
+// k_lattice.cuh -- lattice-pass kernels, templated on the lattice core.
+//
+//   k_gamma_sum : a1 (step 1) -- gamma_i(m', m'+k, D) = P(D_i=D) 2^80 F_{n,n+k}
+//                 (eqn:gamma P:156-161), folded over D on the fly into
+//                 Gamma_i(m', k) = sum_D gamma_i (the only thing the alpha
+//                 and beta recursions eqn:alpha/eqn:beta need).  Stored
+//                 variant: also writes every gamma.
+//   k_app       : a4 (step 3) -- recomputes gamma_i (second lattice pass,
+//                 the paper's "computed at least twice") and
+//                 forms sum_{m',m} alpha_i(m') gamma_i(m',m,D) beta_{i+1}(m)
+//                 (eqn:L/eqn:sigma) into FP64 accumulators.
+//   k_app_stored: a4 for the stored variant -- streams gamma from HBM.
+//   k_gamma_dump: debug -- gamma for one i in FP64 at true scale.
+//
+// Grid: blockIdx.y = symbol index i (+ p.i_base), x over the flat lane index
+// g = f M_tau + (m' - m_tau^-) of the chunk's frames; one lane = one window.
+#pragma once
+#include "lattice.cuh"
+
+namespace bsidmap {
+
+constexpr int kLatticeThreads = 128;
+
+struct LaneGeom {
+  int f, mi, mp, s, rho;
+  bool in, active;
+};
+
+__device__ __forceinline__ LaneGeom lane_geom(const DecodeParams& p, int i) {
+  LaneGeom G;
+  const long g = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  G.in = g < (long)p.F * p.Mt;
+  G.f = G.in ? (int)(g / p.Mt) : 0;
+  G.mi = G.in ? (int)(g - (long)G.f * p.Mt) : 0;
+  G.mp = p.mt_lo + G.mi;                 // start drift m'
+  G.s = p.n * i + G.mp;                  // window start n i + m' (eqn:gamma)
+  G.rho = G.in ? p.rho[G.f] : 0;
+  G.active = G.in && p.status[G.f] == kFrameOk && G.s >= 0 && G.s <= G.rho;
+  return G;
+}
+
+// Output k = m_n^- + e is kept iff the window end n(i+1)+m lies in [s, rho]
+// and m = m' + k is a trellis state (reading R5).
+__device__ __forceinline__ bool out_valid(const DecodeParams& p, const LaneGeom& G, int e) {
+  const int k = p.mn_lo + e;
+  const int m = G.mp + k;
+  return G.active && (p.n + k >= 0) && (G.s + p.n + k <= G.rho) && m >= p.mt_lo && m <= p.mt_hi;
+}
+
+template <class Core, bool kStoreGamma>
+__global__ void __launch_bounds__(kLatticeThreads) k_gamma_sum(const DecodeParams p) {
+  constexpr int MN = Core::Mn;
+  extern __shared__ uint32_t s_C[];  // C_i(0..q-1)
+  const int i = blockIdx.y + p.i_base;
+  for (int t = threadIdx.x; t < p.q; t += blockDim.x) s_C[t] = p.C[(size_t)i * p.q + t];
+  __syncthreads();
+
+  const LaneGeom G = lane_geom(p, i);
+  float acc[MN];
+#pragma unroll
+  for (int e = 0; e < MN; e++) acc[e] = 0.f;
+
+  if (__any_sync(0xffffffffu, G.active)) {
+    typename Core::Lane lane;
+    Core::init(lane, G.active ? load_window(p, G.f, G.s, G.rho) : 0ull, p);
+    const float* pri = p.priors ? p.priors + ((size_t)G.f * p.N + i) * p.q : nullptr;
+    float* gout = kStoreGamma ? p.gamma + (((size_t)G.f * p.N + i) * p.q) * MN * p.Mt + G.mi : nullptr;
+    for (int D = 0; D < p.q; D++) {
+      const float P = pri ? __ldg(pri + D) : 1.f;
+      float fo[MN];
+      Core::run(lane, s_C[D], p, fo);
+#pragma unroll
+      for (int e = 0; e < MN; e++) acc[e] = fmaf(P, fo[e], acc[e]);
+      if constexpr (kStoreGamma) {
+        if (G.in) {
+          const float sc = pri ? P : 1.f / p.q;
+#pragma unroll
+          for (int e = 0; e < MN; e++)
+            __stcs(gout + ((size_t)D * MN + e) * p.Mt, out_valid(p, G, e) ? sc * fo[e] : 0.f);
+        }
+      }
+    }
+  } else if constexpr (kStoreGamma) {
+    if (G.in) {
+      float* gout = p.gamma + (((size_t)G.f * p.N + i) * p.q) * MN * p.Mt + G.mi;
+      for (int D = 0; D < p.q; D++)
+#pragma unroll
+        for (int e = 0; e < MN; e++) __stcs(gout + ((size_t)D * MN + e) * p.Mt, 0.f);
+    }
+  }
+  if (G.in) {
+    const float sc = p.priors ? 1.f : 1.f / p.q;
+    float* out = p.Gsum + ((size_t)G.f * p.N + i) * MN * p.Mt + G.mi;
+#pragma unroll
+    for (int e = 0; e < MN; e++) out[(size_t)e * p.Mt] = out_valid(p, G, e) ? sc * acc[e] : 0.f;
+  }
+}
+
+constexpr int kAppDChunk = 64;  // symbols per smem staging round of the APP passes
+
+// Segmented (per frame) reduction of the CTA's per-lane contributions
+// w(lane) * t(D, lane), D in [D0, D0 + nD), into the FP64 accumulators Lacc[f][i][D].
+__device__ __forceinline__ void app_reduce(const DecodeParams& p, int i, int D0, int nD, const double* s_w,
+                                           const float* s_t) {
+  const long g0 = (long)blockIdx.x * blockDim.x;
+  const long gend = min(g0 + (long)blockDim.x, (long)p.F * p.Mt);
+  if (g0 >= gend) return;
+  const int f0 = (int)(g0 / p.Mt), f1 = (int)((gend - 1) / p.Mt);
+  const int items = (f1 - f0 + 1) * nD;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int f = f0 + it / nD, d = it % nD;
+    const int l0 = (int)(max((long)f * p.Mt, g0) - g0);
+    const int l1 = (int)(min((long)(f + 1) * p.Mt, gend) - g0);
+    double s = 0.0;
+    for (int l = l0; l < l1; l++) {
+      const double w = s_w[l];
+      if (w > 0.0) s += w * (double)s_t[d * blockDim.x + l];
+    }
+    if (s > 0.0) atomicAdd(p.Lacc + ((size_t)f * p.N + i) * p.q + D0 + d, s);
+  }
+}
+
+// Per-lane weights of the APP pass: beta_{i+1}(m'+k) rescaled by its max over
+// the corridor (FP32 copy in [0,1]) and w = alpha_i(m') * that max (FP64).
+template <int MN>
+__device__ __forceinline__ double app_weights(const DecodeParams& p, const LaneGeom& G, int i, float (&bt)[MN]) {
+  double bm = 0.0;
+  double bv[MN];
+  const double* brow = p.beta + ((size_t)G.f * (p.N + 1) + (i + 1)) * p.Mt;
+#pragma unroll
+  for (int e = 0; e < MN; e++) {
+    bv[e] = out_valid(p, G, e) ? brow[G.mi + p.mn_lo + e] : 0.0;
+    bm = fmax(bm, bv[e]);
+  }
+  const double inv = bm > 0.0 ? 1.0 / bm : 0.0;
+#pragma unroll
+  for (int e = 0; e < MN; e++) bt[e] = (float)(bv[e] * inv);
+  return G.active ? p.alpha[((size_t)G.f * (p.N + 1) + i) * p.Mt + G.mi] * bm : 0.0;
+}
+
+// smem: s_w[blockDim] (double) | s_t[min(q, kAppDChunk)][blockDim] (float) | s_C[q]
+template <class Core>
+__global__ void __launch_bounds__(kLatticeThreads) k_app(const DecodeParams p) {
+  constexpr int MN = Core::Mn;
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* s_w = reinterpret_cast<double*>(smem);
+  float* s_t = reinterpret_cast<float*>(s_w + blockDim.x);
+  uint32_t* s_C = reinterpret_cast<uint32_t*>(s_t + (size_t)min(p.q, kAppDChunk) * blockDim.x);
+  const int i = blockIdx.y + p.i_base;
+  for (int t = threadIdx.x; t < p.q; t += blockDim.x) s_C[t] = p.C[(size_t)i * p.q + t];
+
+  const LaneGeom G = lane_geom(p, i);
+  float bt[MN];
+  const double w = app_weights<MN>(p, G, i, bt);
+  s_w[threadIdx.x] = w;
+  __syncthreads();
+  const bool warp_live = __any_sync(0xffffffffu, w > 0.0);
+  typename Core::Lane lane;
+  Core::init(lane, G.active ? load_window(p, G.f, G.s, G.rho) : 0ull, p);
+  const float* pri = p.priors ? p.priors + ((size_t)G.f * p.N + i) * p.q : nullptr;
+
+  for (int D0 = 0; D0 < p.q; D0 += kAppDChunk) {
+    const int nD = min(kAppDChunk, p.q - D0);
+    if (warp_live) {
+      for (int d = 0; d < nD; d++) {
+        const float P = pri ? __ldg(pri + D0 + d) : 1.f;
+        float fo[MN];
+        Core::run(lane, s_C[D0 + d], p, fo);
+        // t(m', D) = sum_k gamma_i(m', m'+k, D) beta_{i+1}(m'+k) / bmax  (two chains for ILP)
+        float t0 = 0.f, t1 = 0.f;
+#pragma unroll
+        for (int e = 0; e < MN; e += 2) {
+          t0 = fmaf(fo[e], bt[e], t0);
+          if (e + 1 < MN) t1 = fmaf(fo[e + 1], bt[e + 1], t1);
+        }
+        s_t[d * blockDim.x + threadIdx.x] = P * (t0 + t1);
+      }
+    }
+    __syncthreads();
+    app_reduce(p, i, D0, nD, s_w, s_t);
+    __syncthreads();
+  }
+}
+
+// Stored variant APP: gamma streamed from HBM instead of recomputed.
+// smem: s_w[blockDim] | s_t[kAppDChunk][blockDim]
+template <int MN>
+__global__ void __launch_bounds__(kLatticeThreads) k_app_stored(const DecodeParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* s_w = reinterpret_cast<double*>(smem);
+  float* s_t = reinterpret_cast<float*>(s_w + blockDim.x);
+  const int i = blockIdx.y + p.i_base;
+  const LaneGeom G = lane_geom(p, i);
+  float bt[MN];
+  const double w = app_weights<MN>(p, G, i, bt);
+  s_w[threadIdx.x] = w;
+  const float* gin = p.gamma + (((size_t)G.f * p.N + i) * p.q) * MN * p.Mt + G.mi;
+  for (int D0 = 0; D0 < p.q; D0 += kAppDChunk) {
+    const int nD = min(kAppDChunk, p.q - D0);
+    if (w > 0.0) {
+      for (int d = 0; d < nD; d++) {
+        const float* gd = gin + (size_t)(D0 + d) * MN * p.Mt;
+        float t0 = 0.f, t1 = 0.f;
+#pragma unroll
+        for (int e = 0; e < MN; e += 2) {
+          t0 = fmaf(__ldcs(gd + (size_t)e * p.Mt), bt[e], t0);
+          if (e + 1 < MN) t1 = fmaf(__ldcs(gd + (size_t)(e + 1) * p.Mt), bt[e + 1], t1);
+        }
+        s_t[d * blockDim.x + threadIdx.x] = t0 + t1;  // gamma already carries the prior
+      }
+    }
+    __syncthreads();
+    app_reduce(p, i, D0, nD, s_w, s_t);
+    __syncthreads();
+  }
+}
+
+template <class Core>
+__global__ void __launch_bounds__(kLatticeThreads) k_gamma_dump(const DecodeParams p) {
+  constexpr int MN = Core::Mn;
+  extern __shared__ uint32_t s_C[];
+  const int i = p.dbg_i;
+  for (int t = threadIdx.x; t < p.q; t += blockDim.x) s_C[t] = p.C[(size_t)i * p.q + t];
+  __syncthreads();
+  const LaneGeom G = lane_geom(p, i);
+  if (!G.in) return;
+  typename Core::Lane lane;
+  Core::init(lane, G.active ? load_window(p, G.f, G.s, G.rho) : 0ull, p);
+  const double unscale = ldexp(1.0, -kLatticeSeedLog2);
+  double* out = p.dbg_gamma + ((size_t)G.f * p.Mt + G.mi) * MN * p.q;
+  for (int D = 0; D < p.q; D++) {
+    const double P = p.priors ? (double)p.priors[((size_t)G.f * p.N + i) * p.q + D] : 1.0 / p.q;
+    float fo[MN];
+    Core::run(lane, s_C[D], p, fo);
+#pragma unroll
+    for (int e = 0; e < MN; e++) out[(size_t)e * p.q + D] = out_valid(p, G, e) ? P * (double)fo[e] * unscale : 0.0;
+  }
+}
+
+// Kernel table for one lattice core.
+struct CoreKernels {
+  void (*gamma_sum)(const DecodeParams);
+  void (*gamma_store)(const DecodeParams);
+  void (*app)(const DecodeParams);
+  void (*app_stored)(const DecodeParams);
+  void (*gamma_dump)(const DecodeParams);
+  long nodes;  // corridor nodes per lattice (0 = generic core: computed on host)
+};
+
+template <class Core>
+CoreKernels make_core_kernels(long nodes) {
+  CoreKernels k;
+  k.gamma_sum = k_gamma_sum<Core, false>;
+  k.gamma_store = k_gamma_sum<Core, true>;
+  k.app = k_app<Core>;
+  k.app_stored = k_app_stored<Core::Mn>;
+  k.gamma_dump = k_gamma_dump<Core>;
+  k.nodes = nodes;
+  return k;
+}
+
+// Registry (defined in the instantiation units).
+bool find_spec_kernels(int n, int mn_lo, int Mn, CoreKernels* out);
+bool find_generic_kernels(int Mn, CoreKernels* out);
+
+}  // namespace bsidmap

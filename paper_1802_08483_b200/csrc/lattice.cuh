@@ -1,0 +1,144 @@
+// lattice.cuh -- the corridor-constrained receiver-metric lattice
+// as register-resident FP32 device code for sm_100a.
+//
+// One lattice per (frame, i, m', D) covers the largest window
+// Y[n i + m' .. n(i+1) + m_n^+) and yields F_{n, n+k} for every drift change
+// k in [m_n^-, m_n^+].  Only nodes inside the corridor
+// m_n^- <= j - r <= m_n^+ are kept, so a lattice row is held in
+// "diagonal" coordinates e = (j - r) - m_n^- in M_n registers:
+//
+//   F_{r,j} = 1/2 Pi F_{r,j-1} + Pd F_{r-1,j} + Q(y_j|x_r) F_{r-1,j-1}   (eqn:F, r < n)
+//   F_{n,j} =                    Pd F_{n-1,j} + Q(y_j|x_n) F_{n-1,j-1}   (eqn:F_lastrow)
+//
+// In e-coordinates (r, j-1) is e-1, (r-1, j) is e+1 and (r-1, j-1) is e, so
+// one row is new[e] = a new[e-1] + b old[e+1] + Q old[e]: one FMUL and two
+// FFMAs per node, only the a-term on the serial chain.  Writing new[e] over
+// old[e] is safe because new[e+1] reads old[e+1], old[e+2] only.
+//
+// Lane mapping (B200 design, not the paper's): a lane owns one window
+// (frame, i, m') and loops over the q symbols D.  x = C_i(D) is therefore
+// warp-uniform, so "which Q-dot row" is a uniform branch on bit x_r and the
+// per-lane Q-dot values Q(y_j|1), Q(y_j|0) for the window's columns are
+// precomputed once per window (registers) and reused for all q lattices.
+//
+// Two cores: SpecCore<n, m_n^-, M_n> is fully unrolled (compile-time
+// columns, structurally-zero nodes j < 0 skipped -- exactly the paper's
+// node count n M_n - m_n^-(m_n^- - 1)/2); GenCore<M_n> has runtime
+// n and m_n^- (rows not unrolled, Q-dot from the window bits per node).
+#pragma once
+#include "common.cuh"
+
+namespace bsidmap {
+
+template <int NN, int LO, int MN>
+struct SpecCore {
+  static constexpr int Mn = MN;
+  static constexpr int lo = LO;
+  static constexpr int hi = LO + MN - 1;
+  static constexpr int J = NN + LO + MN - 1;  // last window column n + m_n^+
+  static_assert(MN >= 1 && MN <= kMaxMn, "corridor width");
+  static_assert(LO <= 0 && LO + MN - 1 >= 0, "corridor must contain 0");
+  static_assert(J <= kMaxWindow, "window must fit 64 bits");
+
+  struct Lane {
+    float q1[J + 1];  // Q(y_j | x = 1), j = 1..J
+    float q0[J + 1];  // Q(y_j | x = 0)
+  };
+
+  __device__ __forceinline__ static void init(Lane& L, uint64_t win, const DecodeParams& p) {
+#pragma unroll
+    for (int j = 1; j <= J; j++) {
+      const bool y = (win >> (j - 1)) & 1ull;
+      L.q1[j] = y ? p.lc.qm : p.lc.qs;
+      L.q0[j] = y ? p.lc.qs : p.lc.qm;
+    }
+  }
+
+  template <int R>
+  __device__ __forceinline__ static void row(float (&f)[MN], const float (&Q)[J + 1], const LatticeConst& lc) {
+    constexpr bool kLast = (R == NN);
+    float prev = 0.f;
+#pragma unroll
+    for (int e = 0; e < MN; e++) {
+      const int j = R + LO + e;  // lattice column of this node
+      if (j < 0) continue;       // left of column 0: structurally zero, stays 0
+      float v;
+      if (j == 0) {
+        v = (e + 1 < MN) ? lc.b * f[e + 1] : 0.f;  // column 0 is reached by deletions only
+      } else {
+        float u;
+        if (e + 1 < MN) {
+          u = lc.b * f[e + 1];          // deletion   Pd F_{r-1,j}
+          u = fmaf(Q[j], f[e], u);      // transmission Q F_{r-1,j-1}
+        } else {
+          u = Q[j] * f[e];
+        }
+        v = (!kLast && e > 0) ? fmaf(lc.a, prev, u) : u;  // insertion 1/2 Pi F_{r,j-1}
+      }
+      f[e] = v;
+      prev = v;
+    }
+  }
+
+  template <int R>
+  __device__ __forceinline__ static void rows(float (&f)[MN], uint32_t x, const Lane& L, const LatticeConst& lc) {
+    if constexpr (R <= NN) {
+      if ((x >> (R - 1)) & 1u)
+        row<R>(f, L.q1, lc);
+      else
+        row<R>(f, L.q0, lc);
+      rows<R + 1>(f, x, L, lc);
+    }
+  }
+
+  // f[e] <- 2^80 F_{n, n + m_n^- + e}
+  __device__ __forceinline__ static void run(const Lane& L, uint32_t x, const DecodeParams& p, float (&f)[MN]) {
+#pragma unroll
+    for (int e = 0; e < MN; e++) f[e] = p.lc.row0[e];  // F_{0,j}: host zeroes j < 0
+    rows<1>(f, x, L, p.lc);
+  }
+
+  static constexpr long nodes() {  // corridor nodes per lattice
+    return (long)NN * MN - (long)LO * (LO - 1) / 2;
+  }
+};
+
+template <int MN>
+struct GenCore {
+  static constexpr int Mn = MN;
+  struct Lane {
+    uint64_t win;
+  };
+  __device__ __forceinline__ static void init(Lane& L, uint64_t win, const DecodeParams&) { L.win = win; }
+
+  __device__ __forceinline__ static void run(const Lane& L, uint32_t x, const DecodeParams& p, float (&f)[MN]) {
+    const LatticeConst& lc = p.lc;
+#pragma unroll
+    for (int e = 0; e < MN; e++) f[e] = lc.row0[e];
+    const int n = p.n;
+    for (int r = 1; r <= n; r++) {
+      const bool last = (r == n);
+      const uint32_t xr = (x >> (r - 1)) & 1u;
+      const int j0 = r + p.mn_lo;
+      float prev = 0.f;
+#pragma unroll
+      for (int e = 0; e < MN; e++) {
+        const int j = j0 + e;
+        float v = 0.f;
+        if (j >= 0) {
+          float u = (e + 1 < MN) ? lc.b * f[e + 1] : 0.f;
+          if (j >= 1) {
+            const uint32_t yb = (uint32_t)(L.win >> (j - 1)) & 1u;
+            u = fmaf((yb == xr) ? lc.qm : lc.qs, f[e], u);
+            if (!last && e > 0) u = fmaf(lc.a, prev, u);
+          }
+          v = u;
+        }
+        f[e] = v;
+        prev = v;
+      }
+    }
+  }
+};
+
+}  // namespace bsidmap
