@@ -1,0 +1,340 @@
+#!/usr/bin/env python
+"""Benchmark of the batched BSID MAP decoder (arXiv 1802.08483) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--mode auto|stored|recompute]
+    python bench.py --impl reference ...      # the FP64 CPU oracle as the reference arm
+
+One "step" = one decode_batch of the whole hot path (frame status -> lattice pass 1
+-> alpha/beta -> lattice pass 2 (APP) -> normalisation) over the rank's frames.
+Default workload: BASELINE.json configs[1] = C2 (q=16, n=10, N=100, Pi=Pd=0.01,
+Ps=0.001), 65536 frames per GPU (weak scaling over ranks; frames are sharded with
+no data-path collective).  Inputs are resident in HBM before timing; L2 is flushed
+(256 MiB write) between timed steps, outside the per-step CUDA events.
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import bsidgen  # noqa: E402
+
+FP32_LANES_PER_SM = 128  # Blackwell SM: 4 SMSPs x 32 FP32 lanes
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--frames", type=int, default=None, help="frames per GPU (default: the config's batch)")
+    ap.add_argument("--mode", default="auto", choices=["auto", "stored", "recompute"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the oracle sample")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi samples every 200 ms while the timed region runs."""
+    FIELDS = ["index", "clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=5)
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+# --------------------------------------------------------------------------- oracle leg
+
+def oracle_sample(cfg, target_seconds, first=10_000_000, max_frames=4096):
+    """Time the FP64 oracle (as it stands) on host cores over a bounded sample of the workload."""
+    import oracle
+    threads = os.cpu_count() or 1
+    prob = oracle.Problem(cfg.q, cfg.n, cfg.N, bsidgen.codebook(cfg), cfg.Pi, cfg.Pd, cfg.Ps, cfg.mn, cfg.mt)
+    probe = min(threads, max_frames)
+    b = bsidgen.make_batch(cfg, first, probe, C=prob.C)
+    t0 = time.perf_counter()
+    oracle.decode_many(prob, [b.bits(f) for f in range(probe)],
+                       [b.priors[f].astype(np.float64) if b.priors is not None else None for f in range(probe)],
+                       threads)
+    dt = time.perf_counter() - t0
+    per_wall = dt / probe
+    count = int(max(probe, min(max_frames, target_seconds / max(per_wall, 1e-9))))
+    count = max(threads, (count // threads) * threads)
+    return prob, count, per_wall, threads
+
+
+def run_oracle_frames(cfg, prob, first, count, threads):
+    import oracle
+    b = bsidgen.make_batch(cfg, first, count, C=prob.C)
+    ys = [b.bits(f) for f in range(count)]
+    pl = [b.priors[f].astype(np.float64) if b.priors is not None else None for f in range(count)]
+    t0 = time.perf_counter()
+    oracle.decode_many(prob, ys, pl, threads)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, target_seconds):
+    prob, count, _, threads = oracle_sample(cfg, target_seconds)
+    dt = run_oracle_frames(cfg, prob, 20_000_000, count, threads)
+    return {"value": count / dt, "unit": "frames/s", "cores": threads, "kind": "oracle",
+            "sample": f"{count} frames of {cfg.name} (global frame indices 20000000..), FP64 C oracle, "
+                      f"{threads} host threads over frames, {dt:.1f} s"}
+
+
+def reference_arm(args, cfg):
+    from paper_1802_08483_b200.sharding import dist_env
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    per_step = max(2.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    prob, count, _, threads = oracle_sample(cfg, per_step)
+    for w in range(args.warmup):
+        run_oracle_frames(cfg, prob, 30_000_000 + w * count, count, threads)
+    times = [run_oracle_frames(cfg, prob, 40_000_000 + s * count, count, threads) for s in range(args.steps)]
+    total = sum(times)
+    value = count * args.steps / total
+    line = {
+        "impl": "reference", "metric": "frames/s", "value": value, "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": describe(cfg), "frames_per_step": count, "sample": "bounded oracle sample"},
+        "symbols_per_s": value * cfg.N,
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "oracle",
+                         "sample": f"{count} frames x {args.steps} steps of {cfg.name}, FP64 C oracle on "
+                                   f"{threads} host threads"},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def describe(cfg):
+    return (f"{cfg.name}: q={cfg.q} n={cfg.n} N={cfg.N} Pi={cfg.Pi} Pd={cfg.Pd} Ps={cfg.Ps} "
+            f"m_n=[{cfg.mn[0]},{cfg.mn[1]}] m_tau=[{cfg.mt[0]},{cfg.mt[1]}] "
+            f"priors={'non-uniform' if cfg.priors else 'uniform'}")
+
+
+# ------------------------------------------------------------------------------ our arm
+
+def main():
+    args = parse()
+    cfg = bsidgen.configs()[args.config]
+    if args.impl == "reference":
+        return reference_arm(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1802_08483_b200 import Decoder, MODE_AUTO, MODE_RECOMPUTE, MODE_STORED
+    from paper_1802_08483_b200.sharding import barrier, dist_env, frame_range, max_over_ranks, sum_over_ranks
+
+    rank, world, local = dist_env()
+    if world != args.gpus and rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    frames = args.frames or cfg.frames
+    first, count = frame_range(rank, world, frames)
+    b = bsidgen.make_batch(cfg, first, count)
+    mode = {"auto": MODE_AUTO, "stored": MODE_STORED, "recompute": MODE_RECOMPUTE}[args.mode]
+    d = Decoder.from_config(cfg, b.C, mode=mode, device=local)
+    rx = torch.from_numpy(b.rx.ravel().copy()).to(dev)
+    off = torch.from_numpy(b.offsets).to(dev)
+    rho = torch.from_numpy(b.rho).to(dev)
+    pri = torch.from_numpy(b.priors).to(dev) if b.priors is not None else None
+    L = torch.empty((count, cfg.N, cfg.q), dtype=torch.float32, device=dev)
+    st = torch.empty((count,), dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    plan = d.plan(count)
+
+    d.set_timing(True)
+    for _ in range(args.warmup):
+        d.decode_batch(rx, off, rho, pri, L, st, stream)
+    torch.cuda.synchronize(dev)
+
+    nodes = d.lattice_nodes()
+    lattices = d.valid_lattices(b.rho)          # windows with 0 <= n i + m' <= rho, per lattice pass
+    flops_per_lattice = 5 * nodes - cfg.Mn       # P:857 node count; 3 mul + 2 add per node, last row 3 flops
+    flops_pass = lattices * flops_per_lattice
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    phases, launches = [], 0
+    clocks = ClockSampler(local)
+    barrier(dev)
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    for s in range(args.steps):
+        flush.zero_()
+        ev[s][0].record(stream)
+        d.decode_batch(rx, off, rho, pri, L, st, stream)
+        ev[s][1].record(stream)
+        phases.append(d.phase_times())   # synchronises the stream (per-step device timing only)
+        launches += d.last_launch_count()
+    torch.cuda.synchronize(dev)
+    barrier(dev)
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(bb) for a, bb in ev]
+    local_ms = sum(step_ms)
+    max_ms = max_over_ranks(local_ms, dev)
+    total_frames = sum_over_ranks(count * args.steps, dev)
+    value = total_frames / (max_ms / 1e3)
+
+    # roofline of the dominant kernel: lattice pass 1 vs pass 2, whichever takes longer on average
+    ph = np.array(phases)  # [steps][5]
+    mean_ph = ph.mean(0)
+    dominant = 1 if mean_ph[1] >= mean_ph[3] else 3
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak_tf = sms * FP32_LANES_PER_SM * 2 * 1965e6 / 1e12
+    achieved = flops_pass / (mean_ph[dominant] / 1e3) / 1e12
+    stored = plan["mode"] == "stored"
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(cfg.name, {}).get(
+                "lattice_pass1" if dominant == 1 else "lattice_pass2", {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # end-to-end through the host-buffer C-ABI entry (pinned buffers, copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        h_rx = torch.from_numpy(b.rx.ravel().copy()).pin_memory()
+        h_off = torch.from_numpy(b.offsets).pin_memory()
+        h_rho = torch.from_numpy(b.rho).pin_memory()
+        h_pri = torch.from_numpy(b.priors).pin_memory() if b.priors is not None else None
+        h_L = torch.empty((count, cfg.N, cfg.q), dtype=torch.float32).pin_memory()
+        h_st = torch.empty((count,), dtype=torch.int32).pin_memory()
+        d.set_timing(False)
+        d.decode_host(h_rx, h_off, h_rho, h_pri, h_L, h_st, stream)  # warm the staging buffers
+        barrier(dev)
+        torch.cuda.synchronize(dev)
+        t_e2e = []
+        for s in range(max(1, min(args.steps, 5))):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            d.decode_host(h_rx, h_off, h_rho, h_pri, h_L, h_st, stream)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            t_e2e.append(e0.elapsed_time(e1))
+        e_ms = max_over_ranks(sum(t_e2e), dev)
+        e_frames = sum_over_ranks(count * len(t_e2e), dev)
+        h2d = h_rx.numel() * 4 + h_off.numel() * 8 + h_rho.numel() * 4 + (h_pri.numel() * 4 if h_pri is not None else 0)
+        d2h = h_L.numel() * 4 + h_st.numel() * 4
+        e2e = {"value": e_frames / (e_ms / 1e3), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h)}
+        ok = (h_st.numpy() == 0).mean()
+        if ok < 0.999 and rank == 0:
+            print(f"warning: only {ok:.4f} of frames decoded OK in e2e", file=sys.stderr)
+
+    st_h = st.cpu().numpy()
+    ser = float((np.argmax(L.cpu().numpy(), 2) != b.msg).mean())
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            cpu = cpu_baseline(cfg, args.cpu_seconds)
+        line = {
+            "metric": "frames/s", "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "dtype_detail": "FP32 lattice (receiver metric, P:272-275); FP64 alpha/beta and APP accumulation",
+            "data": "synthetic",
+            "config": {"workload": describe(cfg), "frames_per_gpu": count, "mode": plan["mode"],
+                       "core": plan["core"], "chunks": plan["chunks"], "parallelism": f"frames sharded x{world}",
+                       "l2": "flushed (256 MiB write) between timed steps; per-step working set > L2"},
+            "symbols_per_s": value * cfg.N,
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tf, "traffic": traffic,
+                         "kernel": "lattice pass 1 (k_gamma_sum)" if dominant == 1 else "lattice pass 2 (k_app)",
+                         "peak_basis": f"{sms} SMs x 128 FP32 lanes x 2 flop x 1965 MHz (max SM clock); "
+                                       "derived, MEASURED_PEAKS.json has no FP32 entry",
+                         "flops_per_launch": flops_pass, "launch_ms": float(mean_ph[dominant])},
+            "phase_ms": {"init": float(mean_ph[0]), "lattice_pass1": float(mean_ph[1]),
+                         "alpha_beta": float(mean_ph[2]), "lattice_pass2": float(mean_ph[3]),
+                         "finalize": float(mean_ph[4])},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "frames_ok": float((st_h == 0).mean()),
+            "symbol_error_rate": ser,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -15,12 +15,13 @@
 #include <vector>
 
 #include "../../include/bsidmap.h"
-#include "k_lattice.cuh"
+#include "k_lattice_x2.cuh"
 
 namespace bsidmap {
 __global__ void k_frame_init(const DecodeParams p);
 __global__ void k_alpha_beta(const DecodeParams p);
 __global__ void k_finalize(const DecodeParams p);
+__global__ void k_zero_failed(const DecodeParams p);
 }  // namespace bsidmap
 
 using namespace bsidmap;
@@ -91,6 +92,8 @@ struct Plan {
   int nchunks;
   int ab_threads;   // k_alpha_beta block size
   size_t ab_smem, app_smem, l1_smem;
+  void (*ab_warp)(const DecodeParams);  // warp-per-task alpha/beta kernel or nullptr
+  bool direct_L;                         // APP pass writes normalised L rows itself
 };
 
 size_t budget(const bsidmap_decoder* d) {
@@ -121,8 +124,19 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   P->nchunks = (int)((F + chunk - 1) / chunk);
   P->ab_threads = std::min(1024, ((d->Mt + 31) / 32) * 32);
   P->ab_smem = (2 * (size_t)d->Mt + 33) * sizeof(double);
-  P->app_smem = kLatticeThreads * sizeof(double) + (size_t)std::min(d->q, kAppDChunk) * kLatticeThreads * 4 +
-                (size_t)d->q * 4;
+  P->ab_warp = nullptr;
+  const int spt = (d->Mt + 31) / 32;
+  if (d->kern.ab_warp[0] && spt <= 4) {
+    const int k = spt == 1 ? 0 : spt == 2 ? 1 : 2;
+    P->ab_warp = d->kern.ab_warp[k];
+    P->ab_smem = (size_t)(kAbWarpThreads / 32) * (spt == 3 ? 4 : spt) * 32 * sizeof(double);
+  }
+  const size_t nwin = kLatticeThreads;
+  P->app_smem = nwin * sizeof(double) + (size_t)kAppSegCap * std::min(d->q, kAppDChunk) * sizeof(double) +
+                nwin * app_tstride(d->q) * 4 + (size_t)d->q * 4;
+  if (mode != BSIDMAP_MODE_STORED && d->kern.W == 2) P->app_smem = (size_t)d->q * 4 * (1 + kX2Warps);
+  // packed-pair APP with one tile per frame writes L directly (no accumulators / finalize)
+  P->direct_L = mode != BSIDMAP_MODE_STORED && d->kern.W == 2 && tiles_per_frame(d->Mt) == 1;
   P->l1_smem = (size_t)d->q * 4;
   return BSIDMAP_OK;
 }
@@ -185,33 +199,47 @@ void for_i_slices(int N, Fn fn) {
 
 int run_chunk(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s, bool first_chunk, bool last_chunk) {
   const long lanes = (long)p.F * d->Mt;
-  const unsigned gx = (unsigned)((lanes + kLatticeThreads - 1) / kLatticeThreads);
+  const bool tiled = d->kern.W == 2;
+  // packed-pair kernels: 4 frame-aligned 64-slot warp tiles per CTA; scalar kernels: 128 flat windows per CTA
+  const unsigned gx_tile = (unsigned)(((long)p.F * tiles_per_frame(d->Mt) + kX2Warps - 1) / kX2Warps);
+  const unsigned gx_flat = (unsigned)((lanes + kLatticeThreads - 1) / kLatticeThreads);
+  const unsigned gx = tiled ? gx_tile : gx_flat;
   if (first_chunk) record(d, 0, s);
   k_frame_init<<<(p.F + 255) / 256, 256, 0, s>>>(p);
-  cudaMemsetAsync(p.Lacc, 0, (size_t)p.F * d->N * d->q * sizeof(double), s);
   d->launches += 1;
+  if (!P.direct_L) cudaMemsetAsync(p.Lacc, 0, (size_t)p.F * d->N * d->q * sizeof(double), s);
   if (first_chunk) record(d, 1, s);
   auto l1 = P.mode == BSIDMAP_MODE_STORED ? d->kern.gamma_store : d->kern.gamma_sum;
   for_i_slices(d->N, [&](int i0, int ni) {
     p.i_base = i0;
-    l1<<<dim3(gx, ni), kLatticeThreads, P.l1_smem, s>>>(p);
+    l1<<<dim3(tiled ? (unsigned)((lanes + 2 * kLatticeThreads - 1) / (2 * kLatticeThreads)) : gx_flat, ni),
+         kLatticeThreads, P.l1_smem, s>>>(p);
     d->launches++;
   });
   p.i_base = 0;
   if (first_chunk) record(d, 2, s);
-  k_alpha_beta<<<dim3(p.F, 2), P.ab_threads, P.ab_smem, s>>>(p);
+  if (P.ab_warp) {
+    const long tasks = 2L * p.F, per = kAbWarpThreads / 32;
+    P.ab_warp<<<(unsigned)((tasks + per - 1) / per), kAbWarpThreads, P.ab_smem, s>>>(p);
+  } else {
+    k_alpha_beta<<<dim3(p.F, 2), P.ab_threads, P.ab_smem, s>>>(p);
+  }
   d->launches++;
   if (first_chunk) record(d, 3, s);
   auto l2 = P.mode == BSIDMAP_MODE_STORED ? d->kern.app_stored : d->kern.app;
   for_i_slices(d->N, [&](int i0, int ni) {
     p.i_base = i0;
-    l2<<<dim3(gx, ni), kLatticeThreads, P.app_smem, s>>>(p);
+    l2<<<dim3(P.mode == BSIDMAP_MODE_STORED ? gx_flat : gx, ni), kLatticeThreads, P.app_smem, s>>>(p);
     d->launches++;
   });
   p.i_base = 0;
   if (first_chunk) record(d, 4, s);
-  const long rows = (long)p.F * d->N;
-  k_finalize<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(p);
+  if (!P.direct_L) {
+    const long rows = (long)p.F * d->N;
+    k_finalize<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(p);
+    d->launches++;
+  }
+  k_zero_failed<<<p.F, 256, 0, s>>>(p);
   d->launches++;
   if (last_chunk) record(d, 5, s);
   cudaError_t e = cudaGetLastError();
@@ -266,17 +294,25 @@ int bsidmap_create(bsidmap_decoder** out, int q, int n, int N, const uint32_t* c
   d->mt_lo = mt_lo; d->mt_hi = mt_hi; d->Mt = mt_hi - mt_lo + 1;
   d->Pi = Pi; d->Pd = Pd; d->Ps = Ps;
   d->mode = mode;
-  // lattice constants (eqn:F, Q-dot); row 0 = insertions only, F_{0,j} = 2^80 (Pi/2)^j
+  // lattice constants (eqn:F, Q-dot); row 0 = insertions only, F_{0,j} = 2^s (Pi/2)^j
   const double Pt = 1.0 - Pi - Pd;
+  // G = F / Pd^r grows by at most Pd^-n over the lattice: keep 2^s Pd^-n q M_n below FLT_MAX / 2^10
+  const double grow = Pd > 0 ? n * std::log2(1.0 / Pd) : 1e9;
+  const bool rescaled = Pd > 0 && grow <= 90.0;
+  int seed = kLatticeSeedMaxLog2;
+  if (rescaled) seed = std::min(seed, (int)std::floor(118.0 - grow - std::log2((double)q) - std::log2((double)Mn)));
+  d->lc.rescaled = rescaled ? 1 : 0;
+  d->lc.seed_log2 = seed;
   d->lc.a = (float)(0.5 * Pi);
-  d->lc.b = (float)Pd;
-  d->lc.qm = (float)(Pt * (1.0 - Ps));
-  d->lc.qs = (float)(Pt * Ps);
+  d->lc.b = rescaled ? 1.0f : (float)Pd;
+  d->lc.qm = (float)(Pt * (1.0 - Ps) / (rescaled ? Pd : 1.0));
+  d->lc.qs = (float)(Pt * Ps / (rescaled ? Pd : 1.0));
+  d->lc.out_scale = std::ldexp(rescaled ? std::pow(Pd, n) : 1.0, -seed);
   for (int e = 0; e < kMaxMn; e++) {
     const int j = mn_lo + e;
-    d->lc.row0[e] = (e < Mn && j >= 0) ? (float)std::ldexp(std::pow(0.5 * Pi, j), kLatticeSeedLog2) : 0.f;
+    d->lc.row0[e] = (e < Mn && j >= 0) ? (float)std::ldexp(std::pow(0.5 * Pi, j), seed) : 0.f;
   }
-  d->spec = find_spec_kernels(n, mn_lo, Mn, &d->kern);
+  d->spec = rescaled && find_spec_kernels(n, mn_lo, Mn, &d->kern);
   if (!d->spec && !find_generic_kernels(Mn, &d->kern)) {
     delete d;
     return fail(nullptr, BSIDMAP_EPLAN, "no lattice core for M_n = " + std::to_string(Mn));
@@ -307,7 +343,7 @@ int bsidmap_decode_batch(bsidmap_decoder* d, int F, const uint32_t* rx, const in
   if ((rc = make_plan(d, F, &P))) return rc;
   const Layout l = layout(d, P.chunk, P.mode);
   if ((rc = ensure_ws(d, l.total))) return rc;
-  if ((rc = set_smem(d, (const void*)k_alpha_beta, P.ab_smem))) return rc;
+  if ((rc = set_smem(d, P.ab_warp ? (const void*)P.ab_warp : (const void*)k_alpha_beta, P.ab_smem))) return rc;
   if ((rc = set_smem(d, (const void*)(P.mode == BSIDMAP_MODE_STORED ? d->kern.app_stored : d->kern.app), P.app_smem)))
     return rc;
   for (int c = 0; c < P.nchunks; c++) {
@@ -442,10 +478,12 @@ int bsidmap_plan_info(bsidmap_decoder* d, int F, char* buf, size_t len) {
       buf, len,
       "{\"mode\": \"%s\", \"frames\": %d, \"chunk\": %d, \"chunks\": %d, \"core\": \"%s\", "
       "\"lattice_grid\": [%ld, %d], \"lattice_block\": %d, \"alpha_beta_grid\": [%d, 2], \"alpha_beta_block\": %d, "
-      "\"workspace_bytes\": %zu, \"q\": %d, \"n\": %d, \"N\": %d, \"Mn\": %d, \"Mtau\": %d}",
+      "\"workspace_bytes\": %zu, \"windows_per_lane\": %d, \"q\": %d, \"n\": %d, \"N\": %d, \"Mn\": %d, \"Mtau\": %d}",
       P.mode == BSIDMAP_MODE_STORED ? "stored" : "recompute", F, P.chunk, P.nchunks, d->spec ? "spec" : "generic",
-      (lanes + kLatticeThreads - 1) / kLatticeThreads, d->N, kLatticeThreads, P.chunk, P.ab_threads,
-      layout(d, P.chunk, P.mode).total, d->q, d->n, d->N, d->Mn, d->Mt);
+      d->kern.W == 2 ? ((long)P.chunk * tiles_per_frame(d->Mt) + kX2Warps - 1) / kX2Warps
+                     : (lanes + kLatticeThreads - 1) / kLatticeThreads,
+      d->N, kLatticeThreads, P.chunk, P.ab_warp ? kAbWarpThreads : P.ab_threads,
+      layout(d, P.chunk, P.mode).total, d->kern.W, d->q, d->n, d->N, d->Mn, d->Mt);
   return nb;
 }
 
@@ -483,8 +521,9 @@ int bsidmap_debug_gamma(bsidmap_decoder* d, int F, const uint32_t* rx, const int
   p.F = F; p.rx = rx; p.rx_off = off; p.rho = rho; p.priors = priors; p.status = st;
   p.dbg_gamma = gamma_out; p.dbg_i = i;
   k_frame_init<<<(F + 255) / 256, 256, 0, s>>>(p);
-  const long lanes = (long)F * d->Mt;
-  d->kern.gamma_dump<<<(unsigned)((lanes + kLatticeThreads - 1) / kLatticeThreads), kLatticeThreads, d->q * 4, s>>>(p);
+  const unsigned gx = d->kern.W == 2 ? (unsigned)(((long)F * tiles_per_frame(d->Mt) + kX2Warps - 1) / kX2Warps)
+                                     : (unsigned)(((long)F * d->Mt + kLatticeThreads - 1) / kLatticeThreads);
+  d->kern.gamma_dump<<<gx, kLatticeThreads, d->q * 4, s>>>(p);
   e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   cudaFree(st);

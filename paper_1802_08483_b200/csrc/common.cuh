@@ -11,17 +11,27 @@ namespace bsidmap {
 
 constexpr int kMaxMn = 32;        // corridor width held in registers
 constexpr int kMaxWindow = 64;    // n + m_n^+ received bits per lattice window
-constexpr int kLatticeSeedLog2 = 80;  // F_{0,0} = 2^80: exact range extension of the FP32 lattice
+constexpr int kLatticeSeedMaxLog2 = 80;  // F_{0,0} = 2^s, s <= 80: exact range extension of the FP32 lattice
 
 enum FrameStatus : int32_t { kFrameOk = 0, kFrameDriftOutOfRange = 1, kFrameUnderflow = 2 };
 
 // Channel constants of the FP32 lattice (eqn:F, eqn:F_lastrow, Q-dot P:207-215).
+//
+// rescaled = 1 (Pd > 0): the kernels run G_{r,j} = F_{r,j} / Pd^r, an exact
+// rescaling under which eqn:F becomes
+//     G_{r,j} = 1/2 Pi G_{r,j-1} + G_{r-1,j} + (Q/Pd) G_{r-1,j-1}
+// -- two FFMAs per node instead of FMUL + 2 FFMA.  Every lattice output then
+// carries the same factor Pd^-n 2^s, which cancels in the alpha/beta and APP
+// normalisations; out_scale undoes it for debug dumps.
 struct LatticeConst {
   float a;                 // 1/2 Pi   (insertion of a matching random bit)
-  float b;                 // Pd       (deletion)
-  float qm;                // Pt (1 - Ps)  Q-dot for y == x
-  float qs;                // Pt Ps        Q-dot for y != x
-  float row0[kMaxMn];      // row 0 of the lattice, F_{0,j} = 2^80 (1/2 Pi)^j, indexed by e = j - m_n^-
+  float b;                 // Pd       (deletion; 1 when rescaled)
+  float qm;                // Pt (1 - Ps)  Q-dot for y == x   (divided by Pd when rescaled)
+  float qs;                // Pt Ps        Q-dot for y != x   (divided by Pd when rescaled)
+  int rescaled;            // 1: G = F / Pd^r recursion, 0: plain eqn:F
+  int seed_log2;           // F_{0,0} = 2^seed_log2
+  double out_scale;        // true metric = out_scale * lattice output
+  float row0[kMaxMn];      // row 0 of the lattice, F_{0,j} = 2^s (1/2 Pi)^j, indexed by e = j - m_n^-
 };
 
 // Everything one decode launch needs, passed by value (lives in the constant bank).

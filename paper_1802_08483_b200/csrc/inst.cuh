@@ -1,13 +1,13 @@
 // inst.cuh -- explicit instantiation helpers (split over compilation units so
 // nvcc compiles the unrolled lattice cores in parallel).
 #pragma once
-#include "k_lattice.cuh"
+#include "k_lattice_x2.cuh"
 
 #define BSIDMAP_SPEC_UNIT(IDX, NN, LO, MN)                                               \
   namespace bsidmap {                                                                    \
   bool spec_unit_##IDX(int n, int lo, int Mn, CoreKernels* out) {                        \
     if (n != NN || lo != LO || Mn != MN) return false;                                   \
-    *out = make_core_kernels<SpecCore<NN, LO, MN>>(SpecCore<NN, LO, MN>::nodes());       \
+    *out = make_core_kernels_x2<SpecCoreX2<NN, LO, MN>>(SpecCoreX2<NN, LO, MN>::nodes()); \
     return true;                                                                         \
   }                                                                                      \
   }

@@ -16,19 +16,24 @@
 // g = f M_tau + (m' - m_tau^-) of the chunk's frames; one lane = one window.
 #pragma once
 #include "lattice.cuh"
+#include "lattice_x2.cuh"
+#include "k_alphabeta_warp.cuh"
 
 namespace bsidmap {
 
 constexpr int kLatticeThreads = 128;
+#ifndef BSIDMAP_LATTICE_MIN_BLOCKS
+#define BSIDMAP_LATTICE_MIN_BLOCKS 4
+#endif
+constexpr int kLatticeMinBlocks = BSIDMAP_LATTICE_MIN_BLOCKS;  // resident CTAs per SM the register budget must allow
 
 struct LaneGeom {
   int f, mi, mp, s, rho;
   bool in, active;
 };
 
-__device__ __forceinline__ LaneGeom lane_geom(const DecodeParams& p, int i) {
+__device__ __forceinline__ LaneGeom lane_geom_at(const DecodeParams& p, int i, long g) {
   LaneGeom G;
-  const long g = (long)blockIdx.x * blockDim.x + threadIdx.x;
   G.in = g < (long)p.F * p.Mt;
   G.f = G.in ? (int)(g / p.Mt) : 0;
   G.mi = G.in ? (int)(g - (long)G.f * p.Mt) : 0;
@@ -37,6 +42,10 @@ __device__ __forceinline__ LaneGeom lane_geom(const DecodeParams& p, int i) {
   G.rho = G.in ? p.rho[G.f] : 0;
   G.active = G.in && p.status[G.f] == kFrameOk && G.s >= 0 && G.s <= G.rho;
   return G;
+}
+
+__device__ __forceinline__ LaneGeom lane_geom(const DecodeParams& p, int i) {
+  return lane_geom_at(p, i, (long)blockIdx.x * blockDim.x + threadIdx.x);
 }
 
 // Output k = m_n^- + e is kept iff the window end n(i+1)+m lies in [s, rho]
@@ -48,7 +57,7 @@ __device__ __forceinline__ bool out_valid(const DecodeParams& p, const LaneGeom&
 }
 
 template <class Core, bool kStoreGamma>
-__global__ void __launch_bounds__(kLatticeThreads) k_gamma_sum(const DecodeParams p) {
+__global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_sum(const DecodeParams p) {
   constexpr int MN = Core::Mn;
   extern __shared__ uint32_t s_C[];  // C_i(0..q-1)
   const int i = blockIdx.y + p.i_base;
@@ -98,25 +107,60 @@ __global__ void __launch_bounds__(kLatticeThreads) k_gamma_sum(const DecodeParam
 
 constexpr int kAppDChunk = 64;  // symbols per smem staging round of the APP passes
 
-// Segmented (per frame) reduction of the CTA's per-lane contributions
-// w(lane) * t(D, lane), D in [D0, D0 + nD), into the FP64 accumulators Lacc[f][i][D].
+constexpr int kAppSegCap = 8;  // frame segments per CTA combined in shared memory before the global atomics
+
+__host__ __device__ __forceinline__ int app_tstride(int q) { return (q < kAppDChunk ? q : kAppDChunk) + 1; }
+
+// Segmented (per frame) reduction of the CTA's contributions w(l) * t(l, D) into
+// the FP64 accumulators Lacc[f][i][D], D in [D0, D0 + nD).  s_t[l * ts + d] holds
+// window l's t for symbol D0 + d (odd stride ts: conflict-free).  Level 1: every
+// thread sums a contiguous chunk of 16 windows for one d, splitting at frame
+// boundaries, into s_part (FP64 smem atomics); level 2: one global atomic per
+// (frame segment, d).  Contains __syncthreads: every thread of the CTA calls it.
 __device__ __forceinline__ void app_reduce(const DecodeParams& p, int i, int D0, int nD, const double* s_w,
-                                           const float* s_t) {
-  const long g0 = (long)blockIdx.x * blockDim.x;
-  const long gend = min(g0 + (long)blockDim.x, (long)p.F * p.Mt);
-  if (g0 >= gend) return;
+                                           const float* s_t, int ts, long g0, int nwin, double* s_part) {
+  constexpr int CH = 16;
+  const long gend = min(g0 + (long)nwin, (long)p.F * p.Mt);
+  if (g0 >= gend) return;  // uniform over the CTA
+  const int nvalid = (int)(gend - g0);
   const int f0 = (int)(g0 / p.Mt), f1 = (int)((gend - 1) / p.Mt);
-  const int items = (f1 - f0 + 1) * nD;
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int f = f0 + it / nD, d = it % nD;
-    const int l0 = (int)(max((long)f * p.Mt, g0) - g0);
-    const int l1 = (int)(min((long)(f + 1) * p.Mt, gend) - g0);
+  const int nseg = f1 - f0 + 1;
+  const bool use_smem = nseg <= kAppSegCap;
+  if (use_smem) {
+    for (int t = threadIdx.x; t < nseg * nD; t += blockDim.x) s_part[t] = 0.0;
+    __syncthreads();
+  }
+  const int nch = (nvalid + CH - 1) / CH;
+  for (int it = threadIdx.x; it < nch * nD; it += blockDim.x) {
+    const int d = it % nD, c = it / nD;
+    const int l0 = c * CH, l1 = min(l0 + CH, nvalid);
+    int f = (int)((g0 + l0) / p.Mt);
+    int bnd = (int)((long)(f + 1) * p.Mt - g0);  // local index of the next frame's first window
     double s = 0.0;
     for (int l = l0; l < l1; l++) {
+      if (l == bnd) {
+        if (s > 0.0) {
+          if (use_smem) atomicAdd(s_part + (f - f0) * nD + d, s);
+          else atomicAdd(p.Lacc + ((size_t)f * p.N + i) * p.q + D0 + d, s);
+        }
+        s = 0.0;
+        f++;
+        bnd += p.Mt;
+      }
       const double w = s_w[l];
-      if (w > 0.0) s += w * (double)s_t[d * blockDim.x + l];
+      if (w > 0.0) s += w * (double)s_t[l * ts + d];
     }
-    if (s > 0.0) atomicAdd(p.Lacc + ((size_t)f * p.N + i) * p.q + D0 + d, s);
+    if (s > 0.0) {
+      if (use_smem) atomicAdd(s_part + (f - f0) * nD + d, s);
+      else atomicAdd(p.Lacc + ((size_t)f * p.N + i) * p.q + D0 + d, s);
+    }
+  }
+  if (use_smem) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < nseg * nD; t += blockDim.x) {
+      const double v = s_part[t];
+      if (v > 0.0) atomicAdd(p.Lacc + ((size_t)(f0 + t / nD) * p.N + i) * p.q + D0 + t % nD, v);
+    }
   }
 }
 
@@ -138,14 +182,17 @@ __device__ __forceinline__ double app_weights(const DecodeParams& p, const LaneG
   return G.active ? p.alpha[((size_t)G.f * (p.N + 1) + i) * p.Mt + G.mi] * bm : 0.0;
 }
 
-// smem: s_w[blockDim] (double) | s_t[min(q, kAppDChunk)][blockDim] (float) | s_C[q]
+// smem: s_w[blockDim] (double) | s_part[kAppSegCap][min(q, kAppDChunk)] (double)
+//       | s_t[blockDim][ts] (float) | s_C[q]
 template <class Core>
-__global__ void __launch_bounds__(kLatticeThreads) k_app(const DecodeParams p) {
+__global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_app(const DecodeParams p) {
   constexpr int MN = Core::Mn;
   extern __shared__ __align__(16) unsigned char smem[];
+  const int ts = app_tstride(p.q);
   double* s_w = reinterpret_cast<double*>(smem);
-  float* s_t = reinterpret_cast<float*>(s_w + blockDim.x);
-  uint32_t* s_C = reinterpret_cast<uint32_t*>(s_t + (size_t)min(p.q, kAppDChunk) * blockDim.x);
+  double* s_part = s_w + blockDim.x;
+  float* s_t = reinterpret_cast<float*>(s_part + kAppSegCap * min(p.q, kAppDChunk));
+  uint32_t* s_C = reinterpret_cast<uint32_t*>(s_t + (size_t)ts * blockDim.x);
   const int i = blockIdx.y + p.i_base;
   for (int t = threadIdx.x; t < p.q; t += blockDim.x) s_C[t] = p.C[(size_t)i * p.q + t];
 
@@ -173,22 +220,24 @@ __global__ void __launch_bounds__(kLatticeThreads) k_app(const DecodeParams p) {
           t0 = fmaf(fo[e], bt[e], t0);
           if (e + 1 < MN) t1 = fmaf(fo[e + 1], bt[e + 1], t1);
         }
-        s_t[d * blockDim.x + threadIdx.x] = P * (t0 + t1);
+        s_t[threadIdx.x * ts + d] = P * (t0 + t1);
       }
     }
     __syncthreads();
-    app_reduce(p, i, D0, nD, s_w, s_t);
+    app_reduce(p, i, D0, nD, s_w, s_t, ts, (long)blockIdx.x * blockDim.x, blockDim.x, s_part);
     __syncthreads();
   }
 }
 
 // Stored variant APP: gamma streamed from HBM instead of recomputed.
-// smem: s_w[blockDim] | s_t[kAppDChunk][blockDim]
+// smem: s_w[blockDim] | s_part[kAppSegCap][min(q, kAppDChunk)] | s_t[blockDim][ts]
 template <int MN>
 __global__ void __launch_bounds__(kLatticeThreads) k_app_stored(const DecodeParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
+  const int ts = app_tstride(p.q);
   double* s_w = reinterpret_cast<double*>(smem);
-  float* s_t = reinterpret_cast<float*>(s_w + blockDim.x);
+  double* s_part = s_w + blockDim.x;
+  float* s_t = reinterpret_cast<float*>(s_part + kAppSegCap * min(p.q, kAppDChunk));
   const int i = blockIdx.y + p.i_base;
   const LaneGeom G = lane_geom(p, i);
   float bt[MN];
@@ -206,11 +255,11 @@ __global__ void __launch_bounds__(kLatticeThreads) k_app_stored(const DecodePara
           t0 = fmaf(__ldcs(gd + (size_t)e * p.Mt), bt[e], t0);
           if (e + 1 < MN) t1 = fmaf(__ldcs(gd + (size_t)(e + 1) * p.Mt), bt[e + 1], t1);
         }
-        s_t[d * blockDim.x + threadIdx.x] = t0 + t1;  // gamma already carries the prior
+        s_t[threadIdx.x * ts + d] = t0 + t1;  // gamma already carries the prior
       }
     }
     __syncthreads();
-    app_reduce(p, i, D0, nD, s_w, s_t);
+    app_reduce(p, i, D0, nD, s_w, s_t, ts, (long)blockIdx.x * blockDim.x, blockDim.x, s_part);
     __syncthreads();
   }
 }
@@ -226,7 +275,7 @@ __global__ void __launch_bounds__(kLatticeThreads) k_gamma_dump(const DecodePara
   if (!G.in) return;
   typename Core::Lane lane;
   Core::init(lane, G.active ? load_window(p, G.f, G.s, G.rho) : 0ull, p);
-  const double unscale = ldexp(1.0, -kLatticeSeedLog2);
+  const double unscale = p.lc.out_scale;
   double* out = p.dbg_gamma + ((size_t)G.f * p.Mt + G.mi) * MN * p.q;
   for (int D = 0; D < p.q; D++) {
     const double P = p.priors ? (double)p.priors[((size_t)G.f * p.N + i) * p.q + D] : 1.0 / p.q;
@@ -245,6 +294,8 @@ struct CoreKernels {
   void (*app_stored)(const DecodeParams);
   void (*gamma_dump)(const DecodeParams);
   long nodes;  // corridor nodes per lattice (0 = generic core: computed on host)
+  int W;       // windows per lane (1 scalar core, 2 packed-pair core)
+  void (*ab_warp[3])(const DecodeParams);  // warp-per-task alpha/beta for M_tau <= 32, 64, 128 (spec only)
 };
 
 template <class Core>
@@ -256,6 +307,8 @@ CoreKernels make_core_kernels(long nodes) {
   k.app_stored = k_app_stored<Core::Mn>;
   k.gamma_dump = k_gamma_dump<Core>;
   k.nodes = nodes;
+  k.W = 1;
+  k.ab_warp[0] = k.ab_warp[1] = k.ab_warp[2] = nullptr;
   return k;
 }
 

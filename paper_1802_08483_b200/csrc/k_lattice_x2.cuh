@@ -1,0 +1,265 @@
+// k_lattice_x2.cuh -- lattice passes on the packed-pair core (SpecCoreX2).
+//
+// Geometry: frame-aligned warp tiles.  A tile is 64 consecutive start drifts
+// m' of ONE frame at one symbol index i (blockIdx.y); lane t owns slots 2t and
+// 2t+1.  A frame of M_tau states spans T = ceil(M_tau / 64) tiles; a CTA is 4
+// tiles.  Because a warp never mixes frames, the symbol priors P(D_i = D) are
+// warp-uniform and the APP sum over m' is a plain warp reduction.
+//
+//   k_gamma_sum_x2 : a1 -- Gamma_i(m', k) = sum_D P(D) G_n(m', k, D)  (eqn:gamma
+//                    folded over D), and every gamma in the stored variant
+//                    (flat geometry: two windows 128 apart per lane).
+//   k_app_x2       : a4 -- second lattice pass (gamma recomputed):
+//                    S_i(D) = sum_{m'} alpha_i(m') sum_k gamma_i(m', m'+k, D) beta_{i+1}(m'+k)
+//                    (eqn:L/eqn:sigma).  With T = 1 the warp holds the whole sum and
+//                    writes L_i(D) = S_i(D) / sum_D S_i(D) directly; with T > 1 the
+//                    warps add FP64 partials into Lacc (k_finalize normalises).
+#pragma once
+#include "k_lattice.cuh"
+
+namespace bsidmap {
+
+constexpr int kTileSlots = 64;
+constexpr int kX2Warps = kLatticeThreads / 32;
+
+__host__ __device__ __forceinline__ int tiles_per_frame(int Mt) { return (Mt + kTileSlots - 1) / kTileSlots; }
+
+// Window geometry of frame f, state index mi at symbol index i.
+__device__ __forceinline__ LaneGeom geom_fm(const DecodeParams& p, int i, int f, int mi, bool in) {
+  LaneGeom G;
+  G.in = in;
+  G.f = in ? f : 0;
+  G.mi = in ? mi : 0;
+  G.mp = p.mt_lo + G.mi;
+  G.s = p.n * i + G.mp;
+  G.rho = in ? p.rho[G.f] : 0;
+  G.active = in && p.status[G.f] == kFrameOk && G.s >= 0 && G.s <= G.rho;
+  return G;
+}
+
+// 2^k as a double, k in [-1022, 1023] (exact; no division on the hot path)
+__device__ __forceinline__ double pow2d(int k) {
+  k = max(-1022, min(1023, k));
+  return __hiloint2double((k + 1023) << 20, 0);
+}
+__device__ __forceinline__ int exp2_of(double x) {  // floor(log2 x) for normal x > 0
+  return ((__double2hiint(x) >> 20) & 0x7ff) - 1023;
+}
+
+// Pass 1 uses flat geometry: lane t of a CTA owns windows g0 + t and g0 + t + 128
+// (g = f M_tau + m' index, g0 = 256 blockIdx.x) -- no frame alignment needed here.
+template <class Core, bool kStoreGamma>
+__global__ void __launch_bounds__(kLatticeThreads, Core::kMinBlocks) k_gamma_sum_x2(const DecodeParams p) {
+  constexpr int MN = Core::Mn;
+  extern __shared__ uint32_t s_C[];
+  const int i = blockIdx.y + p.i_base;
+  for (int t = threadIdx.x; t < p.q; t += blockDim.x) s_C[t] = p.C[(size_t)i * p.q + t];
+  __syncthreads();
+
+  const long ga = (long)blockIdx.x * (2 * blockDim.x) + threadIdx.x;
+  const LaneGeom A = lane_geom_at(p, i, ga), B = lane_geom_at(p, i, ga + blockDim.x);
+  f32x2 acc[MN];
+#pragma unroll
+  for (int e = 0; e < MN; e++) acc[e] = 0ull;
+
+  if (__any_sync(0xffffffffu, A.active || B.active)) {
+    typename Core::Lane lane;
+    Core::init(lane, A.active ? load_window(p, A.f, A.s, A.rho) : 0ull,
+               B.active ? load_window(p, B.f, B.s, B.rho) : 0ull, p);
+    const float* pa = p.priors ? p.priors + ((size_t)A.f * p.N + i) * p.q : nullptr;
+    const float* pb = p.priors ? p.priors + ((size_t)B.f * p.N + i) * p.q : nullptr;
+    const float usc = 1.f / p.q;
+    for (int D = 0; D < p.q; D++) {
+      const f32x2 P = pa ? pk(__ldg(pa + D), __ldg(pb + D)) : pk(1.f, 1.f);
+      f32x2 fo[MN];
+      Core::run(lane, s_C[D], p, fo);
+#pragma unroll
+      for (int e = 0; e < MN; e++) acc[e] = ffma2(P, fo[e], acc[e]);
+      if constexpr (kStoreGamma) {
+        const float sa = pa ? lo_of(P) : usc, sb = pa ? hi_of(P) : usc;
+        if (A.in) {
+          float* g = p.gamma + ((((size_t)A.f * p.N + i) * p.q + D) * MN) * p.Mt + A.mi;
+#pragma unroll
+          for (int e = 0; e < MN; e++) __stcs(g + (size_t)e * p.Mt, out_valid(p, A, e) ? sa * lo_of(fo[e]) : 0.f);
+        }
+        if (B.in) {
+          float* g = p.gamma + ((((size_t)B.f * p.N + i) * p.q + D) * MN) * p.Mt + B.mi;
+#pragma unroll
+          for (int e = 0; e < MN; e++) __stcs(g + (size_t)e * p.Mt, out_valid(p, B, e) ? sb * hi_of(fo[e]) : 0.f);
+        }
+      }
+    }
+  } else if constexpr (kStoreGamma) {
+    for (int w = 0; w < 2; w++) {
+      const LaneGeom& G = w ? B : A;
+      if (!G.in) continue;
+      float* g = p.gamma + (((size_t)G.f * p.N + i) * p.q) * MN * p.Mt + G.mi;
+      for (int D = 0; D < p.q; D++)
+#pragma unroll
+        for (int e = 0; e < MN; e++) __stcs(g + ((size_t)D * MN + e) * p.Mt, 0.f);
+    }
+  }
+  const float sc = p.priors ? 1.f : 1.f / p.q;
+  if (A.in) {
+    float* out = p.Gsum + ((size_t)A.f * p.N + i) * MN * p.Mt + A.mi;
+#pragma unroll
+    for (int e = 0; e < MN; e++) out[(size_t)e * p.Mt] = out_valid(p, A, e) ? sc * lo_of(acc[e]) : 0.f;
+  }
+  if (B.in) {
+    float* out = p.Gsum + ((size_t)B.f * p.N + i) * MN * p.Mt + B.mi;
+#pragma unroll
+    for (int e = 0; e < MN; e++) out[(size_t)e * p.Mt] = out_valid(p, B, e) ? sc * hi_of(acc[e]) : 0.f;
+  }
+}
+
+// beta_{i+1}(m'+k) of one window, scaled by 2^-E (E = exponent of its corridor max),
+// as FP32 in [0, 2); returns w = alpha_i(m') 2^E (FP64) so that w * bt = alpha * beta exactly.
+template <int MN>
+__device__ __forceinline__ double app_weights_p2(const DecodeParams& p, const LaneGeom& G, int i, float (&bt)[MN]) {
+  double bv[MN];
+  double bm = 0.0;
+  const double* brow = p.beta + ((size_t)G.f * (p.N + 1) + (i + 1)) * p.Mt + G.mi + p.mn_lo;
+#pragma unroll
+  for (int e = 0; e < MN; e++) {
+    bv[e] = out_valid(p, G, e) ? brow[e] : 0.0;
+    bm = fmax(bm, bv[e]);
+  }
+  const int E = bm > 0.0 ? exp2_of(bm) : 0;
+  const double sc = pow2d(-E);
+#pragma unroll
+  for (int e = 0; e < MN; e++) bt[e] = (float)(bv[e] * sc);
+  return (G.active && bm > 0.0) ? p.alpha[((size_t)G.f * (p.N + 1) + i) * p.Mt + G.mi] * pow2d(E) : 0.0;
+}
+
+// smem: s_C[q] | s_S[kX2Warps][q] (float)
+template <class Core>
+__global__ void __launch_bounds__(kLatticeThreads, Core::kMinBlocks) k_app_x2(const DecodeParams p) {
+  constexpr int MN = Core::Mn;
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* s_C = reinterpret_cast<uint32_t*>(smem);
+  float* s_S = reinterpret_cast<float*>(s_C + p.q);
+  const int i = blockIdx.y + p.i_base;
+  for (int t = threadIdx.x; t < p.q; t += blockDim.x) s_C[t] = p.C[(size_t)i * p.q + t];
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T = tiles_per_frame(p.Mt);
+  const long tile = (long)blockIdx.x * kX2Warps + warp;
+  const int f = (int)(tile / T);
+  if (f >= p.F) return;  // warp-uniform; no block barrier follows
+  const int mia = (int)(tile % T) * kTileSlots + 2 * lane;
+  const LaneGeom A = geom_fm(p, i, f, mia, mia < p.Mt);
+  const LaneGeom B = geom_fm(p, i, f, mia + 1, mia + 1 < p.Mt);
+  const bool frame_ok = p.status[f] == kFrameOk;
+
+  f32x2 bt[MN];
+  float wa, wb;
+  int Emax;
+  {
+    float ba[MN], bb[MN];
+    const double da = app_weights_p2<MN>(p, A, i, ba), db = app_weights_p2<MN>(p, B, i, bb);
+#pragma unroll
+    for (int e = 0; e < MN; e++) bt[e] = pk(ba[e], bb[e]);
+    // common power-of-two scale of the tile's weights (max exponent over the warp)
+    const double dm = fmax(da, db);
+    Emax = __reduce_max_sync(0xffffffffu, dm > 0.0 ? exp2_of(dm) + 2048 : 0) - 2048;
+    const double sc = pow2d(-Emax);
+    wa = (float)(da * sc);
+    wb = (float)(db * sc);
+  }
+  const bool live = __any_sync(0xffffffffu, wa > 0.f || wb > 0.f);
+  float* S = s_S + warp * p.q;
+  if (live) {
+    typename Core::Lane lane_t;
+    Core::init(lane_t, A.active ? load_window(p, A.f, A.s, A.rho) : 0ull,
+               B.active ? load_window(p, B.f, B.s, B.rho) : 0ull, p);
+    const float* pri = p.priors ? p.priors + ((size_t)f * p.N + i) * p.q : nullptr;
+    for (int D = 0; D < p.q; D++) {
+      f32x2 fo[MN];
+      Core::run(lane_t, s_C[D], p, fo);
+      // t(m', D) = sum_k G(m', k, D) bt(m', k) for both windows (two chains)
+      f32x2 t0 = 0ull, t1 = 0ull;
+#pragma unroll
+      for (int e = 0; e < MN; e += 2) {
+        t0 = ffma2(fo[e], bt[e], t0);
+        if (e + 1 < MN) t1 = ffma2(fo[e + 1], bt[e + 1], t1);
+      }
+      float c = fmaf(wa, lo_of(t0) + lo_of(t1), wb * (hi_of(t0) + hi_of(t1)));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (lane == 0) S[D] = pri ? c * __ldg(pri + D) : c;
+    }
+  }
+  __syncwarp();
+  if (T == 1) {
+    // the warp holds the whole sum over m': L_i(D) = S(D) / sum_D S(D)
+    float tot = 0.f;
+    if (live)
+      for (int D = lane; D < p.q; D += 32) tot += S[D];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    const bool ok = frame_ok && live && tot > 0.f;
+    const float inv = ok ? 1.f / tot : 0.f;
+    float* Lrow = p.L + ((size_t)f * p.N + i) * p.q;
+    for (int D = lane; D < p.q; D += 32) Lrow[D] = ok ? S[D] * inv : 0.f;
+    if (frame_ok && !ok && lane == 0) p.status[f] = kFrameUnderflow;
+  } else if (live) {
+    const double sc = pow2d(Emax);
+    double* acc = p.Lacc + ((size_t)f * p.N + i) * p.q;
+    for (int D = lane; D < p.q; D += 32) {
+      const float v = S[D];
+      if (v > 0.f) atomicAdd(acc + D, (double)v * sc);
+    }
+  }
+}
+
+template <class Core>
+__global__ void __launch_bounds__(kLatticeThreads) k_gamma_dump_x2(const DecodeParams p) {
+  constexpr int MN = Core::Mn;
+  extern __shared__ uint32_t s_C[];
+  const int i = p.dbg_i;
+  for (int t = threadIdx.x; t < p.q; t += blockDim.x) s_C[t] = p.C[(size_t)i * p.q + t];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T = tiles_per_frame(p.Mt);
+  const long tile = (long)blockIdx.x * kX2Warps + warp;
+  const int f = (int)(tile / T);
+  const int mia = (int)(tile % T) * kTileSlots + 2 * lane;
+  const LaneGeom A = geom_fm(p, i, f, mia, f < p.F && mia < p.Mt);
+  const LaneGeom B = geom_fm(p, i, f, mia + 1, f < p.F && mia + 1 < p.Mt);
+  typename Core::Lane lane_t;
+  Core::init(lane_t, A.active ? load_window(p, A.f, A.s, A.rho) : 0ull,
+             B.active ? load_window(p, B.f, B.s, B.rho) : 0ull, p);
+  const double unscale = p.lc.out_scale;
+  for (int D = 0; D < p.q; D++) {
+    f32x2 fo[MN];
+    Core::run(lane_t, s_C[D], p, fo);
+    for (int w = 0; w < 2; w++) {
+      const LaneGeom& G = w ? B : A;
+      if (!G.in) continue;
+      const double P = p.priors ? (double)p.priors[((size_t)G.f * p.N + i) * p.q + D] : 1.0 / p.q;
+      double* out = p.dbg_gamma + ((size_t)G.f * p.Mt + G.mi) * MN * p.q;
+#pragma unroll
+      for (int e = 0; e < MN; e++)
+        out[(size_t)e * p.q + D] = out_valid(p, G, e) ? P * (double)(w ? hi_of(fo[e]) : lo_of(fo[e])) * unscale : 0.0;
+    }
+  }
+}
+
+template <class Core>
+CoreKernels make_core_kernels_x2(long nodes) {
+  CoreKernels k;
+  k.gamma_sum = k_gamma_sum_x2<Core, false>;
+  k.gamma_store = k_gamma_sum_x2<Core, true>;
+  k.app = k_app_x2<Core>;
+  k.app_stored = k_app_stored<Core::Mn>;
+  k.gamma_dump = k_gamma_dump_x2<Core>;
+  k.nodes = nodes;
+  k.W = 2;
+  k.ab_warp[0] = k_alpha_beta_warp<1, Core::Mn>;
+  k.ab_warp[1] = k_alpha_beta_warp<2, Core::Mn>;
+  k.ab_warp[2] = k_alpha_beta_warp<4, Core::Mn>;
+  return k;
+}
+
+}  // namespace bsidmap

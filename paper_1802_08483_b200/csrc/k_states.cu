@@ -70,20 +70,23 @@ __global__ void __launch_bounds__(1024) k_alpha_beta(const DecodeParams p) {
     const float* G = Gf + (size_t)i * Mn * Mt;  // [k][m']
     double part = 0.0;
     for (int m = threadIdx.x; m < Mt; m += blockDim.x) {
-      double acc = 0.0;
-      if (fwd) {
-        // alpha'_{i+1}(m) = sum_k alpha_i(m - k) Gamma_i(m - k, k)
-        for (int e = 0; e < Mn; e++) {
-          const int mp = m - lo - e;
-          if (mp >= 0 && mp < Mt) acc += cur[mp] * (double)__ldg(G + (size_t)e * Mt + mp);
-        }
-      } else {
-        // beta'_i(m') = sum_k Gamma_i(m', k) beta_{i+1}(m' + k)
-        for (int e = 0; e < Mn; e++) {
-          const int mn = m + lo + e;
-          if (mn >= 0 && mn < Mt) acc += (double)__ldg(G + (size_t)e * Mt + m) * cur[mn];
-        }
+      // issue all M_n loads of Gamma_i first (independent, one latency per step)
+      float g[kMaxMn];
+#pragma unroll
+      for (int e = 0; e < kMaxMn; e++) {
+        const int idx = fwd ? m - lo - e : m;  // alpha reads Gamma_i(m - k, k); beta reads Gamma_i(m', k)
+        g[e] = (e < Mn && idx >= 0 && idx < Mt) ? __ldg(G + (size_t)e * Mt + idx) : 0.f;
       }
+      double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+      for (int e = 0; e < kMaxMn; e += 2) {
+        // alpha'_{i+1}(m) = sum_k alpha_i(m - k) Gamma_i(m - k, k);  beta'_i(m') = sum_k Gamma_i(m', k) beta_{i+1}(m' + k)
+        const int j0 = fwd ? m - lo - e : m + lo + e;
+        const int j1 = fwd ? j0 - 1 : j0 + 1;
+        if (e < Mn && j0 >= 0 && j0 < Mt) acc0 = fma(cur[j0], (double)g[e], acc0);
+        if (e + 1 < Mn && j1 >= 0 && j1 < Mt) acc1 = fma(cur[j1], (double)g[e + 1], acc1);
+      }
+      const double acc = acc0 + acc1;
       nxt[m] = acc;
       part += acc;
     }
@@ -101,6 +104,15 @@ __global__ void __launch_bounds__(1024) k_alpha_beta(const DecodeParams p) {
     }
     __syncthreads();
   }
+}
+
+// Frames that failed (status != OK) get all-zero L rows (contract of bsidmap_decode_batch);
+// also catches an UNDERFLOW raised by a late row after other rows were written.
+__global__ void k_zero_failed(const DecodeParams p) {
+  const int f = blockIdx.x;
+  if (p.status[f] == kFrameOk) return;
+  float* L = p.L + (size_t)f * p.N * p.q;
+  for (long k = threadIdx.x; k < (long)p.N * p.q; k += blockDim.x) L[k] = 0.f;
 }
 
 // One warp per (frame, i) row.

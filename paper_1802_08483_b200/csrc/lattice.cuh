@@ -11,9 +11,11 @@
 //   F_{n,j} =                    Pd F_{n-1,j} + Q(y_j|x_n) F_{n-1,j-1}   (eqn:F_lastrow)
 //
 // In e-coordinates (r, j-1) is e-1, (r-1, j) is e+1 and (r-1, j-1) is e, so
-// one row is new[e] = a new[e-1] + b old[e+1] + Q old[e]: one FMUL and two
-// FFMAs per node, only the a-term on the serial chain.  Writing new[e] over
-// old[e] is safe because new[e+1] reads old[e+1], old[e+2] only.
+// one row is new[e] = a new[e-1] + b old[e+1] + Q old[e], only the a-term on
+// the serial chain.  With Pd > 0 the kernels run the exact rescaling
+// G = F / Pd^r (see LatticeConst), new[e] = a new[e-1] + old[e+1] + (Q/Pd) old[e]:
+// two FFMAs per node.  Writing new[e] over old[e] is safe because new[e+1]
+// reads old[e+1], old[e+2] only.
 //
 // Lane mapping (B200 design, not the paper's): a lane owns one window
 // (frame, i, m') and loops over the q symbols D.  x = C_i(D) is therefore
@@ -54,7 +56,7 @@ struct SpecCore {
     }
   }
 
-  template <int R>
+  template <int R, bool kRescaled>
   __device__ __forceinline__ static void row(float (&f)[MN], const float (&Q)[J + 1], const LatticeConst& lc) {
     constexpr bool kLast = (R == NN);
     float prev = 0.f;
@@ -64,15 +66,14 @@ struct SpecCore {
       if (j < 0) continue;       // left of column 0: structurally zero, stays 0
       float v;
       if (j == 0) {
-        v = (e + 1 < MN) ? lc.b * f[e + 1] : 0.f;  // column 0 is reached by deletions only
+        // column 0 is reached by deletions only: F_{r,0} = Pd F_{r-1,0}, i.e. G_{r,0} = G_{r-1,0}
+        v = kRescaled ? f[e + 1] : lc.b * f[e + 1];
       } else {
         float u;
-        if (e + 1 < MN) {
-          u = lc.b * f[e + 1];          // deletion   Pd F_{r-1,j}
-          u = fmaf(Q[j], f[e], u);      // transmission Q F_{r-1,j-1}
-        } else {
+        if (e + 1 < MN)  // deletion Pd F_{r-1,j} + transmission Q F_{r-1,j-1}
+          u = kRescaled ? fmaf(Q[j], f[e], f[e + 1]) : fmaf(Q[j], f[e], lc.b * f[e + 1]);
+        else
           u = Q[j] * f[e];
-        }
         v = (!kLast && e > 0) ? fmaf(lc.a, prev, u) : u;  // insertion 1/2 Pi F_{r,j-1}
       }
       f[e] = v;
@@ -80,18 +81,29 @@ struct SpecCore {
     }
   }
 
+  // Rows are issued in pairs: a 4-way branch on (x_R, x_{R+1}) puts rows R and R+1
+  // in one basic block, so the scheduler interleaves their two insertion chains
+  // (row R+1 node e only needs row R nodes e, e+1) -- ILP 2 without extra registers.
   template <int R>
   __device__ __forceinline__ static void rows(float (&f)[MN], uint32_t x, const Lane& L, const LatticeConst& lc) {
-    if constexpr (R <= NN) {
+    if constexpr (R + 1 <= NN) {
+      switch ((x >> (R - 1)) & 3u) {
+        case 0u: row<R, true>(f, L.q0, lc); row<R + 1, true>(f, L.q0, lc); break;
+        case 1u: row<R, true>(f, L.q1, lc); row<R + 1, true>(f, L.q0, lc); break;
+        case 2u: row<R, true>(f, L.q0, lc); row<R + 1, true>(f, L.q1, lc); break;
+        default: row<R, true>(f, L.q1, lc); row<R + 1, true>(f, L.q1, lc); break;
+      }
+      rows<R + 2>(f, x, L, lc);
+    } else if constexpr (R == NN) {
       if ((x >> (R - 1)) & 1u)
-        row<R>(f, L.q1, lc);
+        row<R, true>(f, L.q1, lc);
       else
-        row<R>(f, L.q0, lc);
-      rows<R + 1>(f, x, L, lc);
+        row<R, true>(f, L.q0, lc);
     }
   }
 
-  // f[e] <- 2^80 F_{n, n + m_n^- + e}
+  // f[e] <- lattice output for drift change k = m_n^- + e (true metric = lc.out_scale * f[e]).
+  // Spec cores run the rescaled recursion only (Pd > 0; the planner routes Pd = 0 to GenCore).
   __device__ __forceinline__ static void run(const Lane& L, uint32_t x, const DecodeParams& p, float (&f)[MN]) {
 #pragma unroll
     for (int e = 0; e < MN; e++) f[e] = p.lc.row0[e];  // F_{0,j}: host zeroes j < 0
@@ -126,7 +138,7 @@ struct GenCore {
         const int j = j0 + e;
         float v = 0.f;
         if (j >= 0) {
-          float u = (e + 1 < MN) ? lc.b * f[e + 1] : 0.f;
+          float u = (e + 1 < MN) ? (lc.rescaled ? f[e + 1] : lc.b * f[e + 1]) : 0.f;
           if (j >= 1) {
             const uint32_t yb = (uint32_t)(L.win >> (j - 1)) & 1u;
             u = fmaf((yb == xr) ? lc.qm : lc.qs, f[e], u);

@@ -1,0 +1,101 @@
+// lattice_x2.cuh -- the spec lattice core on packed FP32 pairs (FFMA2, sm_100a).
+//
+// Same recursion as SpecCore (lattice.cuh: corridor nodes only, rescaled
+// G = F / Pd^r so a node is u = (Q/Pd) G_{r-1,j-1} + G_{r-1,j};
+// G_{r,j} = 1/2 Pi G_{r,j-1} + u), but every lane runs TWO windows -- two
+// start drifts m' of the same (frame chunk, i) -- for the same symbol D, so
+// x = C_i(D) and the row branch stay warp-uniform and every node of both
+// lattices is one fma.rn.f32x2.  Measured on B200 (tools/ubench): a scalar
+// FFMA with three register sources issues at ~0.69 of the FP32 peak, the
+// packed FFMA2 with three register-pair sources at ~0.98 -- the per-lane Q-dot
+// operand makes the scalar node FFMA a three-register one, the packed one
+// is not penalised.
+#pragma once
+#include "common.cuh"
+
+namespace bsidmap {
+
+typedef unsigned long long f32x2;
+
+__device__ __forceinline__ f32x2 pk(float lo, float hi) {
+  return (f32x2)__float_as_uint(lo) | ((f32x2)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ float lo_of(f32x2 v) { return __uint_as_float((unsigned)v); }
+__device__ __forceinline__ float hi_of(f32x2 v) { return __uint_as_float((unsigned)(v >> 32)); }
+
+__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+template <int NN, int LO, int MN>
+struct SpecCoreX2 {
+  static constexpr int Mn = MN;
+  static constexpr int W = 2;
+  static constexpr int J = NN + LO + MN - 1;  // last window column n + m_n^+
+  static_assert(MN >= 1 && MN <= kMaxMn && LO <= 0 && LO + MN - 1 >= 0 && J <= kMaxWindow, "shape");
+  // register estimate: Q-dot tables 4J + band and accumulator 4 M_n + ~30; 3 CTAs/SM fit 168 regs
+  static constexpr int kMinBlocks = (4 * J + 4 * MN + 30 <= 168) ? 3 : 2;
+
+  struct Lane {
+    f32x2 q1[J + 1];  // (Q/Pd)(y_j | x = 1) of windows (a, b), j = 1..J
+    f32x2 q0[J + 1];  // (Q/Pd)(y_j | x = 0)
+  };
+
+  __device__ __forceinline__ static void init(Lane& L, uint64_t wa, uint64_t wb, const DecodeParams& p) {
+#pragma unroll
+    for (int j = 1; j <= J; j++) {
+      const bool ya = (wa >> (j - 1)) & 1ull, yb = (wb >> (j - 1)) & 1ull;
+      L.q1[j] = pk(ya ? p.lc.qm : p.lc.qs, yb ? p.lc.qm : p.lc.qs);
+      L.q0[j] = pk(ya ? p.lc.qs : p.lc.qm, yb ? p.lc.qs : p.lc.qm);
+    }
+  }
+
+  template <int R>
+  __device__ __forceinline__ static void row(f32x2 (&f)[MN], const f32x2 (&Q)[J + 1], f32x2 a2) {
+    constexpr bool kLast = (R == NN);
+    f32x2 prev = 0ull;
+#pragma unroll
+    for (int e = 0; e < MN; e++) {
+      const int j = R + LO + e;
+      if (j < 0) continue;  // structurally zero
+      f32x2 v;
+      if (j == 0) {
+        v = f[e + 1];  // column 0: deletions only, G_{r,0} = G_{r-1,0}
+      } else {
+        const f32x2 u = (e + 1 < MN) ? ffma2(Q[j], f[e], f[e + 1]) : fmul2(Q[j], f[e]);
+        v = (!kLast && e > 0) ? ffma2(a2, prev, u) : u;
+      }
+      f[e] = v;
+      prev = v;
+    }
+  }
+
+  template <int R>
+  __device__ __forceinline__ static void rows(f32x2 (&f)[MN], uint32_t x, const Lane& L, f32x2 a2) {
+    if constexpr (R <= NN) {
+      if ((x >> (R - 1)) & 1u)
+        row<R>(f, L.q1, a2);
+      else
+        row<R>(f, L.q0, a2);
+      rows<R + 1>(f, x, L, a2);
+    }
+  }
+
+  // f[e] <- (window a, window b) lattice outputs for k = m_n^- + e (times lc.out_scale)
+  __device__ __forceinline__ static void run(const Lane& L, uint32_t x, const DecodeParams& p, f32x2 (&f)[MN]) {
+#pragma unroll
+    for (int e = 0; e < MN; e++) f[e] = pk(p.lc.row0[e], p.lc.row0[e]);
+    rows<1>(f, x, L, pk(p.lc.a, p.lc.a));
+  }
+
+  static constexpr long nodes() { return (long)NN * MN - (long)LO * (LO - 1) / 2; }
+};
+
+}  // namespace bsidmap
