@@ -3,7 +3,7 @@
 #   make ptxas      -> register / spill report of every kernel
 NVCC    ?= /usr/local/cuda/bin/nvcc
 ARCH    := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O2 --expt-relaxed-constexpr
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O2 --expt-relaxed-constexpr $(EXTRA)
 CSRC    := paper_1802_08483_b200/csrc
 OBJDIR  := build/obj
 CU      := $(wildcard $(CSRC)/*.cu)

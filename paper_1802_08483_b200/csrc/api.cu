@@ -77,7 +77,7 @@ struct Layout {
 // Bytes per frame of each workspace array (the paper's memory estimate).
 Layout layout(const bsidmap_decoder* d, long F, int mode) {
   Layout l{};
-  l.gsum = align_up((size_t)F * d->N * d->Mn * d->Mt * sizeof(float));
+  l.gsum = align_up((size_t)F * d->N * d->Mn * ((d->Mt + 3) & ~3) * sizeof(float));
   l.gamma = mode == BSIDMAP_MODE_STORED ? align_up((size_t)F * d->N * d->q * d->Mn * d->Mt * sizeof(float)) : 0;
   l.alpha = align_up((size_t)F * (d->N + 1) * d->Mt * sizeof(double));
   l.beta = l.alpha;
@@ -126,10 +126,12 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   P->ab_smem = (2 * (size_t)d->Mt + 33) * sizeof(double);
   P->ab_warp = nullptr;
   const int spt = (d->Mt + 31) / 32;
-  if (d->kern.ab_warp[0] && spt <= 4) {
+  const int spt_k = spt == 3 ? 4 : spt;
+  const size_t ab_warp_bytes = (size_t)(kAbWarpThreads / 32) * ab_warp_smem(spt_k, d->Mn, (d->Mt + 3) & ~3);
+  if (d->kern.ab_warp[0] && spt <= 4 && ab_warp_bytes <= 100 * 1024) {
     const int k = spt == 1 ? 0 : spt == 2 ? 1 : 2;
     P->ab_warp = d->kern.ab_warp[k];
-    P->ab_smem = (size_t)(kAbWarpThreads / 32) * (spt == 3 ? 4 : spt) * 32 * sizeof(double);
+    P->ab_smem = ab_warp_bytes;
   }
   const size_t nwin = kLatticeThreads;
   P->app_smem = nwin * sizeof(double) + (size_t)kAppSegCap * std::min(d->q, kAppDChunk) * sizeof(double) +
@@ -170,6 +172,7 @@ void fill_params(const bsidmap_decoder* d, DecodeParams* p) {
   p->q = d->q; p->n = d->n; p->N = d->N;
   p->mn_lo = d->mn_lo; p->mn_hi = d->mn_hi; p->Mn = d->Mn;
   p->mt_lo = d->mt_lo; p->mt_hi = d->mt_hi; p->Mt = d->Mt;
+  p->Mtp = (d->Mt + 3) & ~3;
   p->C = d->d_C;
   p->lc = d->lc;
 }

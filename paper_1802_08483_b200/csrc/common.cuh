@@ -39,6 +39,7 @@ struct DecodeParams {
   int q, n, N;
   int mn_lo, mn_hi, Mn;
   int mt_lo, mt_hi, Mt;
+  int Mtp;                    // row stride of Gsum: M_tau rounded up to a multiple of 4 (16-byte rows for TMA)
   int F;                      // frames in this chunk
   const uint32_t* C;          // [N][q] codebook, decoder-owned (bit t = t-th transmitted bit)
   const uint32_t* rx;         // packed received words, caller-owned
@@ -46,7 +47,7 @@ struct DecodeParams {
   const int32_t* rho;         // [F] received length
   const float* priors;        // [F][N][q] or nullptr (uniform 1/q)
   int32_t* status;            // [F]
-  float* Gsum;                // [F][N][M_n][M_tau]  Gamma_i(m', k) = sum_D gamma_i(m', m'+k, D), scaled 2^80
+  float* Gsum;                // [F][N][M_n][Mtp]  Gamma_i(m', k) = sum_D gamma_i(m', m'+k, D) (lattice scale)
   float* gamma;               // stored variant: [F][N][q][M_n][M_tau] gamma, scaled 2^80
   double* alpha;              // [F][N+1][M_tau] normalised alpha rows
   double* beta;               // [F][N+1][M_tau] normalised beta rows

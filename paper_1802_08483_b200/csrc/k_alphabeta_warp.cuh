@@ -4,28 +4,81 @@
 //   alpha'_{i+1}(m) = sum_k alpha_i(m - k) Gamma_i(m - k, k)      (eqn:alpha_prenorm)
 //   beta'_i(m')     = sum_k Gamma_i(m', k) beta_{i+1}(m' + k)     (eqn:beta)
 // then division by the row sum (eqn:alpha_norm; "similar" for beta), FP64.
-// The row lives in this warp's shared-memory slice; Gamma_i is read straight from
-// HBM/L2 (M_n coalesced loads per state), latency hidden by the many resident warps.
+//
+// The recursion is sequential in i and HBM-bound (it reads every Gamma_i block,
+// M_n x Mtp FP32, once per direction).  Each warp streams its frame's Gamma_i
+// blocks through a kStages-deep ring in shared memory with the TMA bulk-copy
+// engine (cp.async.bulk ... mbarrier::complete_tx): lane 0 issues the copy of step
+// i + kStages as soon as step i's block is consumed, so the copies overlap the
+// FP64 arithmetic of the steps in between and no register holds prefetched data.
 #pragma once
 #include "common.cuh"
 
 namespace bsidmap {
 
-constexpr int kAbWarpThreads = 256;  // 8 (frame, direction) tasks per CTA
+constexpr int kAbWarpThreads = 128;  // 4 (frame, direction) tasks per CTA
+constexpr int kAbStages = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// bulk global -> shared copy, completion signalled on `bar` (bytes % 16 == 0, both addresses 16-aligned)
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// shared memory per warp: row[SPT*32] doubles | ring[kStages][MN][Mtp] floats | bars[kStages]
+__host__ __device__ __forceinline__ size_t ab_warp_smem(int SPT, int MN, int Mtp) {
+  return (size_t)SPT * 32 * 8 + (size_t)kAbStages * MN * Mtp * 4 + kAbStages * 8;
+}
 
 template <int SPT, int MN>
-__global__ void __launch_bounds__(kAbWarpThreads, 2) k_alpha_beta_warp(const DecodeParams p) {
-  extern __shared__ __align__(16) double s_rows[];  // [8][SPT * 32]
+__global__ void __launch_bounds__(kAbWarpThreads) k_alpha_beta_warp(const DecodeParams p) {
+  extern __shared__ __align__(128) unsigned char s_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Mt = p.Mt, Mtp = p.Mtp, N = p.N, lo = p.mn_lo;
+  unsigned char* base = s_raw + (size_t)warp * ab_warp_smem(SPT, MN, Mtp);
+  double* row = reinterpret_cast<double*>(base);
+  float* ring = reinterpret_cast<float*>(base + SPT * 32 * 8);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + SPT * 32 * 8 + (size_t)kAbStages * MN * Mtp * 4);
   const long task = (long)blockIdx.x * (kAbWarpThreads / 32) + warp;
   if (task >= 2L * p.F) return;  // warp-uniform
   const int f = (int)(task >> 1);
   const bool fwd = (task & 1) == 0;
   if (p.status[f] != kFrameOk) return;
-  const int Mt = p.Mt, N = p.N, lo = p.mn_lo;
-  double* row = s_rows + warp * SPT * 32;
   double* rows_g = (fwd ? p.alpha : p.beta) + (size_t)f * (N + 1) * Mt;
-  const float* Gf = p.Gsum + (size_t)f * N * MN * Mt;
+  const float* Gf = p.Gsum + (size_t)f * N * MN * Mtp;
+  const uint32_t blk_bytes = (uint32_t)(MN * Mtp * 4);
+  auto gblock = [&](int step) { return Gf + (size_t)(fwd ? step : N - 1 - step) * MN * Mtp; };
+
+  if (lane == 0) {
+    for (int s = 0; s < kAbStages; s++) mbar_init(bars + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < kAbStages && s < N; s++) {
+      mbar_expect_tx(bars + s, blk_bytes);
+      tma_bulk_g2s(ring + (size_t)s * MN * Mtp, gblock(s), blk_bytes, bars + s);
+    }
+  }
   const int boundary = fwd ? -p.mt_lo : p.rho[f] - p.n * N - p.mt_lo;  // alpha_0 = delta(0), beta_N = delta(rho - tau)
   const int i0 = fwd ? 0 : N;
 #pragma unroll
@@ -37,20 +90,9 @@ __global__ void __launch_bounds__(kAbWarpThreads, 2) k_alpha_beta_warp(const Dec
   }
   __syncwarp();
   for (int step = 0; step < N; step++) {
-    const int i = fwd ? step : N - 1 - step;
-    const float* G = Gf + (size_t)i * MN * Mt;  // [k][m']
-    // all SPT * M_n loads of Gamma_i first (unconditional, clamped addresses) so they are in
-    // flight together: one memory latency per step
-    float g[SPT][MN];
-#pragma unroll
-    for (int s = 0; s < SPT; s++) {
-      const int m = lane + 32 * s;
-#pragma unroll
-      for (int e = 0; e < MN; e++) {
-        const int idx = fwd ? m - lo - e : m;
-        g[s][e] = __ldg(G + (size_t)e * Mt + min(max(idx, 0), Mt - 1));
-      }
-    }
+    const int stage = step % kAbStages;
+    mbar_wait(bars + stage, (uint32_t)(step / kAbStages) & 1u);
+    const float* G = ring + (size_t)stage * MN * Mtp;  // Gamma_i [k][m'] in smem
     double acc[SPT];
     double part = 0.0;
 #pragma unroll
@@ -62,8 +104,8 @@ __global__ void __launch_bounds__(kAbWarpThreads, 2) k_alpha_beta_warp(const Dec
         const int idx = fwd ? m - lo - e : m;         // Gamma_i column read by this term
         const int j = fwd ? m - lo - e : m + lo + e;  // neighbouring state of the previous row
         const bool ok = m < Mt && idx >= 0 && idx < Mt && j >= 0 && j < Mt;
-        const double r = ok ? row[j] : 0.0;
-        const double gv = ok ? (double)g[s][e] : 0.0;
+        const double r = ok ? row[min(max(j, 0), Mt - 1)] : 0.0;
+        const double gv = ok ? (double)G[e * Mtp + min(max(idx, 0), Mt - 1)] : 0.0;
         if (e & 1) a1 = fma(r, gv, a1); else a0 = fma(r, gv, a0);
       }
       acc[s] = a0 + a1;
@@ -71,13 +113,20 @@ __global__ void __launch_bounds__(kAbWarpThreads, 2) k_alpha_beta_warp(const Dec
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    __syncwarp();  // every lane is done with this stage and with the old row
+    if (lane == 0 && step + kAbStages < N) {
+      mbar_expect_tx(bars + stage, blk_bytes);
+      tma_bulk_g2s(ring + (size_t)stage * MN * Mtp, gblock(step + kAbStages), blk_bytes, bars + stage);
+    }
     if (!(part > 0.0)) {  // all-zero row: Y impossible under the limits (reading R14)
       if (lane == 0) p.status[f] = kFrameUnderflow;
+      // drain the copies already issued for later steps before the warp's smem can be reused
+      for (int t = step + 1; t < N && t <= step + kAbStages; t++)
+        mbar_wait(bars + t % kAbStages, (uint32_t)(t / kAbStages) & 1u);
       return;
     }
     const double inv = 1.0 / part;
-    const int r = fwd ? i + 1 : i;
-    __syncwarp();
+    const int r = fwd ? step + 1 : N - 1 - step;
 #pragma unroll
     for (int s = 0; s < SPT; s++) {
       const int m = lane + 32 * s;

@@ -30,7 +30,18 @@ constexpr int kLatticeMinBlocks = BSIDMAP_LATTICE_MIN_BLOCKS;  // resident CTAs 
 struct LaneGeom {
   int f, mi, mp, s, rho;
   bool in, active;
+  uint32_t vmask;  // bit e set iff output k = m_n^- + e is kept (see out_valid)
 };
+
+// Output k = m_n^- + e is kept iff the window is active, n + k >= 0, the window end
+// n(i+1) + m = s + n + k <= rho, and m = m' + k is a trellis state (reading R5):
+// an interval of e, turned into a bit mask once per window.
+__device__ __forceinline__ uint32_t valid_mask(const DecodeParams& p, const LaneGeom& G) {
+  const int e_lo = max(max(0, -p.n - p.mn_lo), p.mt_lo - G.mp - p.mn_lo);
+  const int e_hi = min(min(p.Mn - 1, G.rho - G.s - p.n - p.mn_lo), p.mt_hi - G.mp - p.mn_lo);
+  if (!G.active || e_hi < e_lo) return 0u;
+  return ((2u << e_hi) - 1u) & ~((1u << e_lo) - 1u);
+}
 
 __device__ __forceinline__ LaneGeom lane_geom_at(const DecodeParams& p, int i, long g) {
   LaneGeom G;
@@ -41,6 +52,7 @@ __device__ __forceinline__ LaneGeom lane_geom_at(const DecodeParams& p, int i, l
   G.s = p.n * i + G.mp;                  // window start n i + m' (eqn:gamma)
   G.rho = G.in ? p.rho[G.f] : 0;
   G.active = G.in && p.status[G.f] == kFrameOk && G.s >= 0 && G.s <= G.rho;
+  G.vmask = valid_mask(p, G);
   return G;
 }
 
@@ -48,12 +60,8 @@ __device__ __forceinline__ LaneGeom lane_geom(const DecodeParams& p, int i) {
   return lane_geom_at(p, i, (long)blockIdx.x * blockDim.x + threadIdx.x);
 }
 
-// Output k = m_n^- + e is kept iff the window end n(i+1)+m lies in [s, rho]
-// and m = m' + k is a trellis state (reading R5).
-__device__ __forceinline__ bool out_valid(const DecodeParams& p, const LaneGeom& G, int e) {
-  const int k = p.mn_lo + e;
-  const int m = G.mp + k;
-  return G.active && (p.n + k >= 0) && (G.s + p.n + k <= G.rho) && m >= p.mt_lo && m <= p.mt_hi;
+__device__ __forceinline__ bool out_valid(const DecodeParams&, const LaneGeom& G, int e) {
+  return (G.vmask >> e) & 1u;
 }
 
 template <class Core, bool kStoreGamma>
@@ -99,9 +107,9 @@ __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_su
   }
   if (G.in) {
     const float sc = p.priors ? 1.f : 1.f / p.q;
-    float* out = p.Gsum + ((size_t)G.f * p.N + i) * MN * p.Mt + G.mi;
+    float* out = p.Gsum + ((size_t)G.f * p.N + i) * MN * p.Mtp + G.mi;
 #pragma unroll
-    for (int e = 0; e < MN; e++) out[(size_t)e * p.Mt] = out_valid(p, G, e) ? sc * acc[e] : 0.f;
+    for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, G, e) ? sc * acc[e] : 0.f;
   }
 }
 

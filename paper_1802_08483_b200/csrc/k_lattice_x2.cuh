@@ -34,6 +34,7 @@ __device__ __forceinline__ LaneGeom geom_fm(const DecodeParams& p, int i, int f,
   G.s = p.n * i + G.mp;
   G.rho = in ? p.rho[G.f] : 0;
   G.active = in && p.status[G.f] == kFrameOk && G.s >= 0 && G.s <= G.rho;
+  G.vmask = valid_mask(p, G);
   return G;
 }
 
@@ -48,8 +49,11 @@ __device__ __forceinline__ int exp2_of(double x) {  // floor(log2 x) for normal 
 
 // Pass 1 uses flat geometry: lane t of a CTA owns windows g0 + t and g0 + t + 128
 // (g = f M_tau + m' index, g0 = 256 blockIdx.x) -- no frame alignment needed here.
+#ifndef BSIDMAP_L1_MINB
+#define BSIDMAP_L1_MINB Core::kMinBlocks
+#endif
 template <class Core, bool kStoreGamma>
-__global__ void __launch_bounds__(kLatticeThreads, Core::kMinBlocks) k_gamma_sum_x2(const DecodeParams p) {
+__global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_x2(const DecodeParams p) {
   constexpr int MN = Core::Mn;
   extern __shared__ uint32_t s_C[];
   const int i = blockIdx.y + p.i_base;
@@ -72,7 +76,7 @@ __global__ void __launch_bounds__(kLatticeThreads, Core::kMinBlocks) k_gamma_sum
     for (int D = 0; D < p.q; D++) {
       const f32x2 P = pa ? pk(__ldg(pa + D), __ldg(pb + D)) : pk(1.f, 1.f);
       f32x2 fo[MN];
-      Core::run(lane, s_C[D], p, fo);
+      Core::template run<true>(lane, s_C[D], p, fo);
 #pragma unroll
       for (int e = 0; e < MN; e++) acc[e] = ffma2(P, fo[e], acc[e]);
       if constexpr (kStoreGamma) {
@@ -101,14 +105,14 @@ __global__ void __launch_bounds__(kLatticeThreads, Core::kMinBlocks) k_gamma_sum
   }
   const float sc = p.priors ? 1.f : 1.f / p.q;
   if (A.in) {
-    float* out = p.Gsum + ((size_t)A.f * p.N + i) * MN * p.Mt + A.mi;
+    float* out = p.Gsum + ((size_t)A.f * p.N + i) * MN * p.Mtp + A.mi;
 #pragma unroll
-    for (int e = 0; e < MN; e++) out[(size_t)e * p.Mt] = out_valid(p, A, e) ? sc * lo_of(acc[e]) : 0.f;
+    for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, A, e) ? sc * lo_of(acc[e]) : 0.f;
   }
   if (B.in) {
-    float* out = p.Gsum + ((size_t)B.f * p.N + i) * MN * p.Mt + B.mi;
+    float* out = p.Gsum + ((size_t)B.f * p.N + i) * MN * p.Mtp + B.mi;
 #pragma unroll
-    for (int e = 0; e < MN; e++) out[(size_t)e * p.Mt] = out_valid(p, B, e) ? sc * hi_of(acc[e]) : 0.f;
+    for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, B, e) ? sc * hi_of(acc[e]) : 0.f;
   }
 }
 
@@ -118,10 +122,12 @@ template <int MN>
 __device__ __forceinline__ double app_weights_p2(const DecodeParams& p, const LaneGeom& G, int i, float (&bt)[MN]) {
   double bv[MN];
   double bm = 0.0;
-  const double* brow = p.beta + ((size_t)G.f * (p.N + 1) + (i + 1)) * p.Mt + G.mi + p.mn_lo;
+  const double* brow = p.beta + ((size_t)G.f * (p.N + 1) + (i + 1)) * p.Mt;
+  const int m0 = G.mi + p.mn_lo;
 #pragma unroll
   for (int e = 0; e < MN; e++) {
-    bv[e] = out_valid(p, G, e) ? brow[e] : 0.0;
+    const double v = __ldg(brow + min(max(m0 + e, 0), p.Mt - 1));  // clamped: all loads in flight together
+    bv[e] = ((G.vmask >> e) & 1u) ? v : 0.0;
     bm = fmax(bm, bv[e]);
   }
   const int E = bm > 0.0 ? exp2_of(bm) : 0;
@@ -131,9 +137,17 @@ __device__ __forceinline__ double app_weights_p2(const DecodeParams& p, const La
   return (G.active && bm > 0.0) ? p.alpha[((size_t)G.f * (p.N + 1) + i) * p.Mt + G.mi] * pow2d(E) : 0.0;
 }
 
+// APP pass: 4 CTAs/SM (128 registers, small spills) and single-row issue measured fastest
+// on B200 for C2 (tools/exp_app.sh: 17.3 ms vs 18.0 ms at 3 CTAs/SM with row pairs)
+#ifndef BSIDMAP_APP_MINB
+#define BSIDMAP_APP_MINB (Core::kMinBlocks > 2 ? 4 : 2)
+#endif
+#ifndef BSIDMAP_APP_PAIRS
+#define BSIDMAP_APP_PAIRS false
+#endif
 // smem: s_C[q] | s_S[kX2Warps][q] (float)
 template <class Core>
-__global__ void __launch_bounds__(kLatticeThreads, Core::kMinBlocks) k_app_x2(const DecodeParams p) {
+__global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_APP_MINB) k_app_x2(const DecodeParams p) {
   constexpr int MN = Core::Mn;
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* s_C = reinterpret_cast<uint32_t*>(smem);
@@ -176,7 +190,7 @@ __global__ void __launch_bounds__(kLatticeThreads, Core::kMinBlocks) k_app_x2(co
     const float* pri = p.priors ? p.priors + ((size_t)f * p.N + i) * p.q : nullptr;
     for (int D = 0; D < p.q; D++) {
       f32x2 fo[MN];
-      Core::run(lane_t, s_C[D], p, fo);
+      Core::template run<BSIDMAP_APP_PAIRS>(lane_t, s_C[D], p, fo);
       // t(m', D) = sum_k G(m', k, D) bt(m', k) for both windows (two chains)
       f32x2 t0 = 0ull, t1 = 0ull;
 #pragma unroll

@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(1024) k_alpha_beta(const DecodeParams p) {
   const int Mt = p.Mt, Mn = p.Mn, N = p.N, lo = p.mn_lo;
   const int end_idx = p.rho[f] - p.n * N - p.mt_lo;
   double* rows = (fwd ? p.alpha : p.beta) + (size_t)f * (N + 1) * Mt;
-  const float* Gf = p.Gsum + (size_t)f * N * Mn * Mt;
+  const float* Gf = p.Gsum + (size_t)f * N * Mn * p.Mtp;
 
   const int i0 = fwd ? 0 : N;
   const int boundary = fwd ? -p.mt_lo : end_idx;  // alpha_0 = delta(0), beta_N = delta(rho - tau)
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(1024) k_alpha_beta(const DecodeParams p) {
 
   for (int step = 0; step < N; step++) {
     const int i = fwd ? step : N - 1 - step;  // Gamma_i used by this step
-    const float* G = Gf + (size_t)i * Mn * Mt;  // [k][m']
+    const float* G = Gf + (size_t)i * Mn * p.Mtp;  // [k][m']
     double part = 0.0;
     for (int m = threadIdx.x; m < Mt; m += blockDim.x) {
       // issue all M_n loads of Gamma_i first (independent, one latency per step)
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(1024) k_alpha_beta(const DecodeParams p) {
 #pragma unroll
       for (int e = 0; e < kMaxMn; e++) {
         const int idx = fwd ? m - lo - e : m;  // alpha reads Gamma_i(m - k, k); beta reads Gamma_i(m', k)
-        g[e] = (e < Mn && idx >= 0 && idx < Mt) ? __ldg(G + (size_t)e * Mt + idx) : 0.f;
+        g[e] = (e < Mn && idx >= 0 && idx < Mt) ? __ldg(G + (size_t)e * p.Mtp + idx) : 0.f;
       }
       double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll

@@ -77,22 +77,34 @@ struct SpecCoreX2 {
     }
   }
 
-  template <int R>
+  // Rows are issued in pairs: a 4-way branch on (x_R, x_{R+1}) puts rows R and R+1 in one
+  // basic block so their insertion chains interleave (row R+1 node e needs row R nodes e, e+1).
+  template <int R, bool kPairs>
   __device__ __forceinline__ static void rows(f32x2 (&f)[MN], uint32_t x, const Lane& L, f32x2 a2) {
-    if constexpr (R <= NN) {
+    if constexpr (kPairs && R + 1 <= NN) {
+      switch ((x >> (R - 1)) & 3u) {
+        case 0u: row<R>(f, L.q0, a2); row<R + 1>(f, L.q0, a2); break;
+        case 1u: row<R>(f, L.q1, a2); row<R + 1>(f, L.q0, a2); break;
+        case 2u: row<R>(f, L.q0, a2); row<R + 1>(f, L.q1, a2); break;
+        default: row<R>(f, L.q1, a2); row<R + 1>(f, L.q1, a2); break;
+      }
+      rows<R + 2, kPairs>(f, x, L, a2);
+    } else if constexpr (R <= NN) {
       if ((x >> (R - 1)) & 1u)
         row<R>(f, L.q1, a2);
       else
         row<R>(f, L.q0, a2);
-      rows<R + 1>(f, x, L, a2);
+      rows<R + 1, kPairs>(f, x, L, a2);
     }
   }
 
   // f[e] <- (window a, window b) lattice outputs for k = m_n^- + e (times lc.out_scale)
+  // kPairs: issue rows in pairs (more ILP, more registers)
+  template <bool kPairs = false>
   __device__ __forceinline__ static void run(const Lane& L, uint32_t x, const DecodeParams& p, f32x2 (&f)[MN]) {
 #pragma unroll
     for (int e = 0; e < MN; e++) f[e] = pk(p.lc.row0[e], p.lc.row0[e]);
-    rows<1>(f, x, L, pk(p.lc.a, p.lc.a));
+    rows<1, kPairs>(f, x, L, pk(p.lc.a, p.lc.a));
   }
 
   static constexpr long nodes() { return (long)NN * MN - (long)LO * (LO - 1) / 2; }
