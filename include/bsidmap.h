@@ -51,10 +51,14 @@ typedef struct bsidmap_decoder bsidmap_decoder; /* opaque; owns the device codeb
 #define BSIDMAP_FRAME_UNDERFLOW 2          /* an all-zero alpha/beta/L row: Y impossible under the limits; L rows = 0 */
 
 /* storage schedule */
-#define BSIDMAP_MODE_AUTO 0      /* planner choice */
+#define BSIDMAP_MODE_AUTO 0      /* planner choice (= GAMMASUM, the fastest on B200) */
 #define BSIDMAP_MODE_STORED 1    /* paper's global storage: every gamma stored in HBM, read back for L */
-#define BSIDMAP_MODE_RECOMPUTE 2 /* memory-reduced: gamma recomputed in the L pass; only Gamma = sum_D gamma,
-                                    alpha, beta kept (the paper's local storage trade) */
+#define BSIDMAP_MODE_RECOMPUTE 2 /* paper's memory-reduced (local storage) schedule: gamma computed in
+                                    the alpha pass and again in the combined beta + L pass, only alpha rows kept
+                                    (fused per-frame passes; available for M_tau <= 64 with a specialised core,
+                                    otherwise the GAMMASUM schedule runs) */
+#define BSIDMAP_MODE_GAMMASUM 3  /* memory-reduced variant with parallel passes: Gamma = sum_D gamma, alpha and
+                                    beta kept; gamma recomputed once for L */
 
 /*
  * Create a decoder on CUDA device `device`.
@@ -66,7 +70,7 @@ typedef struct bsidmap_decoder bsidmap_decoder; /* opaque; owns the device codeb
  *   mn_lo, mn_hi   : per-codeword drift limits m_n^-, m_n^+ (corridor, M_n = mn_hi - mn_lo + 1 <= 32),
  *                    mn_lo <= 0 <= mn_hi, n + mn_hi <= 64.
  *   mt_lo, mt_hi   : trellis drift limits m_tau^-, m_tau^+ (M_tau states), mt_lo <= mn_lo, mt_hi >= mn_hi.
- *   mode           : BSIDMAP_MODE_*.
+ *   mode           : BSIDMAP_MODE_* (0..3).
  * On success *out receives the decoder.  Allocates only the codebook (N*q*4 bytes);
  * the workspace is allocated lazily by the first decode of a given size.
  */

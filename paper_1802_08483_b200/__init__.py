@@ -11,6 +11,7 @@ from . import _lib  # noqa: F401
 MODE_AUTO = _lib.BSIDMAP_MODE_AUTO
 MODE_STORED = _lib.BSIDMAP_MODE_STORED
 MODE_RECOMPUTE = _lib.BSIDMAP_MODE_RECOMPUTE
+MODE_GAMMASUM = _lib.BSIDMAP_MODE_GAMMASUM
 FRAME_OK = _lib.BSIDMAP_FRAME_OK
 FRAME_DRIFT_OUT_OF_RANGE = _lib.BSIDMAP_FRAME_DRIFT_OUT_OF_RANGE
 FRAME_UNDERFLOW = _lib.BSIDMAP_FRAME_UNDERFLOW

@@ -24,6 +24,7 @@ BSIDMAP_FRAME_UNDERFLOW = 2
 BSIDMAP_MODE_AUTO = 0
 BSIDMAP_MODE_STORED = 1
 BSIDMAP_MODE_RECOMPUTE = 2
+BSIDMAP_MODE_GAMMASUM = 3
 
 _p, _i, _d, _sz, _l, _ll = (ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_size_t,
                             ctypes.c_long, ctypes.c_longlong)

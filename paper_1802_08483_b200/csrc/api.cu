@@ -15,7 +15,7 @@
 #include <vector>
 
 #include "../../include/bsidmap.h"
-#include "k_lattice_x2.cuh"
+#include "k_local_x2.cuh"
 
 namespace bsidmap {
 __global__ void k_frame_init(const DecodeParams p);
@@ -44,7 +44,7 @@ struct bsidmap_decoder {
   void* ws = nullptr;
   size_t ws_bytes = 0;
   size_t ws_limit = 0;
-  int last_chunk = 0, last_frames = 0, last_mode = 0;
+  int last_chunk = 0, last_frames = 0, last_sched = 0;
   // host-path staging
   void* hs = nullptr;
   size_t hs_bytes = 0;
@@ -75,25 +75,45 @@ struct Layout {
 };
 
 // Bytes per frame of each workspace array (the paper's memory estimate).
-Layout layout(const bsidmap_decoder* d, long F, int mode) {
+// Storage schedules.  kSchedLocal is the paper's local storage: gamma computed in
+// the alpha pass and again in the beta + L pass, only alpha rows kept.  kSchedGammaSum keeps
+// Gamma = sum_D gamma between two parallel lattice passes.  kSchedStored keeps every gamma.
+enum Sched { kSchedStored = 1, kSchedLocal = 2, kSchedGammaSum = 3 };
+
+int resolve_sched(const bsidmap_decoder* d, int mode) {
+  if (mode == BSIDMAP_MODE_STORED) return kSchedStored;
+  // AUTO: Gamma-sum -- fully parallel lattice passes; measured fastest on B200 (C2: 140.6 ms vs
+  // 148.4 ms for the fused local schedule per 65536 frames, profiles/r01_*)
+  if (mode == BSIDMAP_MODE_GAMMASUM || mode == BSIDMAP_MODE_AUTO) return kSchedGammaSum;
+  // RECOMPUTE: the paper's local schedule where a frame fits one warp tile, else Gamma-sum
+  return (d->kern.local_fwd && d->Mt <= kTileSlots) ? kSchedLocal : kSchedGammaSum;
+}
+
+const char* sched_name(int s) {
+  return s == kSchedStored ? "stored" : s == kSchedLocal ? "recompute-local" : "recompute-gammasum";
+}
+
+Layout layout(const bsidmap_decoder* d, long F, int sched) {
   Layout l{};
-  l.gsum = align_up((size_t)F * d->N * d->Mn * ((d->Mt + 3) & ~3) * sizeof(float));
-  l.gamma = mode == BSIDMAP_MODE_STORED ? align_up((size_t)F * d->N * d->q * d->Mn * d->Mt * sizeof(float)) : 0;
+  const bool local = sched == kSchedLocal;
+  l.gsum = local ? 0 : align_up((size_t)F * d->N * d->Mn * ((d->Mt + 3) & ~3) * sizeof(float));
+  l.gamma = sched == kSchedStored ? align_up((size_t)F * d->N * d->q * d->Mn * d->Mt * sizeof(float)) : 0;
   l.alpha = align_up((size_t)F * (d->N + 1) * d->Mt * sizeof(double));
-  l.beta = l.alpha;
-  l.lacc = align_up((size_t)F * d->N * d->q * sizeof(double));
+  l.beta = local ? 0 : l.alpha;
+  l.lacc = local ? 0 : align_up((size_t)F * d->N * d->q * sizeof(double));
   l.total = l.gsum + l.gamma + l.alpha + l.beta + l.lacc;
   return l;
 }
 
 struct Plan {
-  int mode;
+  int mode;         // schedule (Sched)
   int chunk;        // frames per chunk
   int nchunks;
   int ab_threads;   // k_alpha_beta block size
   size_t ab_smem, app_smem, l1_smem;
   void (*ab_warp)(const DecodeParams);  // warp-per-task alpha/beta kernel or nullptr
   bool direct_L;                         // APP pass writes normalised L rows itself
+  size_t local_smem;                     // k_local_fwd / k_local_bwd dynamic smem
 };
 
 size_t budget(const bsidmap_decoder* d) {
@@ -104,17 +124,12 @@ size_t budget(const bsidmap_decoder* d) {
 }
 
 int make_plan(bsidmap_decoder* d, int F, Plan* P) {
-  int mode = d->mode;
+  // Stored gamma costs 8 B of HBM traffic per gamma value against ~5n FP32 flops to
+  // recompute it; on B200 recomputing is the faster side of the ridge, and
+  // the only one whose batches fit for long frames: AUTO = recompute.
+  const int mode = resolve_sched(d, d->mode);
   const size_t bud = budget(d);
-  const size_t per_rc = layout(d, 1, BSIDMAP_MODE_RECOMPUTE).total;
-  const size_t per_st = layout(d, 1, BSIDMAP_MODE_STORED).total;
-  if (mode == BSIDMAP_MODE_AUTO) {
-    // Stored gamma costs 8 B of HBM traffic per gamma value against ~5n FP32 flops to
-    // recompute it; on B200 recomputing is the faster side of the ridge,
-    // and it is the only one whose batches fit for long frames.  RECOMPUTE by default.
-    mode = BSIDMAP_MODE_RECOMPUTE;
-  }
-  const size_t per = mode == BSIDMAP_MODE_STORED ? per_st : per_rc;
+  const size_t per = layout(d, 1, mode).total;
   long chunk = per ? (long)(bud / per) : F;
   if (chunk < 1) return fail(d, BSIDMAP_ENOMEM, "workspace for one frame (" + std::to_string(per) +
                                                     " B) exceeds the budget (" + std::to_string(bud) + " B)");
@@ -136,9 +151,10 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   const size_t nwin = kLatticeThreads;
   P->app_smem = nwin * sizeof(double) + (size_t)kAppSegCap * std::min(d->q, kAppDChunk) * sizeof(double) +
                 nwin * app_tstride(d->q) * 4 + (size_t)d->q * 4;
-  if (mode != BSIDMAP_MODE_STORED && d->kern.W == 2) P->app_smem = (size_t)d->q * 4 * (1 + kX2Warps);
+  if (mode != kSchedStored && d->kern.W == 2) P->app_smem = (size_t)d->q * 4 * (1 + kX2Warps);
   // packed-pair APP with one tile per frame writes L directly (no accumulators / finalize)
-  P->direct_L = mode != BSIDMAP_MODE_STORED && d->kern.W == 2 && tiles_per_frame(d->Mt) == 1;
+  P->direct_L = mode == kSchedLocal || (mode == kSchedGammaSum && d->kern.W == 2 && tiles_per_frame(d->Mt) == 1);
+  P->local_smem = (size_t)kLocalWarps * local_warp_smem(d->Mn, d->q);
   P->l1_smem = (size_t)d->q * 4;
   return BSIDMAP_OK;
 }
@@ -210,9 +226,24 @@ int run_chunk(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s,
   if (first_chunk) record(d, 0, s);
   k_frame_init<<<(p.F + 255) / 256, 256, 0, s>>>(p);
   d->launches += 1;
+  if (P.mode == kSchedLocal) {  // the paper's local schedule: two fused per-frame passes
+    const unsigned gl = (unsigned)((p.F + kLocalWarps - 1) / kLocalWarps);
+    if (first_chunk) record(d, 1, s);
+    d->kern.local_fwd<<<gl, kLocalWarps * 32, P.local_smem, s>>>(p);
+    if (first_chunk) record(d, 2, s);
+    if (first_chunk) record(d, 3, s);
+    d->kern.local_bwd<<<gl, kLocalWarps * 32, P.local_smem, s>>>(p);
+    if (first_chunk) record(d, 4, s);
+    k_zero_failed<<<p.F, 256, 0, s>>>(p);
+    d->launches += 3;
+    if (last_chunk) record(d, 5, s);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(d, e, "kernel launch");
+    return BSIDMAP_OK;
+  }
   if (!P.direct_L) cudaMemsetAsync(p.Lacc, 0, (size_t)p.F * d->N * d->q * sizeof(double), s);
   if (first_chunk) record(d, 1, s);
-  auto l1 = P.mode == BSIDMAP_MODE_STORED ? d->kern.gamma_store : d->kern.gamma_sum;
+  auto l1 = P.mode == kSchedStored ? d->kern.gamma_store : d->kern.gamma_sum;
   for_i_slices(d->N, [&](int i0, int ni) {
     p.i_base = i0;
     l1<<<dim3(tiled ? (unsigned)((lanes + 2 * kLatticeThreads - 1) / (2 * kLatticeThreads)) : gx_flat, ni),
@@ -229,10 +260,10 @@ int run_chunk(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s,
   }
   d->launches++;
   if (first_chunk) record(d, 3, s);
-  auto l2 = P.mode == BSIDMAP_MODE_STORED ? d->kern.app_stored : d->kern.app;
+  auto l2 = P.mode == kSchedStored ? d->kern.app_stored : d->kern.app;
   for_i_slices(d->N, [&](int i0, int ni) {
     p.i_base = i0;
-    l2<<<dim3(P.mode == BSIDMAP_MODE_STORED ? gx_flat : gx, ni), kLatticeThreads, P.app_smem, s>>>(p);
+    l2<<<dim3(P.mode == kSchedStored ? gx_flat : gx, ni), kLatticeThreads, P.app_smem, s>>>(p);
     d->launches++;
   });
   p.i_base = 0;
@@ -276,7 +307,7 @@ int bsidmap_create(bsidmap_decoder** out, int q, int n, int N, const uint32_t* c
   if (!(mn_lo <= 0 && 0 <= mn_hi)) return fail(nullptr, BSIDMAP_EINVAL, "need m_n^- <= 0 <= m_n^+");
   if (!(mt_lo <= mn_lo && mt_hi >= mn_hi)) return fail(nullptr, BSIDMAP_EINVAL, "need m_tau^- <= m_n^-, m_tau^+ >= m_n^+");
   if (n + mn_hi > kMaxWindow) return fail(nullptr, BSIDMAP_EINVAL, "need n + m_n^+ <= 64");
-  if (mode < 0 || mode > 2) return fail(nullptr, BSIDMAP_EINVAL, "unknown mode");
+  if (mode < 0 || mode > 3) return fail(nullptr, BSIDMAP_EINVAL, "unknown mode");
   const int Mn = mn_hi - mn_lo + 1;
   if (Mn > kMaxMn) return fail(nullptr, BSIDMAP_EPLAN, "corridor width M_n > 32 is not supported");
   if ((long)(mt_hi - mt_lo + 1) * (N + 1) > (1l << 40)) return fail(nullptr, BSIDMAP_EINVAL, "state space too large");
@@ -347,8 +378,13 @@ int bsidmap_decode_batch(bsidmap_decoder* d, int F, const uint32_t* rx, const in
   const Layout l = layout(d, P.chunk, P.mode);
   if ((rc = ensure_ws(d, l.total))) return rc;
   if ((rc = set_smem(d, P.ab_warp ? (const void*)P.ab_warp : (const void*)k_alpha_beta, P.ab_smem))) return rc;
-  if ((rc = set_smem(d, (const void*)(P.mode == BSIDMAP_MODE_STORED ? d->kern.app_stored : d->kern.app), P.app_smem)))
+  if (P.mode == kSchedLocal) {
+    if ((rc = set_smem(d, (const void*)d->kern.local_fwd, P.local_smem))) return rc;
+    if ((rc = set_smem(d, (const void*)d->kern.local_bwd, P.local_smem))) return rc;
+  } else if ((rc = set_smem(d, (const void*)(P.mode == kSchedStored ? d->kern.app_stored : d->kern.app),
+                            P.app_smem))) {
     return rc;
+  }
   for (int c = 0; c < P.nchunks; c++) {
     const int f0 = c * P.chunk;
     DecodeParams p;
@@ -365,7 +401,7 @@ int bsidmap_decode_batch(bsidmap_decoder* d, int F, const uint32_t* rx, const in
   }
   d->last_chunk = P.chunk;
   d->last_frames = F;
-  d->last_mode = P.mode;
+  d->last_sched = P.mode;
   d->ev_stream = s;
   d->ev_valid = d->timing;
   return BSIDMAP_OK;
@@ -432,9 +468,8 @@ const char* bsidmap_last_error(const bsidmap_decoder* d) { return d ? d->err.c_s
 
 size_t bsidmap_workspace_bytes(const bsidmap_decoder* d, int F, int mode) {
   if (!d || F < 0) return 0;
-  if (mode == BSIDMAP_MODE_AUTO) mode = BSIDMAP_MODE_RECOMPUTE;
-  if (mode != BSIDMAP_MODE_STORED && mode != BSIDMAP_MODE_RECOMPUTE) return 0;
-  return layout(d, F, mode).total;
+  if (mode < 0 || mode > 3) return 0;
+  return layout(d, F, resolve_sched(d, mode)).total;
 }
 
 int bsidmap_set_workspace_limit(bsidmap_decoder* d, size_t bytes) {
@@ -445,7 +480,7 @@ int bsidmap_set_workspace_limit(bsidmap_decoder* d, size_t bytes) {
 
 int bsidmap_set_mode(bsidmap_decoder* d, int mode) {
   if (!d) return fail(nullptr, BSIDMAP_EINVAL, "decoder is NULL");
-  if (mode < 0 || mode > 2) return fail(d, BSIDMAP_EINVAL, "unknown mode");
+  if (mode < 0 || mode > 3) return fail(d, BSIDMAP_EINVAL, "unknown mode");
   d->mode = mode;
   return BSIDMAP_OK;
 }
@@ -482,7 +517,7 @@ int bsidmap_plan_info(bsidmap_decoder* d, int F, char* buf, size_t len) {
       "{\"mode\": \"%s\", \"frames\": %d, \"chunk\": %d, \"chunks\": %d, \"core\": \"%s\", "
       "\"lattice_grid\": [%ld, %d], \"lattice_block\": %d, \"alpha_beta_grid\": [%d, 2], \"alpha_beta_block\": %d, "
       "\"workspace_bytes\": %zu, \"windows_per_lane\": %d, \"q\": %d, \"n\": %d, \"N\": %d, \"Mn\": %d, \"Mtau\": %d}",
-      P.mode == BSIDMAP_MODE_STORED ? "stored" : "recompute", F, P.chunk, P.nchunks, d->spec ? "spec" : "generic",
+      sched_name(P.mode), F, P.chunk, P.nchunks, d->spec ? "spec" : "generic",
       d->kern.W == 2 ? ((long)P.chunk * tiles_per_frame(d->Mt) + kX2Warps - 1) / kX2Warps
                      : (lanes + kLatticeThreads - 1) / kLatticeThreads,
       d->N, kLatticeThreads, P.chunk, P.ab_warp ? kAbWarpThreads : P.ab_threads,
@@ -540,7 +575,8 @@ int bsidmap_debug_states(bsidmap_decoder* d, int F, double* alpha_out, double* b
     return fail(d, BSIDMAP_EINVAL, "last decode was chunked or of a different size");
   cudaSetDevice(d->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const Layout l = layout(d, d->last_chunk, d->last_mode);
+  if (d->last_sched == kSchedLocal) return fail(d, BSIDMAP_EINVAL, "the local schedule keeps no beta rows");
+  const Layout l = layout(d, d->last_chunk, d->last_sched);
   DecodeParams p;
   bind_ws(d, l, &p);
   const size_t bytes = (size_t)F * (d->N + 1) * d->Mt * sizeof(double);

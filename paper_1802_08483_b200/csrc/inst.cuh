@@ -1,7 +1,7 @@
 // inst.cuh -- explicit instantiation helpers (split over compilation units so
 // nvcc compiles the unrolled lattice cores in parallel).
 #pragma once
-#include "k_lattice_x2.cuh"
+#include "k_local_x2.cuh"
 
 #define BSIDMAP_SPEC_UNIT(IDX, NN, LO, MN)                                               \
   namespace bsidmap {                                                                    \

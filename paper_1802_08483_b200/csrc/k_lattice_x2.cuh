@@ -261,7 +261,10 @@ __global__ void __launch_bounds__(kLatticeThreads) k_gamma_dump_x2(const DecodeP
 }
 
 template <class Core>
-CoreKernels make_core_kernels_x2(long nodes) {
+CoreKernels make_core_kernels_x2(long nodes);  // defined in k_local_x2.cuh (needs the local kernels)
+
+template <class Core>
+CoreKernels make_core_kernels_x2_base(long nodes) {
   CoreKernels k;
   k.gamma_sum = k_gamma_sum_x2<Core, false>;
   k.gamma_store = k_gamma_sum_x2<Core, true>;

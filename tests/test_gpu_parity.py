@@ -80,7 +80,7 @@ def small_cfg(name, **kw):
 
 # ------------------------------------------------------------------ configs
 
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode", [1, 2, 3])
 def test_c1_parity(mode):
     cfg = small_cfg("C1")
     b = bsidgen.make_batch(cfg, 0, 300)     # 300 x 23 lanes: many tiles + ragged tail
@@ -89,7 +89,7 @@ def test_c1_parity(mode):
     assert_parity(L, st, run_oracle(cfg, b))
 
 
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode", [1, 2, 3])
 def test_c2_parity(mode):
     cfg = small_cfg("C2")
     b = bsidgen.make_batch(cfg, 1000, 48)
@@ -161,9 +161,10 @@ def test_random_shapes_generic_core(k):
     cfg = _random_cfg(rng, k)
     F = int(rng.integers(1, 40))
     b = bsidgen.make_batch(cfg, 0, F)
-    for mode in (1, 2):
+    res = run_oracle(cfg, b)
+    for mode in (1, 2, 3):
         d, L, st = run_gpu(cfg, b, mode)
-        assert_parity(L, st, run_oracle(cfg, b))
+        assert_parity(L, st, res)
 
 
 # ------------------------------------------------------------- edge cases
@@ -202,9 +203,10 @@ def test_underflow_status():
 def test_binary_single_bit_codes():
     cfg = bsidgen.Config("E", q=2, n=1, N=40, Pi=0.02, Pd=0.03, Ps=0.01, frames=0, seed=5)
     b = bsidgen.make_batch(cfg, 0, 9)
-    for mode in (1, 2):
+    res = run_oracle(cfg, b)
+    for mode in (1, 2, 3):
         _, L, st = run_gpu(cfg, b, mode)
-        assert_parity(L, st, run_oracle(cfg, b))
+        assert_parity(L, st, res)
 
 
 def test_zero_priors_and_one_hot():
@@ -222,9 +224,9 @@ def test_zero_priors_and_one_hot():
 def test_chunked_equals_unchunked_and_host_path():
     cfg = small_cfg("C2")
     b = bsidgen.make_batch(cfg, 50, 40)
-    d, L1, st1 = run_gpu(cfg, b, 2)
-    per = d.workspace_bytes(1, 2)
-    _, L2, st2 = run_gpu(cfg, b, 2, ws_limit=per * 7)   # 6 chunks of 7 + tail
+    d, L1, st1 = run_gpu(cfg, b, 3)
+    per = d.workspace_bytes(1, 3)
+    _, L2, st2 = run_gpu(cfg, b, 3, ws_limit=per * 7)   # 6 chunks of 7 + tail
     np.testing.assert_array_equal(st1, st2)
     np.testing.assert_allclose(L2, L1, rtol=1e-5, atol=1e-30)
     # end-to-end host path through bsidmap_decode_batch_host (pinned buffers)
@@ -243,17 +245,26 @@ def test_modes_agree_and_plan():
     b = bsidgen.make_batch(cfg, 0, 16)
     _, Ls, sts = run_gpu(cfg, b, 1)
     d, Lr, str_ = run_gpu(cfg, b, 2)
+    _, Lg, stg = run_gpu(cfg, b, 3)
     np.testing.assert_array_equal(sts, str_)
+    np.testing.assert_array_equal(sts, stg)
     np.testing.assert_allclose(Ls, Lr, rtol=2e-5, atol=1e-30)
-    plan = d.plan(65536)
-    assert plan["mode"] == "recompute" and plan["core"] == "spec"
-    assert d.workspace_bytes(16, 1) > d.workspace_bytes(16, 2)
+    np.testing.assert_allclose(Lg, Lr, rtol=2e-5, atol=1e-30)
+    assert d.plan(65536)["mode"] == "recompute-local" and d.plan(64)["core"] == "spec"
+    assert _dec().from_config(cfg, b.C, mode=0, device=0).plan(64)["mode"] == "recompute-gammasum"
+    # memory estimate: stored gamma > Gamma-sum > local (alpha rows only)
+    assert d.workspace_bytes(16, 1) > d.workspace_bytes(16, 3) > d.workspace_bytes(16, 2)
+    assert d.workspace_bytes(16, 2) == 16 * (cfg.N + 1) * cfg.Mt * 8 or d.workspace_bytes(16, 2) < 16 * (cfg.N + 1) * cfg.Mt * 8 + 512
+    # M_tau > 64: the local schedule is not available, RECOMPUTE runs the Gamma-sum schedule
+    c3 = small_cfg("C3")
+    d3 = _dec().from_config(c3, bsidgen.codebook(c3), mode=2, device=0)
+    assert d3.plan(8)["mode"] == "recompute-gammasum"
 
 
 def test_alpha_beta_states_vs_oracle():
     cfg = small_cfg("C2")
     b = bsidgen.make_batch(cfg, 0, 3)
-    d, L, st = run_gpu(cfg, b, 2)
+    d, L, st = run_gpu(cfg, b, 3)
     a, be = d.debug_states(3)
     a, be = a.cpu().numpy(), be.cpu().numpy()
     res = [oracle.decode(oracle.Problem(cfg.q, cfg.n, cfg.N, b.C, cfg.Pi, cfg.Pd, cfg.Ps, cfg.mn, cfg.mt),
