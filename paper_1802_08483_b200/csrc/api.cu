@@ -19,7 +19,8 @@
 
 namespace bsidmap {
 __global__ void k_frame_init(const DecodeParams p);
-__global__ void k_alpha_beta(const DecodeParams p);
+__global__ void k_alpha_beta(const DecodeParams p, int stages);
+size_t ab_cta_smem(int Mn, int Mtp, int stages);
 __global__ void k_finalize(const DecodeParams p);
 __global__ void k_zero_failed(const DecodeParams p);
 }  // namespace bsidmap
@@ -110,6 +111,7 @@ struct Plan {
   int chunk;        // frames per chunk
   int nchunks;
   int ab_threads;   // k_alpha_beta block size
+  int ab_stages;    // k_alpha_beta TMA ring depth
   size_t ab_smem, app_smem, l1_smem;
   void (*ab_warp)(const DecodeParams);  // warp-per-task alpha/beta kernel or nullptr
   bool direct_L;                         // APP pass writes normalised L rows itself
@@ -138,7 +140,14 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   P->chunk = (int)chunk;
   P->nchunks = (int)((F + chunk - 1) / chunk);
   P->ab_threads = std::min(1024, ((d->Mt + 31) / 32) * 32);
-  P->ab_smem = (2 * (size_t)d->Mt + 33) * sizeof(double);
+  {  // TMA ring depth: up to 4 stages of Gamma_i blocks within ~200 KB of shared memory
+    const int Mtp = (d->Mt + 3) & ~3;
+    const size_t blk = (size_t)d->Mn * Mtp * 4;
+    P->ab_stages = (int)std::max<size_t>(1, std::min<size_t>(4, (200u * 1024 - 2 * (size_t)Mtp * 8 - 600) / blk));
+    P->ab_smem = ab_cta_smem(d->Mn, Mtp, P->ab_stages);
+    if (mode != kSchedLocal && P->ab_smem > 227u * 1024)
+      return fail(d, BSIDMAP_EPLAN, "M_n x M_tau too large for the shared-memory Gamma ring of the alpha/beta kernel");
+  }
   P->ab_warp = nullptr;
   const int spt = (d->Mt + 31) / 32;
   const int spt_k = spt == 3 ? 4 : spt;
@@ -151,7 +160,7 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   const size_t nwin = kLatticeThreads;
   P->app_smem = nwin * sizeof(double) + (size_t)kAppSegCap * std::min(d->q, kAppDChunk) * sizeof(double) +
                 nwin * app_tstride(d->q) * 4 + (size_t)d->q * 4;
-  if (mode != kSchedStored && d->kern.W == 2) P->app_smem = (size_t)d->q * 4 * (1 + kX2Warps);
+  if (mode != kSchedStored && d->kern.W == 2) P->app_smem = app_x2_smem(d->q, d->Mn);
   // packed-pair APP with one tile per frame writes L directly (no accumulators / finalize)
   P->direct_L = mode == kSchedLocal || (mode == kSchedGammaSum && d->kern.W == 2 && tiles_per_frame(d->Mt) == 1);
   P->local_smem = (size_t)kLocalWarps * local_warp_smem(d->Mn, d->q);
@@ -256,7 +265,7 @@ int run_chunk(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s,
     const long tasks = 2L * p.F, per = kAbWarpThreads / 32;
     P.ab_warp<<<(unsigned)((tasks + per - 1) / per), kAbWarpThreads, P.ab_smem, s>>>(p);
   } else {
-    k_alpha_beta<<<dim3(p.F, 2), P.ab_threads, P.ab_smem, s>>>(p);
+    k_alpha_beta<<<dim3(p.F, 2), P.ab_threads, P.ab_smem, s>>>(p, P.ab_stages);
   }
   d->launches++;
   if (first_chunk) record(d, 3, s);

@@ -195,7 +195,7 @@ __device__ __forceinline__ double app_weights(const DecodeParams& p, const LaneG
 template <class Core>
 __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_app(const DecodeParams p) {
   constexpr int MN = Core::Mn;
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   const int ts = app_tstride(p.q);
   double* s_w = reinterpret_cast<double*>(smem);
   double* s_part = s_w + blockDim.x;
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_app(cons
 // smem: s_w[blockDim] | s_part[kAppSegCap][min(q, kAppDChunk)] | s_t[blockDim][ts]
 template <int MN>
 __global__ void __launch_bounds__(kLatticeThreads) k_app_stored(const DecodeParams p) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   const int ts = app_tstride(p.q);
   double* s_w = reinterpret_cast<double*>(smem);
   double* s_part = s_w + blockDim.x;

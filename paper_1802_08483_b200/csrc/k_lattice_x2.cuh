@@ -52,6 +52,10 @@ __device__ __forceinline__ int exp2_of(double x) {  // floor(log2 x) for normal 
 #ifndef BSIDMAP_L1_MINB
 #define BSIDMAP_L1_MINB Core::kMinBlocks
 #endif
+// row pairs (ILP) in pass 1 only where the register budget allows 3 CTAs/SM
+#ifndef BSIDMAP_L1_PAIRS
+#define BSIDMAP_L1_PAIRS (Core::kMinBlocks > 2)
+#endif
 template <class Core, bool kStoreGamma>
 __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_x2(const DecodeParams p) {
   constexpr int MN = Core::Mn;
@@ -76,7 +80,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_
     for (int D = 0; D < p.q; D++) {
       const f32x2 P = pa ? pk(__ldg(pa + D), __ldg(pb + D)) : pk(1.f, 1.f);
       f32x2 fo[MN];
-      Core::template run<true>(lane, s_C[D], p, fo);
+      Core::template run<BSIDMAP_L1_PAIRS>(lane, s_C[D], p, fo);
 #pragma unroll
       for (int e = 0; e < MN; e++) acc[e] = ffma2(P, fo[e], acc[e]);
       if constexpr (kStoreGamma) {
@@ -137,20 +141,28 @@ __device__ __forceinline__ double app_weights_p2(const DecodeParams& p, const La
   return (G.active && bm > 0.0) ? p.alpha[((size_t)G.f * (p.N + 1) + i) * p.Mt + G.mi] * pow2d(E) : 0.0;
 }
 
-// APP pass: 4 CTAs/SM (128 registers, small spills) and single-row issue measured fastest
-// on B200 for C2 (tools/exp_app.sh: 17.3 ms vs 18.0 ms at 3 CTAs/SM with row pairs)
+// APP pass: 5 CTAs/SM (102 registers; the beta corridor lives in smem) with row pairs measured
+// fastest on B200 for C2 (tools/exp_app.sh: 17.06 ms vs 17.3-18.0 ms for 3-4 CTAs/SM)
 #ifndef BSIDMAP_APP_MINB
-#define BSIDMAP_APP_MINB (Core::kMinBlocks > 2 ? 4 : 2)
+#define BSIDMAP_APP_MINB (Core::kMinBlocks > 2 ? 5 : 2)
 #endif
 #ifndef BSIDMAP_APP_PAIRS
-#define BSIDMAP_APP_PAIRS false
+#define BSIDMAP_APP_PAIRS (Core::kMinBlocks > 2)
 #endif
-// smem: s_C[q] | s_S[kX2Warps][q] (float)
+#ifndef BSIDMAP_APP_BT_SMEM
+#define BSIDMAP_APP_BT_SMEM 1
+#endif
+__host__ __device__ __forceinline__ size_t app_x2_smem(int q, int Mn) {
+  return (size_t)kX2Warps * Mn * 32 * 8 + (size_t)q * 4 * (1 + kX2Warps);
+}
+// smem: s_bt[kX2Warps][M_n][32] (f32x2, the scaled beta corridor of each lane's two windows;
+//       kept in smem, not registers, to free 2 M_n registers) | s_C[q] | s_S[kX2Warps][q] (float)
 template <class Core>
 __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_APP_MINB) k_app_x2(const DecodeParams p) {
   constexpr int MN = Core::Mn;
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* s_C = reinterpret_cast<uint32_t*>(smem);
+  extern __shared__ __align__(128) unsigned char smem[];
+  f32x2* s_bt = reinterpret_cast<f32x2*>(smem);
+  uint32_t* s_C = reinterpret_cast<uint32_t*>(s_bt + kX2Warps * MN * 32);
   float* s_S = reinterpret_cast<float*>(s_C + p.q);
   const int i = blockIdx.y + p.i_base;
   for (int t = threadIdx.x; t < p.q; t += blockDim.x) s_C[t] = p.C[(size_t)i * p.q + t];
@@ -166,14 +178,20 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_APP_MINB) k_app_x2(co
   const LaneGeom B = geom_fm(p, i, f, mia + 1, mia + 1 < p.Mt);
   const bool frame_ok = p.status[f] == kFrameOk;
 
+#if BSIDMAP_APP_BT_SMEM
+  f32x2* bt = s_bt + (size_t)warp * MN * 32 + lane;  // bt[e * 32]
+#define BT(e) bt[(e) * 32]
+#else
   f32x2 bt[MN];
+#define BT(e) bt[e]
+#endif
   float wa, wb;
   int Emax;
   {
     float ba[MN], bb[MN];
     const double da = app_weights_p2<MN>(p, A, i, ba), db = app_weights_p2<MN>(p, B, i, bb);
 #pragma unroll
-    for (int e = 0; e < MN; e++) bt[e] = pk(ba[e], bb[e]);
+    for (int e = 0; e < MN; e++) BT(e) = pk(ba[e], bb[e]);
     // common power-of-two scale of the tile's weights (max exponent over the warp)
     const double dm = fmax(da, db);
     Emax = __reduce_max_sync(0xffffffffu, dm > 0.0 ? exp2_of(dm) + 2048 : 0) - 2048;
@@ -195,8 +213,8 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_APP_MINB) k_app_x2(co
       f32x2 t0 = 0ull, t1 = 0ull;
 #pragma unroll
       for (int e = 0; e < MN; e += 2) {
-        t0 = ffma2(fo[e], bt[e], t0);
-        if (e + 1 < MN) t1 = ffma2(fo[e + 1], bt[e + 1], t1);
+        t0 = ffma2(fo[e], BT(e), t0);
+        if (e + 1 < MN) t1 = ffma2(fo[e + 1], BT(e + 1), t1);
       }
       float c = fmaf(wa, lo_of(t0) + lo_of(t1), wb * (hi_of(t0) + hi_of(t1)));
 #pragma unroll
@@ -204,6 +222,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_APP_MINB) k_app_x2(co
       if (lane == 0) S[D] = pri ? c * __ldg(pri + D) : c;
     }
   }
+#undef BT
   __syncwarp();
   if (T == 1) {
     // the warp holds the whole sum over m': L_i(D) = S(D) / sum_D S(D)

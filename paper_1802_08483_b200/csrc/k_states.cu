@@ -3,7 +3,8 @@
 //
 //   k_frame_init : end drift rho - tau outside [m_tau^-, m_tau^+] -> status
 //                  DRIFT_OUT_OF_RANGE.
-//   k_alpha_beta : a2/a3 -- one CTA per (frame, direction), persistent over i:
+//   k_alpha_beta : a2/a3 -- one CTA per (frame, direction), persistent over i
+//                  (TMA-fed Gamma ring, one barrier per step, see below):
 //                  alpha'_{i+1}(m) = sum_k alpha_i(m-k) Gamma_i(m-k, k)
 //                  (eqn:alpha_prenorm with sum_D folded into Gamma),
 //                  alpha_{i+1} = alpha'/sum_m alpha' (eqn:alpha_norm); the
@@ -16,6 +17,7 @@
 //                  1/lambda_N(rho - tau) of eqn:L in exact arithmetic
 //                  (reading R2); FP32 output.
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace bsidmap {
 
@@ -26,83 +28,96 @@ __global__ void k_frame_init(const DecodeParams p) {
   p.status[f] = (drift >= p.mt_lo && drift <= p.mt_hi) ? kFrameOk : kFrameDriftOutOfRange;
 }
 
-__device__ __forceinline__ double block_sum(double v, double* s_red) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
-  if (lane == 0) s_red[warp] = v;
-  __syncthreads();
-  if (warp == 0) {
-    double t = lane < nw ? s_red[lane] : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (lane == 0) s_red[32] = t;
-  }
-  __syncthreads();
-  return s_red[32];
+// Shared memory of k_alpha_beta: ring[stages][M_n][Mtp] floats | R[2][Mtp] doubles |
+// part[2][32] doubles | bars[stages].
+__host__ __device__ size_t ab_cta_smem(int Mn, int Mtp, int stages) {
+  return (size_t)stages * Mn * Mtp * 4 + 2 * (size_t)Mtp * 8 + 2 * 32 * 8 + (size_t)stages * 8;
 }
 
 // blockIdx.x = frame, blockIdx.y = 0 (alpha, forward) / 1 (beta, backward).
-__global__ void __launch_bounds__(1024) k_alpha_beta(const DecodeParams p) {
-  extern __shared__ __align__(16) double s_st[];  // cur[Mt] | nxt[Mt] | red[33]
-  double* cur = s_st;
-  double* nxt = s_st + p.Mt;
-  double* red = s_st + 2 * p.Mt;
+//
+// One CTA per (frame, direction), persistent over the N steps, ONE block barrier
+// per step: the row is kept unnormalised, R_{i+1} = (1/c_i) sum_k R_i Gamma_i with
+// c_i = sum_m R_i(m) taken from the previous step's per-warp partial sums, and rows
+// are ping-ponged so no thread overwrites a row another thread may still read.  The
+// Gamma_i blocks (M_n x Mtp FP32, contiguous) stream through a `stages`-deep ring
+// via TMA bulk copies (one thread issues, an mbarrier per stage signals arrival).
+__global__ void __launch_bounds__(1024) k_alpha_beta(const DecodeParams p, int stages) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int Mt = p.Mt, Mn = p.Mn, Mtp = p.Mtp, N = p.N, lo = p.mn_lo;
+  float* ring = reinterpret_cast<float*>(smem);
+  double* R = reinterpret_cast<double*>(smem + (size_t)stages * Mn * Mtp * 4);
+  double* part = R + 2 * Mtp;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(part + 64);
   const int f = blockIdx.x;
   const bool fwd = blockIdx.y == 0;
-  if (p.status[f] != kFrameOk) return;
-  const int Mt = p.Mt, Mn = p.Mn, N = p.N, lo = p.mn_lo;
-  const int end_idx = p.rho[f] - p.n * N - p.mt_lo;
+  if (p.status[f] != kFrameOk) return;  // uniform over the CTA
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31, nw = (nt + 31) >> 5;
   double* rows = (fwd ? p.alpha : p.beta) + (size_t)f * (N + 1) * Mt;
-  const float* Gf = p.Gsum + (size_t)f * N * Mn * p.Mtp;
-
+  const float* Gf = p.Gsum + (size_t)f * N * Mn * Mtp;
+  const uint32_t blk = (uint32_t)(Mn * Mtp * 4);
+  auto gblock = [&](int step) { return Gf + (size_t)(fwd ? step : N - 1 - step) * Mn * Mtp; };
+  if (tid == 0) {
+    for (int s = 0; s < stages; s++) mbar_init(bars + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < stages && s < N; s++) {
+      mbar_expect_tx(bars + s, blk);
+      tma_bulk_g2s(ring + (size_t)s * Mn * Mtp, gblock(s), blk, bars + s);
+    }
+  }
+  const int boundary = fwd ? -p.mt_lo : p.rho[f] - p.n * N - p.mt_lo;  // alpha_0 = delta(0), beta_N = delta(rho - tau)
   const int i0 = fwd ? 0 : N;
-  const int boundary = fwd ? -p.mt_lo : end_idx;  // alpha_0 = delta(0), beta_N = delta(rho - tau)
-  for (int m = threadIdx.x; m < Mt; m += blockDim.x) {
+  for (int m = tid; m < Mt; m += nt) {
     const double v = (m == boundary) ? 1.0 : 0.0;
-    cur[m] = v;
+    R[m] = v;
     rows[(size_t)i0 * Mt + m] = v;
   }
   __syncthreads();
-
+  double inv_c = 1.0;  // 1 / sum_m R_cur(m)
   for (int step = 0; step < N; step++) {
-    const int i = fwd ? step : N - 1 - step;  // Gamma_i used by this step
-    const float* G = Gf + (size_t)i * Mn * p.Mtp;  // [k][m']
-    double part = 0.0;
-    for (int m = threadIdx.x; m < Mt; m += blockDim.x) {
-      // issue all M_n loads of Gamma_i first (independent, one latency per step)
-      float g[kMaxMn];
-#pragma unroll
-      for (int e = 0; e < kMaxMn; e++) {
-        const int idx = fwd ? m - lo - e : m;  // alpha reads Gamma_i(m - k, k); beta reads Gamma_i(m', k)
-        g[e] = (e < Mn && idx >= 0 && idx < Mt) ? __ldg(G + (size_t)e * p.Mtp + idx) : 0.f;
+    const int stage = step % stages;
+    mbar_wait(bars + stage, (uint32_t)(step / stages) & 1u);
+    const float* G = ring + (size_t)stage * Mn * Mtp;
+    const double* cur = R + (step & 1) * Mtp;
+    double* nxt = R + ((step + 1) & 1) * Mtp;
+    double ps = 0.0;
+    for (int m = tid; m < Mt; m += nt) {
+      double a0 = 0.0, a1 = 0.0;
+      for (int e = 0; e < Mn; e++) {
+        // alpha: R(m - k) Gamma_i(m - k, k); beta: Gamma_i(m', k) R(m' + k)
+        const int j = fwd ? m - lo - e : m + lo + e;
+        const int idx = fwd ? j : m;
+        if (j >= 0 && j < Mt) {
+          const double t = cur[j] * (double)G[e * Mtp + idx];
+          if (e & 1) a1 += t; else a0 += t;
+        }
       }
-      double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-      for (int e = 0; e < kMaxMn; e += 2) {
-        // alpha'_{i+1}(m) = sum_k alpha_i(m - k) Gamma_i(m - k, k);  beta'_i(m') = sum_k Gamma_i(m', k) beta_{i+1}(m' + k)
-        const int j0 = fwd ? m - lo - e : m + lo + e;
-        const int j1 = fwd ? j0 - 1 : j0 + 1;
-        if (e < Mn && j0 >= 0 && j0 < Mt) acc0 = fma(cur[j0], (double)g[e], acc0);
-        if (e + 1 < Mn && j1 >= 0 && j1 < Mt) acc1 = fma(cur[j1], (double)g[e + 1], acc1);
-      }
-      const double acc = acc0 + acc1;
-      nxt[m] = acc;
-      part += acc;
+      const double v = (a0 + a1) * inv_c;
+      nxt[m] = v;
+      ps += v;
     }
-    const double c = block_sum(part, red);
-    const int row = fwd ? i + 1 : i;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+    double* pp = part + ((step + 1) & 1) * 32;
+    if (lane == 0) pp[warp] = ps;
+    __syncthreads();  // nxt and the partials are complete; the ring stage is consumed
+    if (tid == 0 && step + stages < N) {
+      mbar_expect_tx(bars + stage, blk);
+      tma_bulk_g2s(ring + (size_t)stage * Mn * Mtp, gblock(step + stages), blk, bars + stage);
+    }
+    double c = 0.0;
+    for (int w = 0; w < nw; w++) c += pp[w];
     if (!(c > 0.0)) {  // all-zero row: Y impossible under the limits (reading R14)
-      if (threadIdx.x == 0) p.status[f] = kFrameUnderflow;
+      if (tid == 0) {
+        p.status[f] = kFrameUnderflow;
+        for (int t = step + 1; t < N && t <= step + stages; t++)  // drain issued copies
+          mbar_wait(bars + t % stages, (uint32_t)(t / stages) & 1u);
+      }
       return;
     }
-    const double inv = 1.0 / c;
-    for (int m = threadIdx.x; m < Mt; m += blockDim.x) {
-      const double v = nxt[m] * inv;
-      cur[m] = v;
-      rows[(size_t)row * Mt + m] = v;
-    }
-    __syncthreads();
+    inv_c = 1.0 / c;
+    const int r = fwd ? step + 1 : N - 1 - step;
+    for (int m = tid; m < Mt; m += nt) rows[(size_t)r * Mt + m] = nxt[m] * inv_c;  // eqn:alpha_norm
   }
 }
 
