@@ -255,7 +255,7 @@ int run_chunk(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s,
   auto l1 = P.mode == kSchedStored ? d->kern.gamma_store : d->kern.gamma_sum;
   for_i_slices(d->N, [&](int i0, int ni) {
     p.i_base = i0;
-    l1<<<dim3(tiled ? (unsigned)((lanes + 2 * kLatticeThreads - 1) / (2 * kLatticeThreads)) : gx_flat, ni),
+    l1<<<dim3(d->kern.l1_W == 2 ? (unsigned)((lanes + 2 * kLatticeThreads - 1) / (2 * kLatticeThreads)) : gx_flat, ni),
          kLatticeThreads, P.l1_smem, s>>>(p);
     d->launches++;
   });

@@ -8,6 +8,11 @@
   bool spec_unit_##IDX(int n, int lo, int Mn, CoreKernels* out) {                        \
     if (n != NN || lo != LO || Mn != MN) return false;                                   \
     *out = make_core_kernels_x2<SpecCoreX2<NN, LO, MN>>(SpecCoreX2<NN, LO, MN>::nodes()); \
+    if (SpecCoreX2<NN, LO, MN>::kMinBlocks <= 2 && MN <= 20) { /* measured: scalar pass 1 wins (C3, C5) */ \
+      out->gamma_sum = k_gamma_sum<SpecCore<NN, LO, MN>, false>;                        \
+      out->gamma_store = k_gamma_sum<SpecCore<NN, LO, MN>, true>;                       \
+      out->l1_W = 1;                                                                    \
+    }                                                                                   \
     return true;                                                                         \
   }                                                                                      \
   }

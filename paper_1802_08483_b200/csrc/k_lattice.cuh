@@ -303,6 +303,7 @@ struct CoreKernels {
   void (*gamma_dump)(const DecodeParams);
   long nodes;  // corridor nodes per lattice (0 = generic core: computed on host)
   int W;       // windows per lane (1 scalar core, 2 packed-pair core)
+  int l1_W;    // windows per lane of the pass-1 kernel (the scalar core may serve pass 1 of a pair core)
   void (*ab_warp[3])(const DecodeParams);  // warp-per-task alpha/beta for M_tau <= 32, 64, 128 (spec only)
   void (*local_fwd)(const DecodeParams);   // fused local schedule, M_tau <= 64 (spec only)
   void (*local_bwd)(const DecodeParams);
@@ -318,6 +319,7 @@ CoreKernels make_core_kernels(long nodes) {
   k.gamma_dump = k_gamma_dump<Core>;
   k.nodes = nodes;
   k.W = 1;
+  k.l1_W = 1;
   k.ab_warp[0] = k.ab_warp[1] = k.ab_warp[2] = nullptr;
   k.local_fwd = k.local_bwd = nullptr;
   return k;

@@ -292,6 +292,7 @@ CoreKernels make_core_kernels_x2_base(long nodes) {
   k.gamma_dump = k_gamma_dump_x2<Core>;
   k.nodes = nodes;
   k.W = 2;
+  k.l1_W = 2;
   k.ab_warp[0] = k_alpha_beta_warp<1, Core::Mn>;
   k.ab_warp[1] = k_alpha_beta_warp<2, Core::Mn>;
   k.ab_warp[2] = k_alpha_beta_warp<4, Core::Mn>;
