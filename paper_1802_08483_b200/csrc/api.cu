@@ -49,6 +49,11 @@ struct bsidmap_decoder {
   // host-path staging
   void* hs = nullptr;
   size_t hs_bytes = 0;
+  // host-side caches: the free-memory query and the smem opt-ins cost ~1 ms per call,
+  // which would dominate single-frame latency (C1)
+  size_t budget_cache = 0;
+  int budget_frames = -1, budget_mode = -1;
+  std::vector<std::pair<const void*, size_t>> smem_set;
   // timing
   bool timing = false;
   cudaEvent_t ev[kPhases + 1] = {};
@@ -125,13 +130,24 @@ size_t budget(const bsidmap_decoder* d) {
   return (size_t)((double)(fr + d->ws_bytes) * 0.85);
 }
 
+// Budget for a plan of F frames: re-query free memory only when the request changes or the
+// current workspace is too small (the query is a synchronous driver call).
+size_t budget_for(bsidmap_decoder* d, int F, int mode, size_t need) {
+  if (d->ws_limit) return d->ws_limit;
+  if (d->budget_frames == F && d->budget_mode == mode && need <= d->ws_bytes) return d->budget_cache;
+  d->budget_cache = budget(d);
+  d->budget_frames = F;
+  d->budget_mode = mode;
+  return d->budget_cache;
+}
+
 int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   // Stored gamma costs 8 B of HBM traffic per gamma value against ~5n FP32 flops to
   // recompute it; on B200 recomputing is the faster side of the ridge, and
   // the only one whose batches fit for long frames: AUTO = recompute.
   const int mode = resolve_sched(d, d->mode);
-  const size_t bud = budget(d);
   const size_t per = layout(d, 1, mode).total;
+  const size_t bud = budget_for(d, F, mode, layout(d, F, mode).total);
   long chunk = per ? (long)(bud / per) : F;
   if (chunk < 1) return fail(d, BSIDMAP_ENOMEM, "workspace for one frame (" + std::to_string(per) +
                                                     " B) exceeds the budget (" + std::to_string(bud) + " B)");
@@ -187,8 +203,11 @@ int ensure_ws(bsidmap_decoder* d, size_t bytes) {
 
 int set_smem(bsidmap_decoder* d, const void* fn, size_t bytes) {
   if (bytes <= 48 * 1024) return BSIDMAP_OK;
+  for (auto& fs : d->smem_set)
+    if (fs.first == fn && fs.second >= bytes) return BSIDMAP_OK;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e != cudaSuccess) return cuda_fail(d, e, "cudaFuncSetAttribute(smem)");
+  d->smem_set.emplace_back(fn, bytes);
   return BSIDMAP_OK;
 }
 
