@@ -29,6 +29,7 @@ using namespace bsidmap;
 
 namespace {
 constexpr int kPhases = 5;
+constexpr int kHostSub = 8;  // sub-batches of the host-buffer pipeline
 std::string g_err;  // failures without a decoder (create)
 }  // namespace
 
@@ -46,9 +47,11 @@ struct bsidmap_decoder {
   size_t ws_bytes = 0;
   size_t ws_limit = 0;
   int last_chunk = 0, last_frames = 0, last_sched = 0;
-  // host-path staging
+  // host-path staging and the D2H pipeline
   void* hs = nullptr;
   size_t hs_bytes = 0;
+  cudaStream_t s_copy = nullptr;
+  cudaEvent_t ev_sub[8] = {};
   // host-side caches: the free-memory query and the smem opt-ins cost ~1 ms per call,
   // which would dominate single-frame latency (C1)
   size_t budget_cache = 0;
@@ -134,7 +137,7 @@ size_t budget(const bsidmap_decoder* d) {
 // current workspace is too small (the query is a synchronous driver call).
 size_t budget_for(bsidmap_decoder* d, int F, int mode, size_t need) {
   if (d->ws_limit) return d->ws_limit;
-  if (d->budget_frames == F && d->budget_mode == mode && need <= d->ws_bytes) return d->budget_cache;
+  if (d->budget_cache && d->budget_mode == mode && need <= d->ws_bytes) return d->budget_cache;
   d->budget_cache = budget(d);
   d->budget_frames = F;
   d->budget_mode = mode;
@@ -468,14 +471,35 @@ int bsidmap_decode_batch_host(bsidmap_decoder* d, int F, const uint32_t* rx, siz
   float* d_pri = priors ? reinterpret_cast<float*>(b) : nullptr; b += b_pri;
   float* d_L = reinterpret_cast<float*>(b); b += b_L;
   int32_t* d_st = reinterpret_cast<int32_t*>(b);
+  // Pipeline: inputs go up on `s`; the batch is decoded in sub-batches on `s`, and each
+  // sub-batch's APPs go back on a second stream while the next sub-batch computes, so the
+  // large D2H of L (N q 4 bytes per frame) overlaps the decode instead of following it.
+  if (!d->s_copy) {
+    cudaError_t e = cudaStreamCreateWithFlags(&d->s_copy, cudaStreamNonBlocking);
+    for (int k = 0; e == cudaSuccess && k < kHostSub; k++) e = cudaEventCreateWithFlags(&d->ev_sub[k], cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(d, e, "copy stream");
+  }
   cudaMemcpyAsync(d_rx, rx, rx_words_total * 4, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(d_off, off, (size_t)F * 8, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(d_rho, rho, (size_t)F * 4, cudaMemcpyHostToDevice, s);
   if (priors) cudaMemcpyAsync(d_pri, priors, nL * 4, cudaMemcpyHostToDevice, s);
-  if ((rc = bsidmap_decode_batch(d, F, d_rx, d_off, d_rho, d_pri, d_L, d_st, stream))) return rc;
-  cudaMemcpyAsync(L, d_L, nL * 4, cudaMemcpyDeviceToHost, s);
-  cudaMemcpyAsync(status, d_st, (size_t)F * 4, cudaMemcpyDeviceToHost, s);
-  cudaError_t e = cudaStreamSynchronize(s);
+  const int nsub = std::max(1, std::min(kHostSub, F / 8192));
+  const size_t row = (size_t)d->N * d->q;
+  long launches = 0;
+  for (int k = 0; k < nsub; k++) {
+    const int f0 = (int)((long)F * k / nsub), f1 = (int)((long)F * (k + 1) / nsub);
+    if ((rc = bsidmap_decode_batch(d, f1 - f0, d_rx, d_off + f0, d_rho + f0, d_pri ? d_pri + f0 * row : nullptr,
+                                   d_L + f0 * row, d_st + f0, stream)))
+      return rc;
+    launches += d->launches;
+    cudaEventRecord(d->ev_sub[k], s);
+    cudaStreamWaitEvent(d->s_copy, d->ev_sub[k], 0);
+    cudaMemcpyAsync(L + f0 * row, d_L + f0 * row, (size_t)(f1 - f0) * row * 4, cudaMemcpyDeviceToHost, d->s_copy);
+    cudaMemcpyAsync(status + f0, d_st + f0, (size_t)(f1 - f0) * 4, cudaMemcpyDeviceToHost, d->s_copy);
+  }
+  d->launches = launches;
+  cudaError_t e = cudaStreamSynchronize(d->s_copy);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(d, e, "decode_batch_host");
   return BSIDMAP_OK;
 }
@@ -486,6 +510,9 @@ void bsidmap_destroy(bsidmap_decoder* d) {
   cudaDeviceSynchronize();
   if (d->ws) cudaFree(d->ws);
   if (d->hs) cudaFree(d->hs);
+  if (d->s_copy) cudaStreamDestroy(d->s_copy);
+  for (int k = 0; k < kHostSub; k++)
+    if (d->ev_sub[k]) cudaEventDestroy(d->ev_sub[k]);
   if (d->d_C) cudaFree(d->d_C);
   for (int k = 0; k <= kPhases; k++)
     if (d->ev[k]) cudaEventDestroy(d->ev[k]);
