@@ -53,7 +53,9 @@ def _load():
             lib.oracle_receiver.restype = d
             lib.oracle_receiver.argtypes = [i, p, i, p, d, d, d, i, i, i]
             lib.oracle_decode.restype = i
-            lib.oracle_decode.argtypes = [i, i, i, p, d, d, d, i, i, i, i, p, i, p, p, p, p, p, p, p]
+            lib.oracle_decode.argtypes = [i, i, i, p, d, d, d, i, i, i, i, p, i, p, p, p, p, p, p, p, p, p]
+            lib.oracle_extrinsic.restype = i
+            lib.oracle_extrinsic.argtypes = [i, i, p, p, p]
             lib.oracle_gamma_at.restype = i
             lib.oracle_gamma_at.argtypes = [i, i, i, p, d, d, d, i, i, i, i, p, i, p, i, p]
             _lib = lib
@@ -121,17 +123,22 @@ def gamma(prob: Problem, y, i: int, priors=None):
     return g
 
 
-def decode(prob: Problem, y, priors=None, want_states=False):
-    """Decode one frame.  Returns dict(status, L[N][q], log_lambda[, alpha, beta, logA, logB])."""
+def decode(prob: Problem, y, priors=None, want_states=False, alpha0=None, betaN=None, extrinsic=False):
+    """Decode one frame.  Returns dict(status, L[N][q], log_lambda[, alpha, beta, logA, logB][, E]).
+
+    alpha0 / betaN: optional frame-boundary priors over the M_tau states (P:152-154);
+    default point masses delta(0), delta(rho - tau)."""
     y = np.ascontiguousarray(y, dtype=np.uint8)
     pr = None if priors is None else np.ascontiguousarray(priors, dtype=np.float64).reshape(prob.N, prob.q)
+    a0 = None if alpha0 is None else np.ascontiguousarray(alpha0, dtype=np.float64).reshape(prob.Mt)
+    bN = None if betaN is None else np.ascontiguousarray(betaN, dtype=np.float64).reshape(prob.Mt)
     L = np.zeros((prob.N, prob.q), dtype=np.float64)
     ll = ctypes.c_double(0.0)
     extra = {}
     if want_states:
         extra = dict(alpha=np.zeros((prob.N + 1, prob.Mt)), beta=np.zeros((prob.N + 1, prob.Mt)),
                      logA=np.zeros(prob.N + 1), logB=np.zeros(prob.N + 1))
-    rc = _load().oracle_decode(*prob._args(), _ptr(y) if len(y) else None, len(y), _ptr(pr), _ptr(L),
+    rc = _load().oracle_decode(*prob._args(), _ptr(y) if len(y) else None, len(y), _ptr(pr), _ptr(a0), _ptr(bN), _ptr(L),
                                ctypes.cast(ctypes.pointer(ll), ctypes.c_void_p),
                                _ptr(extra.get("alpha")), _ptr(extra.get("beta")),
                                _ptr(extra.get("logA")), _ptr(extra.get("logB")))
@@ -139,13 +146,17 @@ def decode(prob: Problem, y, priors=None, want_states=False):
         raise ValueError("oracle_decode: invalid arguments")
     out = dict(status=rc, L=L, log_lambda=ll.value)
     out.update(extra)
+    if extrinsic:
+        E = np.zeros_like(L)
+        _load().oracle_extrinsic(prob.N, prob.q, _ptr(L), _ptr(pr), _ptr(E))
+        out["E"] = E
     return out
 
 
-def decode_many(prob: Problem, ys, priors_list=None, threads=None):
+def decode_many(prob: Problem, ys, priors_list=None, threads=None, **kw):
     """Decode many frames on host threads (ctypes drops the GIL during the C call)."""
     threads = threads or os.cpu_count() or 1
     priors_list = priors_list if priors_list is not None else [None] * len(ys)
     _load()
     with ThreadPoolExecutor(max_workers=threads) as ex:
-        return list(ex.map(lambda a: decode(prob, a[0], a[1]), zip(ys, priors_list)))
+        return list(ex.map(lambda a: decode(prob, a[0], a[1], **kw), zip(ys, priors_list)))

@@ -187,14 +187,19 @@ int oracle_gamma(const oracle_problem *p, int i, double *g)
  *   alpha_hat, beta_hat ((N+1) x M_tau, optional) and logA, logB ((N+1),
  *   optional): normalised rows and the log of the accumulated normalisers,
  *   so that alpha_i(m) = alpha_hat_i(m) exp(logA_i) (eqn:alpha_norm).
+ *   alpha0, betaN (M_tau each, optional): the "prior probabilities of the frame
+ *   boundaries" alpha_0(m), beta_N(m); NULL = point masses delta(0),
+ *   delta(rho - tau) (reading R1).  With betaN given, rho - tau need not be a state.
+ *   lambda_N = sum_m alpha_N(m) beta_N(m) (eqn:lambda at i = N).
  * Returns ORACLE_OK, ORACLE_DRIFT_OUT_OF_RANGE (rho - tau outside
- * [m_tau^-, m_tau^+]) or ORACLE_UNDERFLOW (an all-zero alpha or
- * beta row: Y impossible under the limits).
+ * [m_tau^-, m_tau^+] with the point-mass beta_N) or ORACLE_UNDERFLOW
+ * (an all-zero alpha or beta row: Y impossible under the limits).
  */
 int oracle_decode(int q, int n, int N, const uint32_t *C,
                   double Pi, double Pd, double Ps,
                   int mn_lo, int mn_hi, int mt_lo, int mt_hi,
                   const uint8_t *y, int rho, const double *priors,
+                  const double *alpha0, const double *betaN,
                   double *L, double *log_lambda,
                   double *alpha_hat, double *beta_hat, double *logA, double *logB)
 {
@@ -213,7 +218,7 @@ int oracle_decode(int q, int n, int N, const uint32_t *C,
     memset(L, 0, sizeof(double) * (size_t)N * q);
     if (log_lambda)
         *log_lambda = -INFINITY;
-    if (rho - tau < mt_lo || rho - tau > mt_hi)
+    if (betaN == NULL && (rho - tau < mt_lo || rho - tau > mt_hi))
         return ORACLE_DRIFT_OUT_OF_RANGE;
 
     A = (double *)calloc((size_t)(N + 1) * Mt, sizeof(double));
@@ -226,9 +231,23 @@ int oracle_decode(int q, int n, int N, const uint32_t *C,
         return ORACLE_EINVAL;
     }
 
-    /* Boundary priors (R1): alpha_0 = delta(0), log scale 0. */
-    A[0 - mt_lo] = 1.0;
-    lA[0] = 0.0;
+    /* Boundary priors (R1): alpha_0 = delta(0) or the given alpha0,
+       normalised, its sum kept in the log scale. */
+    if (alpha0) {
+        double c = 0.0;
+        for (m = 0; m < Mt; m++)
+            c += alpha0[m];
+        if (!(c > 0.0)) {
+            free(A); free(B); free(lA); free(lB); free(g);
+            return ORACLE_EINVAL;
+        }
+        for (m = 0; m < Mt; m++)
+            A[m] = alpha0[m] / c;
+        lA[0] = log(c);
+    } else {
+        A[0 - mt_lo] = 1.0;
+        lA[0] = 0.0;
+    }
     /* Forward pass, eqn:alpha_prenorm then eqn:alpha_norm, gamma_{i-1} on the fly. */
     for (i = 1; i <= N && status == ORACLE_OK; i++) {
         double c = 0.0;
@@ -252,18 +271,38 @@ int oracle_decode(int q, int n, int N, const uint32_t *C,
             An[m] /= c;
         lA[i] = lA[i - 1] + log(c);
     }
+    /* beta_N = delta(rho - tau) or the given betaN, normalised (log scale kept). */
     if (status == ORACLE_OK) {
-        /* ln lambda_N(rho - tau) = ln alpha_N(rho - tau) since beta_N = delta(rho - tau). */
-        if (!(A[(size_t)N * Mt + (rho - tau - mt_lo)] > 0.0))
+        double *BN = B + (size_t)N * Mt;
+        if (betaN) {
+            double c = 0.0;
+            for (m = 0; m < Mt; m++)
+                c += betaN[m];
+            if (!(c > 0.0)) {
+                free(A); free(B); free(lA); free(lB); free(g);
+                return ORACLE_EINVAL;
+            }
+            for (m = 0; m < Mt; m++)
+                BN[m] = betaN[m] / c;
+            lB[N] = log(c);
+        } else {
+            BN[rho - tau - mt_lo] = 1.0;
+            lB[N] = 0.0;
+        }
+    }
+    if (status == ORACLE_OK) {
+        /* ln lambda_N = ln sum_m alpha_N(m) beta_N(m) (eqn:lambda at i = N) */
+        double lam = 0.0;
+        for (m = 0; m < Mt; m++)
+            lam += A[(size_t)N * Mt + m] * B[(size_t)N * Mt + m];
+        if (!(lam > 0.0))
             status = ORACLE_UNDERFLOW;
         else
-            lnlam = lA[N] + log(A[(size_t)N * Mt + (rho - tau - mt_lo)]);
+            lnlam = lA[N] + lB[N] + log(lam);
     }
     /* Backward pass (eqn:beta, normalised like alpha) with L_i in the same
        pass (eqn:L/eqn:lambda/eqn:sigma): gamma_i recomputed once more. */
     if (status == ORACLE_OK) {
-        B[(size_t)N * Mt + (rho - tau - mt_lo)] = 1.0;
-        lB[N] = 0.0;
         for (i = N - 1; i >= 0; i--) {
             double c = 0.0;
             double *Bi = B + (size_t)i * Mt, *Bn = B + (size_t)(i + 1) * Mt, *Ai = A + (size_t)i * Mt;
@@ -329,4 +368,27 @@ int oracle_gamma_at(int q, int n, int N, const uint32_t *C,
     if (!check_problem(&p) || i < 0 || i >= N || g == NULL)
         return ORACLE_EINVAL;
     return oracle_gamma(&p, i, g);
+}
+
+/*
+ * Extrinsic output for iterative decoding:
+ * E_i(D) = L_i(D) / P(D_i = D), normalised over D -- the APP with the symbol's own
+ * prior removed.  E_i(D) = 0 where P(D_i = D) = 0; priors NULL = uniform (E = L).
+ */
+int oracle_extrinsic(int N, int q, const double *L, const double *priors, double *E)
+{
+    int i, D;
+    if (N < 1 || q < 1 || L == NULL || E == NULL)
+        return ORACLE_EINVAL;
+    for (i = 0; i < N; i++) {
+        double s = 0.0;
+        for (D = 0; D < q; D++) {
+            const double P = priors ? priors[(size_t)i * q + D] : 1.0 / q;
+            E[(size_t)i * q + D] = P > 0.0 ? L[(size_t)i * q + D] / P : 0.0;
+            s += E[(size_t)i * q + D];
+        }
+        for (D = 0; D < q; D++)
+            E[(size_t)i * q + D] = s > 0.0 ? E[(size_t)i * q + D] / s : 0.0;
+    }
+    return ORACLE_OK;
 }

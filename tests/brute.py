@@ -133,3 +133,90 @@ def posterior_enum(C, n, Y, Pi, Pd, Ps, priors=None, mn=None, mt=None):
     if evidence == 0.0:
         return None, 0.0
     return [[v / evidence for v in row] for row in num], evidence
+
+
+def drift_enum(T, Pi, Pd, kmax=12):
+    """P(S_T = m) by enumerating per-bit event tuples (k insertions, then delete or
+    transmit) for T bits -- the generative definition of the drift."""
+    Pt = 1.0 - Pi - Pd
+    per_bit = []
+    for k in range(kmax + 1):
+        per_bit.append((k - 1, Pi ** k * Pd))
+        per_bit.append((k, Pi ** k * Pt))
+    out = {}
+    for seq in itertools.product(per_bit, repeat=T):
+        m = sum(c for c, _ in seq)
+        p = 1.0
+        for _, w in seq:
+            p *= w
+        out[m] = out.get(m, 0.0) + p
+    return out
+
+
+def frame_likelihood_soft(X, Y, n, Pi, Pd, Ps, mn, mt, alpha0, betaN):
+    """sum_{d0} alpha0(d0) sum_paths P(path) betaN(end drift): the frame's first bit
+    enters when d0 received bits precede it and its last bit leaves the channel at any
+    received position j <= |Y| (end drift j - tau); bits outside are not explained by
+    the frame.  alpha0 / betaN: dicts drift -> weight (frame-boundary priors).
+    Same node constraints as frame_likelihood_enum."""
+    X = [int(b) for b in X]
+    Y = [int(b) for b in Y]
+    tau, rho = len(X), len(Y)
+
+    def in_corridor(j, t, d0):
+        return mn[0] <= (j - t) - d0 <= mn[1]
+
+    def in_frame_limits(j, t):
+        return mt[0] <= j - t <= mt[1]
+
+    total = 0.0
+    for start, w0 in alpha0.items():
+        if w0 == 0.0 or start < 0 or start > rho or not in_frame_limits(start, 0):
+            continue
+        stack = [(0, start, start, w0)]
+        while stack:
+            t, j, d0, p = stack.pop()
+            if t == tau:
+                total += p * betaN.get(j - tau, 0.0)
+                continue
+            if j < rho and Pi > 0 and in_corridor(j + 1, t, d0):
+                stack.append((t, j + 1, d0, p * Pi * 0.5))
+            events = [(j, Pd)]
+            if j < rho:
+                events.append((j + 1, _transmit_prob(Y[j], X[t], Pi, Pd, Ps)))
+            for nj, pe in events:
+                if pe == 0.0:
+                    continue
+                nt = t + 1
+                if not in_corridor(nj, nt, d0):
+                    continue
+                nd0 = d0
+                if nt % n == 0:
+                    if not in_frame_limits(nj, nt):
+                        continue
+                    nd0 = nj - nt
+                stack.append((nt, nj, nd0, p * pe))
+    return total
+
+
+def posterior_soft(C, n, Y, Pi, Pd, Ps, priors, mn, mt, alpha0, betaN):
+    """Exhaustive Bayes with frame-boundary priors; returns (L, evidence)."""
+    N, q = len(C), len(C[0])
+    num = [[0.0] * q for _ in range(N)]
+    evidence = 0.0
+    for msg in itertools.product(range(q), repeat=N):
+        X = []
+        pm = 1.0
+        for i, D in enumerate(msg):
+            w = int(C[i][D])
+            X.extend((w >> t) & 1 for t in range(n))
+            pm *= (priors[i][D] if priors is not None else 1.0 / q)
+        if pm == 0.0:
+            continue
+        w = pm * frame_likelihood_soft(X, Y, n, Pi, Pd, Ps, mn, mt, alpha0, betaN)
+        evidence += w
+        for i, D in enumerate(msg):
+            num[i][D] += w
+    if evidence == 0.0:
+        return None, 0.0
+    return [[v / evidence for v in row] for row in num], evidence

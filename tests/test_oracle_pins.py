@@ -326,3 +326,72 @@ def test_drift_limits_cover_pr():
     off, p = bsidgen.drift_pmf(50, 0.1, 0.05)
     d = np.arange(len(p)) + off
     assert (p * d).sum() == pytest.approx(50 * (0.1 - 0.05) / (1 - 0.1), rel=1e-9)
+
+
+# ------------------------------------------- NEXT-1 / NEXT-4 oracle extensions
+
+def test_soft_boundary_priors_equal_exhaustive_bayes():
+    """alpha_0 / beta_N as distributions over drift states (Phi_T): the
+    oracle equals Bayes over messages x start offsets x event sequences x end drifts."""
+    rng = np.random.default_rng(21)
+    checked = 0
+    for trial in range(14):
+        prob, Y, priors = _tiny_problem(rng, wide=(trial % 2 == 0))
+        # pad the received sequence with random bits that no frame bit explains
+        Y = np.concatenate([rng.integers(0, 2, int(rng.integers(0, 3))), Y,
+                            rng.integers(0, 2, int(rng.integers(0, 3)))]).astype(np.uint8)
+        Mt = prob.Mt
+        a0 = rng.random(Mt) * (rng.random(Mt) < 0.6)
+        a0[0 - prob.mt_lo] += 0.3
+        bN = rng.random(Mt)
+        res = oracle.decode(prob, Y, priors, alpha0=a0, betaN=bN)
+        states = range(prob.mt_lo, prob.mt_hi + 1)
+        Lb, ev = brute.posterior_soft(prob.C.tolist(), prob.n, Y.tolist(), prob.Pi, prob.Pd, prob.Ps,
+                                      priors.tolist() if priors is not None else None,
+                                      (prob.mn_lo, prob.mn_hi), (prob.mt_lo, prob.mt_hi),
+                                      {m: a0[m - prob.mt_lo] for m in states}, {m: bN[m - prob.mt_lo] for m in states})
+        if ev == 0.0:
+            assert res["status"] == oracle.UNDERFLOW
+            continue
+        assert res["status"] == oracle.OK
+        np.testing.assert_allclose(res["L"], np.array(Lb), rtol=0, atol=1e-9)
+        assert res["log_lambda"] == pytest.approx(math.log(ev), rel=1e-10, abs=1e-10)
+        checked += 1
+    assert checked >= 6
+
+
+def test_point_mass_boundaries_reduce_to_default():
+    cfg, b, prob = _frame("C1", 3)
+    Y = b.bits(0)
+    base = oracle.decode(prob, Y)
+    a0 = np.zeros(prob.Mt)
+    a0[-prob.mt_lo] = 2.0
+    bN = np.zeros(prob.Mt)
+    bN[len(Y) - cfg.tau - prob.mt_lo] = 5.0
+    soft = oracle.decode(prob, Y, alpha0=a0, betaN=bN)
+    np.testing.assert_allclose(soft["L"], base["L"], rtol=1e-13)
+
+
+def test_extrinsic_equals_posterior_without_own_prior():
+    """E_i(D) proportional to L_i(D)/P(D_i=D) equals the exhaustive
+    Bayes posterior of D_i computed with row i of the priors replaced by uniform."""
+    rng = np.random.default_rng(33)
+    for _ in range(5):
+        prob, Y, _ = _tiny_problem(rng, wide=True)
+        pri = rng.random((prob.N, prob.q)) + 0.05
+        res = oracle.decode(prob, Y, pri, extrinsic=True)
+        for i in range(prob.N):
+            mod = pri.copy()
+            mod[i] = 1.0
+            Lb, ev = brute.posterior_enum(prob.C.tolist(), prob.n, Y.tolist(), prob.Pi, prob.Pd, prob.Ps,
+                                          mod.tolist(), (prob.mn_lo, prob.mn_hi), (prob.mt_lo, prob.mt_hi))
+            np.testing.assert_allclose(res["E"][i], np.array(Lb[i]), rtol=0, atol=1e-9)
+    # zero prior: the extrinsic is 0 there, and E = L under uniform priors
+    cfg, b, prob = _frame("C1", 0)
+    pri = np.full((cfg.N, cfg.q), 1.0)
+    pri[2, 1] = 0.0
+    res = oracle.decode(prob, b.bits(0), pri, extrinsic=True)
+    assert res["E"][2, 1] == 0.0
+    np.testing.assert_allclose(res["E"].sum(1), 1.0, atol=1e-12)
+    res_u = oracle.decode(prob, b.bits(0), extrinsic=True)
+    np.testing.assert_allclose(res_u["E"], res_u["L"] / res_u["L"].sum(1, keepdims=True), rtol=1e-13)
