@@ -167,6 +167,24 @@ int bsidmap_debug_gamma(bsidmap_decoder *d, int num_frames, const uint32_t *rx_w
 int bsidmap_debug_states(bsidmap_decoder *d, int num_frames, double *alpha_out, double *beta_out,
                          void *cuda_stream);
 
+/* ---------------------------------------------------------------------------------------
+ * State-space sizing.  Host functions, no device needed.
+ * The drift S_T after T transmitted bits is the T-fold convolution of the per-bit
+ * change: k insertions then deletion (k-1, prob Pi^k Pd) or transmission (k, prob Pi^k Pt).
+ */
+/* pmf[m - lo] = P(S_T = m) for m in [lo, hi] (FP64; mass outside the range is dropped). */
+int bsidmap_drift_pmf(int T, double Pi, double Pd, int lo, int hi, double *pmf);
+/* Limits with exclusion probability Pr (reading R8; the paper defers the rule to
+ * bbw14joe): lo = max{m : P(S_T < m) <= Pr/2},
+ * hi = min{m : P(S_T > m) <= Pr/2}, clamped to -T <= lo <= 0 <= hi. */
+int bsidmap_drift_limits(int T, double Pi, double Pd, double Pr, int *lo, int *hi);
+/* m_n^± from T = n and m_tau^± from T = n N, widened to contain m_n (bsidmap_create's rule). */
+int bsidmap_state_space(int n, int N, double Pi, double Pd, double Pr, int *mn_lo, int *mn_hi, int *mt_lo,
+                        int *mt_hi);
+/* Phi_T (named but undefined in the paper; read as the drift PMF over T bits) written
+ * on the device for num_frames frames: out_dev[f][m - lo] = P(S_T = m).  Synchronous. */
+int bsidmap_phi(int T, double Pi, double Pd, int lo, int hi, int num_frames, double *out_dev, void *cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -5,7 +5,7 @@ The hot path lives in ``libbsidmap.so`` (hand-written CUDA for sm_100a behind
 the C ABI of ``include/bsidmap.h``); this package only marshals arguments.
 PyTorch supplies device memory, streams and process groups.
 """
-from .decoder import Decoder  # noqa: F401
+from .decoder import Decoder, drift_limits, drift_pmf, phi, state_space  # noqa: F401
 from . import _lib  # noqa: F401
 
 MODE_AUTO = _lib.BSIDMAP_MODE_AUTO

@@ -47,6 +47,10 @@ SIGNATURES = {
     "bsidmap_valid_lattices": (_ll, [_p, _i, _p]),
     "bsidmap_debug_gamma": (_i, [_p, _i, _p, _p, _p, _p, _i, _p, _p]),
     "bsidmap_debug_states": (_i, [_p, _i, _p, _p, _p]),
+    "bsidmap_drift_pmf": (_i, [_i, _d, _d, _i, _i, _p]),
+    "bsidmap_drift_limits": (_i, [_i, _d, _d, _d, _p, _p]),
+    "bsidmap_state_space": (_i, [_i, _i, _d, _d, _d, _p, _p, _p, _p]),
+    "bsidmap_phi": (_i, [_i, _d, _d, _i, _i, _i, _p, _p]),
 }
 
 _lib = None

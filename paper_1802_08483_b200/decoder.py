@@ -137,3 +137,38 @@ class Decoder:
         b = torch.empty_like(a)
         _lib.check(self._lib.bsidmap_debug_states(self.h, int(F), _ptr(a), _ptr(b), _stream(stream)), self.h)
         return a, b
+
+
+# ---------------------------------------------------------------- state-space sizing (host)
+def drift_pmf(T, Pi, Pd, lo, hi):
+    """P(S_T = m) for m in [lo, hi] (bsidmap_drift_pmf)."""
+    lib = _lib.load()
+    out = np.zeros(hi - lo + 1, dtype=np.float64)
+    _lib.check(lib.bsidmap_drift_pmf(int(T), float(Pi), float(Pd), int(lo), int(hi), _ptr(out)))
+    return out
+
+
+def drift_limits(T, Pi, Pd, Pr=1e-10):
+    """(m_T^-, m_T^+) with exclusion probability Pr (bsidmap_drift_limits)."""
+    lib = _lib.load()
+    lo, hi = ctypes.c_int(), ctypes.c_int()
+    _lib.check(lib.bsidmap_drift_limits(int(T), float(Pi), float(Pd), float(Pr), ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
+def state_space(n, N, Pi, Pd, Pr=1e-10):
+    """((m_n^-, m_n^+), (m_tau^-, m_tau^+)) (bsidmap_state_space)."""
+    lib = _lib.load()
+    v = [ctypes.c_int() for _ in range(4)]
+    _lib.check(lib.bsidmap_state_space(int(n), int(N), float(Pi), float(Pd), float(Pr), *[ctypes.byref(x) for x in v]))
+    return (v[0].value, v[1].value), (v[2].value, v[3].value)
+
+
+def phi(T, Pi, Pd, lo, hi, num_frames, device=None, stream=None):
+    """Phi_T on the device: [num_frames][hi - lo + 1] drift PMF (bsidmap_phi)."""
+    lib = _lib.load()
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    out = torch.empty((num_frames, hi - lo + 1), dtype=torch.float64, device=dev)
+    _lib.check(lib.bsidmap_phi(int(T), float(Pi), float(Pd), int(lo), int(hi), int(num_frames), _ptr(out),
+                               _stream(stream)))
+    return out
