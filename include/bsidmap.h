@@ -97,6 +97,29 @@ int bsidmap_decode_batch(bsidmap_decoder *d, int num_frames, const uint32_t *rx_
                          float *L_out, int32_t *frame_status, void *cuda_stream);
 
 /*
+ * Options of bsidmap_decode_batch_opts (all DEVICE pointers, caller-owned; NULL = default).
+ *   alpha0, betaN : [num_frames][M_tau] FP64 frame-boundary priors alpha_0(m), beta_N(m), state m at
+ *                   index m - m_tau^- ("set as the prior probabilities of the frame boundaries",
+ *                   P:152-154; e.g. Phi_T from bsidmap_phi).  Default: alpha_0 = delta(0) and
+ *                   beta_N = delta(rho - tau).  With betaN given, rho - tau need not be a state
+ *                   (no DRIFT_OUT_OF_RANGE), as in stream decoding.  Any positive scale.
+ *   extrinsic     : [num_frames][N][q] FP32 output E_i(D) = L_i(D) / P(D_i = D) normalised over D
+ *                   (0 where the prior is 0; = L for uniform priors): the extrinsic information
+ *                   for an outer decoder in iterative decoding.
+ */
+typedef struct bsidmap_decode_opts {
+  const double *alpha0;
+  const double *betaN;
+  float *extrinsic;
+} bsidmap_decode_opts;
+
+/* bsidmap_decode_batch with options (opts may be NULL). */
+int bsidmap_decode_batch_opts(bsidmap_decoder *d, int num_frames, const uint32_t *rx_words,
+                              const int64_t *rx_word_offset, const int32_t *rho, const float *priors,
+                              const bsidmap_decode_opts *opts, float *L_out, int32_t *frame_status,
+                              void *cuda_stream);
+
+/*
  * Same computation with HOST buffers (end-to-end path): copies the inputs to the
  * device (pinned memory gives async copies), decodes, copies L and the status back and
  * synchronises `cuda_stream` before returning.  rx_words_total = number of words in rx_words.
@@ -184,6 +207,28 @@ int bsidmap_state_space(int n, int N, double Pi, double Pd, double Pr, int *mn_l
 /* Phi_T (named but undefined in the paper; read as the drift PMF over T bits) written
  * on the device for num_frames frames: out_dev[f][m - lo] = P(S_T = m).  Synchronous. */
 int bsidmap_phi(int T, double Pi, double Pd, int lo, int hi, int num_frames, double *out_dev, void *cuda_stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Monte-Carlo symbol/frame error rates on the device (the decoder inside the
+ * paper's simulator).  Messages D_i ~ U[0,q), encoding with the
+ * decoder's codebook and the literal BSID event loop use the counter-based
+ * stream of the host generator (bsidgen), so frame (seed, index) is bit-identical on host and
+ * device; frames with rho - tau outside [m_tau^-, m_tau^+] are redrawn and counted.
+ */
+/* Generate frames [first_frame, first_frame + num_frames) into DEVICE buffers: msg [F][N] int32,
+ * rx [F][words_per_frame] packed LSB-first (frame f at word f * words_per_frame), rho [F];
+ * *redraws (device counter) is incremented.  Asynchronous. */
+int bsidmap_mc_generate(bsidmap_decoder *d, uint64_t seed, int64_t first_frame, int num_frames, int words_per_frame,
+                        int32_t *msg, uint32_t *rx, int32_t *rho, unsigned long long *redraws, void *cuda_stream);
+/* Hard decisions argmax_D L_i(D) (lowest D on ties) against msg: counters (DEVICE, accumulated):
+ * [0] symbol errors, [1] frame errors, [2] failed frames (status != OK; all their symbols count as
+ * errors).  Asynchronous. */
+int bsidmap_count_errors(bsidmap_decoder *d, int num_frames, const float *L, const int32_t *msg,
+                         const int32_t *frame_status, unsigned long long *counters, void *cuda_stream);
+/* Generate, decode (uniform priors) and count num_frames frames in batches of `batch` frames.
+ * results (HOST, 4 entries): frames, symbol errors, frame errors, channel redraws.  Synchronous. */
+int bsidmap_mc_run(bsidmap_decoder *d, uint64_t seed, int64_t first_frame, int num_frames, int batch,
+                   unsigned long long *results, void *cuda_stream);
 
 #ifdef __cplusplus
 }

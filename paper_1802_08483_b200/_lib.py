@@ -34,6 +34,7 @@ SIGNATURES = {
     "bsidmap_create": (_i, [ctypes.POINTER(_p), _i, _i, _i, _p, _d, _d, _d, _i, _i, _i, _i, _i, _i]),
     "bsidmap_decode_batch": (_i, [_p, _i, _p, _p, _p, _p, _p, _p, _p]),
     "bsidmap_decode_batch_host": (_i, [_p, _i, _p, _sz, _p, _p, _p, _p, _p, _p]),
+    "bsidmap_decode_batch_opts": (_i, [_p, _i, _p, _p, _p, _p, _p, _p, _p, _p]),
     "bsidmap_destroy": (None, [_p]),
     "bsidmap_last_error": (ctypes.c_char_p, [_p]),
     "bsidmap_workspace_bytes": (_sz, [_p, _i, _i]),
@@ -51,6 +52,9 @@ SIGNATURES = {
     "bsidmap_drift_limits": (_i, [_i, _d, _d, _d, _p, _p]),
     "bsidmap_state_space": (_i, [_i, _i, _d, _d, _d, _p, _p, _p, _p]),
     "bsidmap_phi": (_i, [_i, _d, _d, _i, _i, _i, _p, _p]),
+    "bsidmap_mc_generate": (_i, [_p, ctypes.c_uint64, ctypes.c_int64, _i, _i, _p, _p, _p, _p, _p]),
+    "bsidmap_count_errors": (_i, [_p, _i, _p, _p, _p, _p, _p]),
+    "bsidmap_mc_run": (_i, [_p, ctypes.c_uint64, ctypes.c_int64, _i, _i, _p, _p]),
 }
 
 _lib = None
@@ -69,6 +73,11 @@ def load():
             fn.argtypes = args
         _lib = lib
     return _lib
+
+
+class DecodeOpts(ctypes.Structure):
+    """struct bsidmap_decode_opts (device pointers)."""
+    _fields_ = [("alpha0", ctypes.c_void_p), ("betaN", ctypes.c_void_p), ("extrinsic", ctypes.c_void_p)]
 
 
 class BsidmapError(RuntimeError):

@@ -23,7 +23,29 @@ __global__ void k_alpha_beta(const DecodeParams p, int stages);
 size_t ab_cta_smem(int Mn, int Mtp, int stages);
 __global__ void k_finalize(const DecodeParams p);
 __global__ void k_zero_failed(const DecodeParams p);
+__global__ void k_extrinsic(const DecodeParams p, float* E);
+struct McParams {
+  uint64_t seed;
+  long first;
+  int F, N, q, n, wpf, mt_lo, mt_hi;
+  double Pi, Pd, Ps;
+  const uint32_t* C;
+  int32_t* msg;
+  uint32_t* rx;
+  int32_t* rho;
+  unsigned long long* redraws;
+};
+__global__ void k_mc_generate(const McParams P);
+__global__ void k_mc_count(const float* L, const int32_t* msg, const int32_t* status, int F, int N, int q,
+                           unsigned long long* counters);
 }  // namespace bsidmap
+
+namespace {
+__global__ void k_iota_offsets(int64_t* off, int F, int wpf) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < F) off[f] = (int64_t)f * wpf;
+}
+}  // namespace
 
 using namespace bsidmap;
 
@@ -397,6 +419,12 @@ int bsidmap_create(bsidmap_decoder** out, int q, int n, int N, const uint32_t* c
 
 int bsidmap_decode_batch(bsidmap_decoder* d, int F, const uint32_t* rx, const int64_t* off, const int32_t* rho,
                          const float* priors, float* L, int32_t* status, void* stream) {
+  return bsidmap_decode_batch_opts(d, F, rx, off, rho, priors, nullptr, L, status, stream);
+}
+
+int bsidmap_decode_batch_opts(bsidmap_decoder* d, int F, const uint32_t* rx, const int64_t* off, const int32_t* rho,
+                              const float* priors, const bsidmap_decode_opts* opts, float* L, int32_t* status,
+                              void* stream) {
   int rc = check_inputs(d, F, rx, off, rho, L, status);
   if (rc) return rc;
   d->launches = 0;
@@ -426,9 +454,16 @@ int bsidmap_decode_batch(bsidmap_decoder* d, int F, const uint32_t* rx, const in
     p.rx_off = off + f0;
     p.rho = rho + f0;
     p.priors = priors ? priors + (size_t)f0 * d->N * d->q : nullptr;
+    p.alpha0 = (opts && opts->alpha0) ? opts->alpha0 + (size_t)f0 * d->Mt : nullptr;
+    p.betaN = (opts && opts->betaN) ? opts->betaN + (size_t)f0 * d->Mt : nullptr;
     p.status = status + f0;
     p.L = L + (size_t)f0 * d->N * d->q;
     if ((rc = run_chunk(d, P, p, s, c == 0, c == P.nchunks - 1))) return rc;
+    if (opts && opts->extrinsic) {  // NEXT-4: extrinsic APPs for an outer decoder
+      const long rows = (long)p.F * d->N;
+      k_extrinsic<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(p, opts->extrinsic + (size_t)f0 * d->N * d->q);
+      d->launches++;
+    }
   }
   d->last_chunk = P.chunk;
   d->last_frames = F;
@@ -640,6 +675,76 @@ int bsidmap_debug_states(bsidmap_decoder* d, int F, double* alpha_out, double* b
   cudaError_t e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(d, e, "debug_states");
   return BSIDMAP_OK;
+}
+
+int bsidmap_mc_generate(bsidmap_decoder* d, uint64_t seed, int64_t first_frame, int F, int wpf, int32_t* msg,
+                        uint32_t* rx, int32_t* rho, unsigned long long* redraws, void* stream) {
+  if (!d || F < 1 || !msg || !rx || !rho || !redraws || (long)wpf * 32 < (long)d->n * d->N + d->mt_hi)
+    return fail(d, BSIDMAP_EINVAL, "bad arguments");
+  cudaSetDevice(d->device);
+  McParams P;
+  P.seed = seed; P.first = first_frame; P.F = F; P.N = d->N; P.q = d->q; P.n = d->n; P.wpf = wpf;
+  P.mt_lo = d->mt_lo; P.mt_hi = d->mt_hi; P.Pi = d->Pi; P.Pd = d->Pd; P.Ps = d->Ps;
+  P.C = d->d_C; P.msg = msg; P.rx = rx; P.rho = rho; P.redraws = redraws;
+  k_mc_generate<<<(F + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(P);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BSIDMAP_OK : cuda_fail(d, e, "mc_generate");
+}
+
+int bsidmap_count_errors(bsidmap_decoder* d, int F, const float* L, const int32_t* msg, const int32_t* status,
+                         unsigned long long* counters, void* stream) {
+  if (!d || F < 1 || !L || !msg || !status || !counters) return fail(d, BSIDMAP_EINVAL, "bad arguments");
+  cudaSetDevice(d->device);
+  k_mc_count<<<F, 128, 0, static_cast<cudaStream_t>(stream)>>>(L, msg, status, F, d->N, d->q, counters);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BSIDMAP_OK : cuda_fail(d, e, "count_errors");
+}
+
+int bsidmap_mc_run(bsidmap_decoder* d, uint64_t seed, int64_t first_frame, int num_frames, int batch,
+                   unsigned long long* results, void* stream) {
+  if (!d || num_frames < 1 || batch < 1 || !results) return fail(d, BSIDMAP_EINVAL, "bad arguments");
+  cudaSetDevice(d->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  batch = std::min(batch, num_frames);
+  const int wpf = (d->n * d->N + d->mt_hi + 31) / 32 + 1;  // as the host generator (bsidgen)
+  const size_t nL = (size_t)batch * d->N * d->q;
+  char* buf = nullptr;
+  const size_t b_msg = align_up((size_t)batch * d->N * 4), b_rx = align_up((size_t)batch * wpf * 4),
+               b_rho = align_up((size_t)batch * 4), b_off = align_up((size_t)batch * 8), b_L = align_up(nL * 4),
+               b_st = align_up((size_t)batch * 4), b_cnt = 256;
+  cudaError_t e = cudaMallocAsync(&buf, b_msg + b_rx + b_rho + b_off + b_L + b_st + b_cnt, s);
+  if (e != cudaSuccess) return cuda_fail(d, e, "mc_run alloc");
+  int32_t* msg = reinterpret_cast<int32_t*>(buf);
+  uint32_t* rx = reinterpret_cast<uint32_t*>(buf + b_msg);
+  int32_t* rho = reinterpret_cast<int32_t*>(buf + b_msg + b_rx);
+  int64_t* off = reinterpret_cast<int64_t*>(buf + b_msg + b_rx + b_rho);
+  float* L = reinterpret_cast<float*>(buf + b_msg + b_rx + b_rho + b_off);
+  int32_t* st = reinterpret_cast<int32_t*>(buf + b_msg + b_rx + b_rho + b_off + b_L);
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(buf + b_msg + b_rx + b_rho + b_off + b_L + b_st);
+  cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned long long), s);
+  int rc = BSIDMAP_OK;
+  long launches = 0;
+  for (int f0 = 0; f0 < num_frames && rc == BSIDMAP_OK; f0 += batch) {
+    const int F = std::min(batch, num_frames - f0);
+    k_iota_offsets<<<(F + 255) / 256, 256, 0, s>>>(off, F, wpf);
+    if ((rc = bsidmap_mc_generate(d, seed, first_frame + f0, F, wpf, msg, rx, rho, cnt + 3, stream))) break;
+    if ((rc = bsidmap_decode_batch(d, F, rx, off, rho, nullptr, L, st, stream))) break;
+    launches += d->launches + 3;
+    if ((rc = bsidmap_count_errors(d, F, L, msg, st, cnt, stream))) break;
+  }
+  unsigned long long h[4] = {0, 0, 0, 0};
+  if (rc == BSIDMAP_OK) {
+    cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s);
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = cuda_fail(d, e, "mc_run");
+  }
+  cudaFreeAsync(buf, s);
+  d->launches = launches;
+  results[0] = (unsigned long long)num_frames;
+  results[1] = h[0];
+  results[2] = h[1];
+  results[3] = h[3];
+  return rc;
 }
 
 }  // extern "C"

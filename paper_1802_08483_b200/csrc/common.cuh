@@ -46,6 +46,8 @@ struct DecodeParams {
   const int64_t* rx_off;      // [F] word offset of each frame in rx
   const int32_t* rho;         // [F] received length
   const float* priors;        // [F][N][q] or nullptr (uniform 1/q)
+  const double* alpha0;       // [F][M_tau] frame-boundary prior alpha_0 or nullptr (= delta(0))
+  const double* betaN;        // [F][M_tau] frame-boundary prior beta_N or nullptr (= delta(rho - tau))
   int32_t* status;            // [F]
   float* Gsum;                // [F][N][M_n][Mtp]  Gamma_i(m', k) = sum_D gamma_i(m', m'+k, D) (lattice scale)
   float* gamma;               // stored variant: [F][N][q][M_n][M_tau] gamma, scaled 2^80
@@ -58,6 +60,13 @@ struct DecodeParams {
   int i_base;                 // first symbol index of this launch (blockIdx.y offset)
   LatticeConst lc;
 };
+
+// Boundary row of frame f at state index m: alpha_0 (fwd) / beta_N (bwd), point masses by default.
+__device__ __forceinline__ double boundary_row(const DecodeParams& p, int f, int m, bool fwd) {
+  if (m >= p.Mt) return 0.0;
+  if (fwd) return p.alpha0 ? p.alpha0[(size_t)f * p.Mt + m] : (m == -p.mt_lo ? 1.0 : 0.0);
+  return p.betaN ? p.betaN[(size_t)f * p.Mt + m] : (m == p.rho[f] - p.n * p.N - p.mt_lo ? 1.0 : 0.0);
+}
 
 // 64 received bits starting at bit `s` of frame f (LSB-first); bits at or
 // beyond rho read as 0 (they only feed lattice columns that are masked).

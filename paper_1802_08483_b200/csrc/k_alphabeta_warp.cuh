@@ -52,12 +52,11 @@ __global__ void __launch_bounds__(kAbWarpThreads) k_alpha_beta_warp(const Decode
       tma_bulk_g2s(ring + (size_t)s * MN * Mtp, gblock(s), blk_bytes, bars + s);
     }
   }
-  const int boundary = fwd ? -p.mt_lo : p.rho[f] - p.n * N - p.mt_lo;  // alpha_0 = delta(0), beta_N = delta(rho - tau)
   const int i0 = fwd ? 0 : N;
 #pragma unroll
   for (int s = 0; s < SPT; s++) {
     const int m = lane + 32 * s;
-    const double v = (m == boundary) ? 1.0 : 0.0;
+    const double v = boundary_row(p, f, m, fwd);  // alpha_0 / beta_N
     row[m] = v;
     if (m < Mt) rows_g[(size_t)i0 * Mt + m] = v;
   }

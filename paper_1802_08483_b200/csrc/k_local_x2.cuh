@@ -44,9 +44,9 @@ __global__ void __launch_bounds__(kLocalWarps * 32, Core::kMinBlocks) k_local_fw
   const int Mt = p.Mt, N = p.N, lo = p.mn_lo;
   double* rows_g = p.alpha + (size_t)f * (N + 1) * Mt;
   const int ma = 2 * lane, mb = 2 * lane + 1;
-  // alpha_0 = delta(0) (reading R1)
+  // alpha_0 (delta(0) by default, reading R1)
   {
-    const double va = (ma == -p.mt_lo) ? 1.0 : 0.0, vb = (mb == -p.mt_lo) ? 1.0 : 0.0;
+    const double va = boundary_row(p, f, ma, true), vb = boundary_row(p, f, mb, true);
     row[ma] = va;
     row[mb] = vb;
     if (ma < Mt) rows_g[ma] = va;
@@ -125,11 +125,8 @@ __global__ void __launch_bounds__(kLocalWarps * 32, BSIDMAP_APP_MINB) k_local_bw
   }
   const double* alpha_f = p.alpha + (size_t)f * (N + 1) * Mt;
   const int ma = 2 * lane, mb = 2 * lane + 1;
-  {  // beta_N = delta(rho - tau)
-    const int end = p.rho[f] - p.n * N - p.mt_lo;
-    row[ma] = (ma == end) ? 1.0 : 0.0;
-    row[mb] = (mb == end) ? 1.0 : 0.0;
-  }
+  row[ma] = boundary_row(p, f, ma, false);  // beta_N (delta(rho - tau) by default)
+  row[mb] = boundary_row(p, f, mb, false);
   __syncwarp();
   for (int i = N - 1; i >= 0; i--) {
     for (int t = lane; t < p.q; t += 32) sC[t] = p.C[(size_t)i * p.q + t];

@@ -25,7 +25,8 @@ __global__ void k_frame_init(const DecodeParams p) {
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= p.F) return;
   const int drift = p.rho[f] - p.n * p.N;
-  p.status[f] = (drift >= p.mt_lo && drift <= p.mt_hi) ? kFrameOk : kFrameDriftOutOfRange;
+  // with soft beta_N weights the end drift need not be a state (stream decoding)
+  p.status[f] = (p.betaN || (drift >= p.mt_lo && drift <= p.mt_hi)) ? kFrameOk : kFrameDriftOutOfRange;
 }
 
 // Shared memory of k_alpha_beta: ring[stages][M_n][Mtp] floats | R[2][Mtp] doubles |
@@ -65,15 +66,14 @@ __global__ void __launch_bounds__(1024) k_alpha_beta(const DecodeParams p, int s
       tma_bulk_g2s(ring + (size_t)s * Mn * Mtp, gblock(s), blk, bars + s);
     }
   }
-  const int boundary = fwd ? -p.mt_lo : p.rho[f] - p.n * N - p.mt_lo;  // alpha_0 = delta(0), beta_N = delta(rho - tau)
   const int i0 = fwd ? 0 : N;
   for (int m = tid; m < Mt; m += nt) {
-    const double v = (m == boundary) ? 1.0 : 0.0;
+    const double v = boundary_row(p, f, m, fwd);  // alpha_0 / beta_N
     R[m] = v;
     rows[(size_t)i0 * Mt + m] = v;
   }
   __syncthreads();
-  double inv_c = 1.0;  // 1 / sum_m R_cur(m)
+  double inv_c = 1.0;  // scale of R_cur (any constant: every row is normalised by its own sum)
   for (int step = 0; step < N; step++) {
     const int stage = step % stages;
     mbar_wait(bars + stage, (uint32_t)(step / stages) & 1u);
@@ -128,6 +128,29 @@ __global__ void k_zero_failed(const DecodeParams p) {
   if (p.status[f] == kFrameOk) return;
   float* L = p.L + (size_t)f * p.N * p.q;
   for (long k = threadIdx.x; k < (long)p.N * p.q; k += blockDim.x) L[k] = 0.f;
+}
+
+// Extrinsic output (NEXT-4): E_i(D) = L_i(D) / P(D_i = D), normalised,
+// 0 where the prior is 0; uniform priors give E = L.  One warp per (frame, i) row.
+__global__ void k_extrinsic(const DecodeParams p, float* E) {
+  const long row = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= (long)p.F * p.N) return;
+  const float* Lr = p.L + row * p.q;
+  const float* Pr = p.priors ? p.priors + row * p.q : nullptr;
+  float* Er = E + row * p.q;
+  float s = 0.f;
+  for (int D = lane; D < p.q; D += 32) {
+    const float P = Pr ? Pr[D] : 1.f;
+    s += P > 0.f ? Lr[D] / P : 0.f;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float inv = s > 0.f ? 1.f / s : 0.f;
+  for (int D = lane; D < p.q; D += 32) {
+    const float P = Pr ? Pr[D] : 1.f;
+    Er[D] = P > 0.f ? Lr[D] / P * inv : 0.f;
+  }
 }
 
 // One warp per (frame, i) row.

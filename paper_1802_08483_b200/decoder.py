@@ -68,13 +68,22 @@ class Decoder:
                                             _ptr(L), _ptr(status), _stream(stream))
         _lib.check(rc, self.h)
 
-    def decode(self, rx, rx_off, rho, priors=None, stream=None):
-        """Allocate outputs and decode; returns (L [F][N][q] fp32, status [F] int32) on the device."""
+    def decode(self, rx, rx_off, rho, priors=None, stream=None, alpha0=None, betaN=None, extrinsic=False):
+        """Allocate outputs and decode; returns (L [F][N][q] fp32, status [F] int32) on the device,
+        plus E (extrinsic) if requested.  alpha0/betaN: [F][M_tau] fp64 boundary priors."""
         F = int(rho.numel())
         L = torch.empty((F, self.N, self.q), dtype=torch.float32, device=self.device)
         st = torch.empty((F,), dtype=torch.int32, device=self.device)
-        self.decode_batch(rx, rx_off, rho, priors, L, st, stream)
-        return L, st
+        if alpha0 is None and betaN is None and not extrinsic:
+            self.decode_batch(rx, rx_off, rho, priors, L, st, stream)
+            return L, st
+        E = torch.empty_like(L) if extrinsic else None
+        opts = _lib.DecodeOpts(None if alpha0 is None else alpha0.data_ptr(),
+                               None if betaN is None else betaN.data_ptr(), None if E is None else E.data_ptr())
+        rc = self._lib.bsidmap_decode_batch_opts(self.h, F, _ptr(rx), _ptr(rx_off), _ptr(rho), _ptr(priors),
+                                                 ctypes.byref(opts), _ptr(L), _ptr(st), _stream(stream))
+        _lib.check(rc, self.h)
+        return (L, st, E) if extrinsic else (L, st)
 
     def decode_host(self, rx, rx_off, rho, priors, L, status, stream=None):
         """bsidmap_decode_batch_host on host (ideally pinned) tensors/arrays; synchronous."""
@@ -120,6 +129,31 @@ class Decoder:
     def valid_lattices(self, rho_host):
         r = np.ascontiguousarray(rho_host, dtype=np.int32)
         return int(self._lib.bsidmap_valid_lattices(self.h, len(r), r.ctypes.data_as(ctypes.c_void_p)))
+
+    # ------------------------------------------------------------- Monte Carlo
+    def mc_generate(self, seed, first, F, words_per_frame, stream=None):
+        """Device-generated frames (bsidmap_mc_generate): (msg, rx, rho, redraws) tensors."""
+        msg = torch.empty((F, self.N), dtype=torch.int32, device=self.device)
+        rx = torch.zeros((F, words_per_frame), dtype=torch.int32, device=self.device)
+        rho = torch.empty((F,), dtype=torch.int32, device=self.device)
+        red = torch.zeros((1,), dtype=torch.int64, device=self.device)
+        _lib.check(self._lib.bsidmap_mc_generate(self.h, int(seed), int(first), int(F), int(words_per_frame), _ptr(msg),
+                                                 _ptr(rx), _ptr(rho), _ptr(red), _stream(stream)), self.h)
+        return msg, rx, rho, red
+
+    def count_errors(self, L, msg, status, counters=None, stream=None):
+        """bsidmap_count_errors; returns the device counters [symbol errors, frame errors, failed]."""
+        counters = torch.zeros((3,), dtype=torch.int64, device=self.device) if counters is None else counters
+        _lib.check(self._lib.bsidmap_count_errors(self.h, int(msg.shape[0]), _ptr(L), _ptr(msg), _ptr(status),
+                                                  _ptr(counters), _stream(stream)), self.h)
+        return counters
+
+    def mc_run(self, seed, first, F, batch, stream=None):
+        """bsidmap_mc_run: dict(frames, symbol_errors, frame_errors, redraws)."""
+        res = (ctypes.c_ulonglong * 4)()
+        _lib.check(self._lib.bsidmap_mc_run(self.h, int(seed), int(first), int(F), int(batch), res, _stream(stream)),
+                   self.h)
+        return dict(frames=res[0], symbol_errors=res[1], frame_errors=res[2], redraws=res[3])
 
     # ------------------------------------------------------------------ debug
     def debug_gamma(self, rx, rx_off, rho, priors, i, stream=None):
