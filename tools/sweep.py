@@ -56,6 +56,45 @@ def run(name, mode, steps):
             "symbol_error_rate": ser}
 
 
+def run_next(steps):
+    """NEXT rows at C2 (65536 frames): soft boundaries + extrinsic overhead, and the Monte-Carlo loop."""
+    from paper_1802_08483_b200 import phi
+    cfg = bsidgen.configs()["C2"]
+    F = BATCH["C2"]
+    b = bsidgen.make_batch(cfg, 0, F)
+    dev = torch.device("cuda", 0)
+    d = Decoder.from_config(cfg, b.C, device=0)
+    rx = torch.from_numpy(b.rx.ravel().copy()).to(dev)
+    off = torch.from_numpy(b.offsets).to(dev)
+    rho = torch.from_numpy(b.rho).to(dev)
+    a0 = phi(1, cfg.Pi, cfg.Pd, cfg.mt[0], cfg.mt[1], F, device=0)          # start-drift prior Phi_1
+    bN = phi(cfg.tau, cfg.Pi, cfg.Pd, cfg.mt[0], cfg.mt[1], F, device=0)    # end drift Phi_tau
+    d.decode(rx, off, rho, None, alpha0=a0, betaN=bN, extrinsic=True)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        d.decode(rx, off, rho, None, alpha0=a0, betaN=bN, extrinsic=True)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = float(np.median(ts))
+    out = [{"config": "C2+soft-boundaries+extrinsic (NEXT-1, NEXT-4)", "frames": F, "ms_per_batch": ms,
+            "frames_per_s": F / ms * 1e3}]
+    d.mc_run(cfg.seed, 0, 8192, 8192)
+    ts = []
+    for k in range(steps):
+        t0 = time.perf_counter()
+        res = d.mc_run(cfg.seed, 10_000_000 + k * F, F, 16384)
+        ts.append(time.perf_counter() - t0)
+    s = float(np.median(ts))
+    out.append({"config": "C2 Monte-Carlo generate+decode+count (NEXT-3)", "frames": F, "ms_per_batch": s * 1e3,
+                "frames_per_s": F / s, "symbol_error_rate": res["symbol_errors"] / (F * cfg.N),
+                "frame_error_rate": res["frame_errors"] / F, "redraws": res["redraws"]})
+    return out
+
+
 def main():
     out = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else "gpurun_out/sweep.json"
     steps = int(sys.argv[sys.argv.index("--steps") + 1]) if "--steps" in sys.argv else 3
@@ -70,6 +109,9 @@ def main():
             r["wall_s"] = time.time() - t
             print(json.dumps(r), flush=True)
             res.append(r)
+    for r in run_next(steps):
+        print(json.dumps(r), flush=True)
+        res.append(r)
     os.makedirs(os.path.dirname(out) or ".", exist_ok=True)
     json.dump(res, open(out, "w"), indent=1)
 
