@@ -201,9 +201,11 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   const size_t nwin = kLatticeThreads;
   P->app_smem = nwin * sizeof(double) + (size_t)kAppSegCap * std::min(d->q, kAppDChunk) * sizeof(double) +
                 nwin * app_tstride(d->q) * 4 + (size_t)d->q * 4;
-  if (mode != kSchedStored && d->kern.W == 2) P->app_smem = app_x2_smem(d->q, d->Mn);
-  // packed-pair APP with one tile per frame writes L directly (no accumulators / finalize)
-  P->direct_L = mode == kSchedLocal || (mode == kSchedGammaSum && d->kern.W == 2 && tiles_per_frame(d->Mt) == 1);
+  if (mode != kSchedStored && d->kern.W == 2)
+    P->app_smem = d->kern.app_W == 2 ? app_x2_smem(d->q, d->Mn) : app_x1_smem(d->q);
+  // tiled APP with one warp tile per frame writes L directly (no accumulators / finalize)
+  P->direct_L = mode == kSchedLocal ||
+                (mode == kSchedGammaSum && d->kern.W == 2 && tiles_per_frame_w(d->Mt, d->kern.app_W) == 1);
   P->local_smem = (size_t)kLocalWarps * local_warp_smem(d->Mn, d->q);
   P->l1_smem = (size_t)d->q * 4;
   return BSIDMAP_OK;
@@ -273,7 +275,8 @@ int run_chunk(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s,
   const long lanes = (long)p.F * d->Mt;
   const bool tiled = d->kern.W == 2;
   // packed-pair kernels: 4 frame-aligned 64-slot warp tiles per CTA; scalar kernels: 128 flat windows per CTA
-  const unsigned gx_tile = (unsigned)(((long)p.F * tiles_per_frame(d->Mt) + kX2Warps - 1) / kX2Warps);
+  const unsigned gx_tile =
+      (unsigned)(((long)p.F * tiles_per_frame_w(d->Mt, d->kern.app_W) + kX2Warps - 1) / kX2Warps);
   const unsigned gx_flat = (unsigned)((lanes + kLatticeThreads - 1) / kLatticeThreads);
   const unsigned gx = tiled ? gx_tile : gx_flat;
   if (first_chunk) record(d, 0, s);

@@ -12,6 +12,8 @@
       out->gamma_sum = k_gamma_sum<SpecCore<NN, LO, MN>, false>;                        \
       out->gamma_store = k_gamma_sum<SpecCore<NN, LO, MN>, true>;                       \
       out->l1_W = 1;                                                                    \
+      out->app = k_app_x1<SpecCore<NN, LO, MN>>;                                        \
+      out->app_W = 1;                                                                   \
     }                                                                                   \
     return true;                                                                         \
   }                                                                                      \

@@ -304,6 +304,7 @@ struct CoreKernels {
   long nodes;  // corridor nodes per lattice (0 = generic core: computed on host)
   int W;       // windows per lane (1 scalar core, 2 packed-pair core)
   int l1_W;    // windows per lane of the pass-1 kernel (the scalar core may serve pass 1 of a pair core)
+  int app_W;   // windows per lane of the tiled APP kernel (32 * app_W states per warp tile)
   void (*ab_warp[3])(const DecodeParams);  // warp-per-task alpha/beta for M_tau <= 32, 64, 128 (spec only)
   void (*local_fwd)(const DecodeParams);   // fused local schedule, M_tau <= 64 (spec only)
   void (*local_bwd)(const DecodeParams);
@@ -320,6 +321,7 @@ CoreKernels make_core_kernels(long nodes) {
   k.nodes = nodes;
   k.W = 1;
   k.l1_W = 1;
+  k.app_W = 1;
   k.ab_warp[0] = k.ab_warp[1] = k.ab_warp[2] = nullptr;
   k.local_fwd = k.local_bwd = nullptr;
   return k;

@@ -152,8 +152,11 @@ __device__ __forceinline__ double app_weights_p2(const DecodeParams& p, const La
 #ifndef BSIDMAP_APP_BT_SMEM
 #define BSIDMAP_APP_BT_SMEM 1
 #endif
+// per-warp staging of the per-lane contributions c(lane, D): [q][33] floats (odd stride), reduced
+// over the lanes once after the D loop instead of one shuffle chain per D
+__host__ __device__ __forceinline__ size_t app_stage_floats(int q) { return (size_t)q * 33; }
 __host__ __device__ __forceinline__ size_t app_x2_smem(int q, int Mn) {
-  return (size_t)kX2Warps * Mn * 32 * 8 + (size_t)q * 4 * (1 + kX2Warps);
+  return (size_t)kX2Warps * Mn * 32 * 8 + (size_t)q * 4 + (size_t)kX2Warps * (app_stage_floats(q) + q) * 4;
 }
 // smem: s_bt[kX2Warps][M_n][32] (f32x2, the scaled beta corridor of each lane's two windows;
 //       kept in smem, not registers, to free 2 M_n registers) | s_C[q] | s_S[kX2Warps][q] (float)
@@ -164,6 +167,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_APP_MINB) k_app_x2(co
   f32x2* s_bt = reinterpret_cast<f32x2*>(smem);
   uint32_t* s_C = reinterpret_cast<uint32_t*>(s_bt + kX2Warps * MN * 32);
   float* s_S = reinterpret_cast<float*>(s_C + p.q);
+  float* s_stage = s_S + kX2Warps * p.q;
   const int i = blockIdx.y + p.i_base;
   for (int t = threadIdx.x; t < p.q; t += blockDim.x) s_C[t] = p.C[(size_t)i * p.q + t];
   __syncthreads();
@@ -201,6 +205,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_APP_MINB) k_app_x2(co
   }
   const bool live = __any_sync(0xffffffffu, wa > 0.f || wb > 0.f);
   float* S = s_S + warp * p.q;
+  float* stg = s_stage + (size_t)warp * app_stage_floats(p.q);
   if (live) {
     typename Core::Lane lane_t;
     Core::init(lane_t, A.active ? load_window(p, A.f, A.s, A.rho) : 0ull,
@@ -216,16 +221,102 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_APP_MINB) k_app_x2(co
         t0 = ffma2(fo[e], BT(e), t0);
         if (e + 1 < MN) t1 = ffma2(fo[e + 1], BT(e + 1), t1);
       }
-      float c = fmaf(wa, lo_of(t0) + lo_of(t1), wb * (hi_of(t0) + hi_of(t1)));
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-      if (lane == 0) S[D] = pri ? c * __ldg(pri + D) : c;
+      stg[D * 33 + lane] = fmaf(wa, lo_of(t0) + lo_of(t1), wb * (hi_of(t0) + hi_of(t1)));
+    }
+    __syncwarp();
+    for (int D = lane; D < p.q; D += 32) {  // S(D) = P(D) sum over the warp's windows
+      float c = 0.f;
+#pragma unroll 8
+      for (int l = 0; l < 32; l++) c += stg[D * 33 + l];
+      S[D] = pri ? c * __ldg(pri + D) : c;
     }
   }
 #undef BT
   __syncwarp();
   if (T == 1) {
     // the warp holds the whole sum over m': L_i(D) = S(D) / sum_D S(D)
+    float tot = 0.f;
+    if (live)
+      for (int D = lane; D < p.q; D += 32) tot += S[D];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    const bool ok = frame_ok && live && tot > 0.f;
+    const float inv = ok ? 1.f / tot : 0.f;
+    float* Lrow = p.L + ((size_t)f * p.N + i) * p.q;
+    for (int D = lane; D < p.q; D += 32) Lrow[D] = ok ? S[D] * inv : 0.f;
+    if (frame_ok && !ok && lane == 0) p.status[f] = kFrameUnderflow;
+  } else if (live) {
+    const double sc = pow2d(Emax);
+    double* acc = p.Lacc + ((size_t)f * p.N + i) * p.q;
+    for (int D = lane; D < p.q; D += 32) {
+      const float v = S[D];
+      if (v > 0.f) atomicAdd(acc + D, (double)v * sc);
+    }
+  }
+}
+
+// Scalar-core APP on frame-aligned 32-state warp tiles (one window per lane): used where the
+// pair core is register-bound (C3, C5) -- also wastes fewer slots (C3: 9 x 32 vs 5 x 64 for 267).
+__host__ __device__ __forceinline__ int tiles_per_frame_w(int Mt, int W) { return (Mt + 32 * W - 1) / (32 * W); }
+__host__ __device__ __forceinline__ size_t app_x1_smem(int q) {
+  return (size_t)q * 4 + (size_t)kX2Warps * (app_stage_floats(q) + q) * 4;
+}
+
+template <class Core>
+__global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_app_x1(const DecodeParams p) {
+  constexpr int MN = Core::Mn;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint32_t* s_C = reinterpret_cast<uint32_t*>(smem);
+  float* s_S = reinterpret_cast<float*>(s_C + p.q);
+  float* s_stage = s_S + kX2Warps * p.q;
+  const int i = blockIdx.y + p.i_base;
+  for (int t = threadIdx.x; t < p.q; t += blockDim.x) s_C[t] = p.C[(size_t)i * p.q + t];
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T = tiles_per_frame_w(p.Mt, 1);
+  const long tile = (long)blockIdx.x * kX2Warps + warp;
+  const int f = (int)(tile / T);
+  if (f >= p.F) return;  // warp-uniform; no block barrier follows
+  const int mi = (int)(tile % T) * 32 + lane;
+  const LaneGeom A = geom_fm(p, i, f, mi, mi < p.Mt);
+  const bool frame_ok = p.status[f] == kFrameOk;
+  float bt[MN];
+  float wa;
+  int Emax;
+  {
+    const double da = app_weights_p2<MN>(p, A, i, bt);
+    Emax = __reduce_max_sync(0xffffffffu, da > 0.0 ? exp2_of(da) + 2048 : 0) - 2048;
+    wa = (float)(da * pow2d(-Emax));
+  }
+  const bool live = __any_sync(0xffffffffu, wa > 0.f);
+  float* S = s_S + warp * p.q;
+  float* stg = s_stage + (size_t)warp * app_stage_floats(p.q);
+  if (live) {
+    typename Core::Lane lane_t;
+    Core::init(lane_t, A.active ? load_window(p, A.f, A.s, A.rho) : 0ull, p);
+    const float* pri = p.priors ? p.priors + ((size_t)f * p.N + i) * p.q : nullptr;
+    for (int D = 0; D < p.q; D++) {
+      float fo[MN];
+      Core::run(lane_t, s_C[D], p, fo);
+      float t0 = 0.f, t1 = 0.f;
+#pragma unroll
+      for (int e = 0; e < MN; e += 2) {
+        t0 = fmaf(fo[e], bt[e], t0);
+        if (e + 1 < MN) t1 = fmaf(fo[e + 1], bt[e + 1], t1);
+      }
+      stg[D * 33 + lane] = wa * (t0 + t1);
+    }
+    __syncwarp();
+    for (int D = lane; D < p.q; D += 32) {
+      float c = 0.f;
+#pragma unroll 8
+      for (int l = 0; l < 32; l++) c += stg[D * 33 + l];
+      S[D] = pri ? c * __ldg(pri + D) : c;
+    }
+  }
+  __syncwarp();
+  if (T == 1) {
     float tot = 0.f;
     if (live)
       for (int D = lane; D < p.q; D += 32) tot += S[D];
@@ -293,6 +384,7 @@ CoreKernels make_core_kernels_x2_base(long nodes) {
   k.nodes = nodes;
   k.W = 2;
   k.l1_W = 2;
+  k.app_W = 2;
   k.ab_warp[0] = k_alpha_beta_warp<1, Core::Mn>;
   k.ab_warp[1] = k_alpha_beta_warp<2, Core::Mn>;
   k.ab_warp[2] = k_alpha_beta_warp<4, Core::Mn>;
