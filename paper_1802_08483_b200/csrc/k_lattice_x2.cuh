@@ -156,16 +156,17 @@ __device__ __forceinline__ double app_weights_p2(const DecodeParams& p, const La
 // over the lanes once after the D loop instead of one shuffle chain per D
 __host__ __device__ __forceinline__ size_t app_stage_floats(int q) { return (size_t)q * 33; }
 __host__ __device__ __forceinline__ size_t app_x2_smem(int q, int Mn) {
-  return (size_t)kX2Warps * Mn * 32 * 8 + (size_t)q * 4 + (size_t)kX2Warps * (app_stage_floats(q) + q) * 4;
+  return (size_t)kX2Warps * 2 * Mn * 32 * 8 + (size_t)q * 4 + (size_t)kX2Warps * (app_stage_floats(q) + q) * 4;
 }
-// smem: s_bt[kX2Warps][M_n][32] (f32x2, the scaled beta corridor of each lane's two windows;
-//       kept in smem, not registers, to free 2 M_n registers) | s_C[q] | s_S[kX2Warps][q] (float)
+// smem: s_w[kX2Warps][2][M_n][32] (f32x2: the scaled beta corridor of each lane's two windows with
+//       the last lattice row folded in, one table per value of x_n; smem, not registers) | s_C[q] |
+//       s_S[kX2Warps][q] (float) | staging [kX2Warps][q][33]
 template <class Core>
 __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_APP_MINB) k_app_x2(const DecodeParams p) {
   constexpr int MN = Core::Mn;
   extern __shared__ __align__(128) unsigned char smem[];
   f32x2* s_bt = reinterpret_cast<f32x2*>(smem);
-  uint32_t* s_C = reinterpret_cast<uint32_t*>(s_bt + kX2Warps * MN * 32);
+  uint32_t* s_C = reinterpret_cast<uint32_t*>(s_bt + kX2Warps * 2 * MN * 32);
   float* s_S = reinterpret_cast<float*>(s_C + p.q);
   float* s_stage = s_S + kX2Warps * p.q;
   const int i = blockIdx.y + p.i_base;
@@ -182,20 +183,15 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_APP_MINB) k_app_x2(co
   const LaneGeom B = geom_fm(p, i, f, mia + 1, mia + 1 < p.Mt);
   const bool frame_ok = p.status[f] == kFrameOk;
 
-#if BSIDMAP_APP_BT_SMEM
-  f32x2* bt = s_bt + (size_t)warp * MN * 32 + lane;  // bt[e * 32]
-#define BT(e) bt[(e) * 32]
-#else
-  f32x2 bt[MN];
-#define BT(e) bt[e]
-#endif
+  f32x2* wt = s_bt + (size_t)warp * 2 * MN * 32 + lane;  // w1[e] at wt[e*32], w0[e] at wt[(MN+e)*32]
   float wa, wb;
   int Emax;
+  f32x2 bt[MN];
   {
     float ba[MN], bb[MN];
     const double da = app_weights_p2<MN>(p, A, i, ba), db = app_weights_p2<MN>(p, B, i, bb);
 #pragma unroll
-    for (int e = 0; e < MN; e++) BT(e) = pk(ba[e], bb[e]);
+    for (int e = 0; e < MN; e++) bt[e] = pk(ba[e], bb[e]);
     // common power-of-two scale of the tile's weights (max exponent over the warp)
     const double dm = fmax(da, db);
     Emax = __reduce_max_sync(0xffffffffu, dm > 0.0 ? exp2_of(dm) + 2048 : 0) - 2048;
@@ -210,16 +206,21 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_APP_MINB) k_app_x2(co
     typename Core::Lane lane_t;
     Core::init(lane_t, A.active ? load_window(p, A.f, A.s, A.rho) : 0ull,
                B.active ? load_window(p, B.f, B.s, B.rho) : 0ull, p);
+    Core::last_row_weights(lane_t, [&](int e) { return bt[e]; }, [&](int e) -> f32x2& { return wt[e * 32]; },
+                           [&](int e) -> f32x2& { return wt[(MN + e) * 32]; });
     const float* pri = p.priors ? p.priors + ((size_t)f * p.N + i) * p.q : nullptr;
+    const int nb = p.n - 1;
     for (int D = 0; D < p.q; D++) {
+      const uint32_t x = s_C[D];
       f32x2 fo[MN];
-      Core::template run<BSIDMAP_APP_PAIRS>(lane_t, s_C[D], p, fo);
-      // t(m', D) = sum_k G(m', k, D) bt(m', k) for both windows (two chains)
+      Core::template run_penultimate<BSIDMAP_APP_PAIRS>(lane_t, x, p, fo);
+      // t(m', D) = sum_k G_n(m', k, D) bt(m', k) = sum_e G_{n-1}[e] w_{x_n}[e]  (two chains)
+      const f32x2* W = wt + (((x >> nb) & 1u) ? 0 : MN * 32);
       f32x2 t0 = 0ull, t1 = 0ull;
 #pragma unroll
       for (int e = 0; e < MN; e += 2) {
-        t0 = ffma2(fo[e], BT(e), t0);
-        if (e + 1 < MN) t1 = ffma2(fo[e + 1], BT(e + 1), t1);
+        t0 = ffma2(fo[e], W[e * 32], t0);
+        if (e + 1 < MN) t1 = ffma2(fo[e + 1], W[(e + 1) * 32], t1);
       }
       stg[D * 33 + lane] = fmaf(wa, lo_of(t0) + lo_of(t1), wb * (hi_of(t0) + hi_of(t1)));
     }
@@ -231,7 +232,6 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_APP_MINB) k_app_x2(co
       S[D] = pri ? c * __ldg(pri + D) : c;
     }
   }
-#undef BT
   __syncwarp();
   if (T == 1) {
     // the warp holds the whole sum over m': L_i(D) = S(D) / sum_D S(D)
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_app_x1(c
   float wa;
   int Emax;
   {
-    const double da = app_weights_p2<MN>(p, A, i, bt);
+    const double da = app_weights_p2<MN>(p, A, i, bt);  // bt: corridor weights (see app_weights_p2)
     Emax = __reduce_max_sync(0xffffffffu, da > 0.0 ? exp2_of(da) + 2048 : 0) - 2048;
     wa = (float)(da * pow2d(-Emax));
   }
@@ -295,15 +295,27 @@ __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_app_x1(c
   if (live) {
     typename Core::Lane lane_t;
     Core::init(lane_t, A.active ? load_window(p, A.f, A.s, A.rho) : 0ull, p);
+    float w1[MN], w0[MN];  // last lattice row folded into the weights (one table per x_n)
+    Core::last_row_weights(lane_t, bt, w1, w0);
     const float* pri = p.priors ? p.priors + ((size_t)f * p.N + i) * p.q : nullptr;
+    const int nb = p.n - 1;
     for (int D = 0; D < p.q; D++) {
+      const uint32_t x = s_C[D];
       float fo[MN];
-      Core::run(lane_t, s_C[D], p, fo);
+      Core::run_penultimate(lane_t, x, p, fo);
       float t0 = 0.f, t1 = 0.f;
+      if ((x >> nb) & 1u) {
 #pragma unroll
-      for (int e = 0; e < MN; e += 2) {
-        t0 = fmaf(fo[e], bt[e], t0);
-        if (e + 1 < MN) t1 = fmaf(fo[e + 1], bt[e + 1], t1);
+        for (int e = 0; e < MN; e += 2) {
+          t0 = fmaf(fo[e], w1[e], t0);
+          if (e + 1 < MN) t1 = fmaf(fo[e + 1], w1[e + 1], t1);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < MN; e += 2) {
+          t0 = fmaf(fo[e], w0[e], t0);
+          if (e + 1 < MN) t1 = fmaf(fo[e + 1], w0[e + 1], t1);
+        }
       }
       stg[D * 33 + lane] = wa * (t0 + t1);
     }

@@ -84,21 +84,40 @@ struct SpecCore {
   // Rows are issued in pairs: a 4-way branch on (x_R, x_{R+1}) puts rows R and R+1
   // in one basic block, so the scheduler interleaves their two insertion chains
   // (row R+1 node e only needs row R nodes e, e+1) -- ILP 2 without extra registers.
-  template <int R>
+  template <int R, int RLAST = NN>
   __device__ __forceinline__ static void rows(float (&f)[MN], uint32_t x, const Lane& L, const LatticeConst& lc) {
-    if constexpr (R + 1 <= NN) {
+    if constexpr (R + 1 <= RLAST) {
       switch ((x >> (R - 1)) & 3u) {
         case 0u: row<R, true>(f, L.q0, lc); row<R + 1, true>(f, L.q0, lc); break;
         case 1u: row<R, true>(f, L.q1, lc); row<R + 1, true>(f, L.q0, lc); break;
         case 2u: row<R, true>(f, L.q0, lc); row<R + 1, true>(f, L.q1, lc); break;
         default: row<R, true>(f, L.q1, lc); row<R + 1, true>(f, L.q1, lc); break;
       }
-      rows<R + 2>(f, x, L, lc);
-    } else if constexpr (R == NN) {
+      rows<R + 2, RLAST>(f, x, L, lc);
+    } else if constexpr (R == RLAST) {
       if ((x >> (R - 1)) & 1u)
         row<R, true>(f, L.q1, lc);
       else
         row<R, true>(f, L.q0, lc);
+    }
+  }
+
+  // Rows 1..n-1 only (see SpecCoreX2::run_penultimate / last_row_weights).
+  __device__ __forceinline__ static void run_penultimate(const Lane& L, uint32_t x, const DecodeParams& p,
+                                                         float (&f)[MN]) {
+#pragma unroll
+    for (int e = 0; e < MN; e++) f[e] = p.lc.row0[e];
+    if constexpr (NN >= 2) rows<1, NN - 1>(f, x, L, p.lc);
+  }
+  // w_x[e] = bt[e-1] + [j >= 1] bt[e] (Q/Pd)_j(x), the last row (eqn:F_lastrow) folded into t's weights.
+  __device__ __forceinline__ static void last_row_weights(const Lane& L, const float (&bt)[MN], float (&w1)[MN],
+                                                          float (&w0)[MN]) {
+#pragma unroll
+    for (int e = 0; e < MN; e++) {
+      const int j = NN + LO + e;
+      const float del = (e >= 1) ? bt[e - 1] : 0.f;
+      w1[e] = (j >= 1) ? fmaf(bt[e], L.q1[j < 1 ? 1 : j], del) : del;
+      w0[e] = (j >= 1) ? fmaf(bt[e], L.q0[j < 1 ? 1 : j], del) : del;
     }
   }
 

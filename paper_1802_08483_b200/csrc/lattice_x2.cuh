@@ -79,22 +79,52 @@ struct SpecCoreX2 {
 
   // Rows are issued in pairs: a 4-way branch on (x_R, x_{R+1}) puts rows R and R+1 in one
   // basic block so their insertion chains interleave (row R+1 node e needs row R nodes e, e+1).
-  template <int R, bool kPairs>
+  template <int R, bool kPairs, int RLAST = NN>
   __device__ __forceinline__ static void rows(f32x2 (&f)[MN], uint32_t x, const Lane& L, f32x2 a2) {
-    if constexpr (kPairs && R + 1 <= NN) {
+    if constexpr (kPairs && R + 1 <= RLAST) {
       switch ((x >> (R - 1)) & 3u) {
         case 0u: row<R>(f, L.q0, a2); row<R + 1>(f, L.q0, a2); break;
         case 1u: row<R>(f, L.q1, a2); row<R + 1>(f, L.q0, a2); break;
         case 2u: row<R>(f, L.q0, a2); row<R + 1>(f, L.q1, a2); break;
         default: row<R>(f, L.q1, a2); row<R + 1>(f, L.q1, a2); break;
       }
-      rows<R + 2, kPairs>(f, x, L, a2);
-    } else if constexpr (R <= NN) {
+      rows<R + 2, kPairs, RLAST>(f, x, L, a2);
+    } else if constexpr (R <= RLAST) {
       if ((x >> (R - 1)) & 1u)
         row<R>(f, L.q1, a2);
       else
         row<R>(f, L.q0, a2);
-      rows<R + 1, kPairs>(f, x, L, a2);
+      rows<R + 1, kPairs, RLAST>(f, x, L, a2);
+    }
+  }
+
+  // Rows 1..n-1 only: f[e] <- G_{n-1} in diagonal coordinates.  A consumer that only needs
+  // t = sum_k bt(k) G_n(k) folds the last row (eqn:F_lastrow) into its weights:
+  // t = sum_e G_{n-1}[e] w_{x_n}[e], w_x[e] = bt[e-1] + bt[e] (Q/Pd)(y_{n+k_e} | x)  (last_row_weights).
+  template <bool kPairs = false>
+  __device__ __forceinline__ static void run_penultimate(const Lane& L, uint32_t x, const DecodeParams& p,
+                                                         f32x2 (&f)[MN]) {
+#pragma unroll
+    for (int e = 0; e < MN; e++) f[e] = pk(p.lc.row0[e], p.lc.row0[e]);
+    rows<1, kPairs, NN - 1>(f, x, L, pk(p.lc.a, p.lc.a));
+  }
+
+  // w1 (x_n = 1), w0 (x_n = 0) of run_penultimate from the corridor weights bt[e] of both windows.
+  // Row n node e' (column j'): G_n[e'] = G_{n-1}[e'+1] + [j' >= 1] (Q/Pd)_{j'} G_{n-1}[e'], so the
+  // coefficient of G_{n-1}[e] in sum_e' bt[e'] G_n[e'] is bt[e-1] + [j >= 1] bt[e] (Q/Pd)_j.
+  template <class BtAt, class W1At, class W0At>
+  __device__ __forceinline__ static void last_row_weights(const Lane& L, BtAt bt, W1At w1, W0At w0) {
+#pragma unroll
+    for (int e = 0; e < MN; e++) {
+      const int j = NN + LO + e;
+      const f32x2 del = (e >= 1) ? bt(e - 1) : 0ull;
+      if constexpr (NN + LO >= 1) {  // every last-row column is >= 1
+        w1(e) = ffma2(bt(e), L.q1[j], del);
+        w0(e) = ffma2(bt(e), L.q0[j], del);
+      } else {
+        w1(e) = (j >= 1) ? ffma2(bt(e), L.q1[j < 1 ? 1 : j], del) : del;
+        w0(e) = (j >= 1) ? ffma2(bt(e), L.q0[j < 1 ? 1 : j], del) : del;
+      }
     }
   }
 
