@@ -146,6 +146,7 @@ struct Plan {
   void (*ab_warp)(const DecodeParams);  // warp-per-task alpha/beta kernel or nullptr
   bool direct_L;                         // APP pass writes normalised L rows itself
   size_t local_smem;                     // k_local_fwd / k_local_bwd dynamic smem
+  void (*l1_kernel)(const DecodeParams);  // pass-1 kernel of the recompute schedules
 };
 
 size_t budget(const bsidmap_decoder* d) {
@@ -207,7 +208,11 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   P->direct_L = mode == kSchedLocal ||
                 (mode == kSchedGammaSum && d->kern.W == 2 && tiles_per_frame_w(d->Mt, d->kern.app_W) == 1);
   P->local_smem = (size_t)kLocalWarps * local_warp_smem(d->Mn, d->q);
-  P->l1_smem = (size_t)d->q * 4;
+  // pass 1: hoist the last K lattice rows out of the symbol loop (K = 3 for q > 24, else 2)
+  P->l1_kernel = (d->q > 24 && d->kern.gamma_sum_k3) ? d->kern.gamma_sum_k3 : d->kern.gamma_sum;
+  P->l1_smem = (d->kern.gamma_sum_k3 && mode != kSchedStored)
+                   ? (size_t)d->Mn * kLatticeThreads * 8 + (size_t)d->q * 6 + 64 + 16
+                   : (size_t)d->q * 4;
   return BSIDMAP_OK;
 }
 
@@ -299,7 +304,7 @@ int run_chunk(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s,
   }
   if (!P.direct_L) cudaMemsetAsync(p.Lacc, 0, (size_t)p.F * d->N * d->q * sizeof(double), s);
   if (first_chunk) record(d, 1, s);
-  auto l1 = P.mode == kSchedStored ? d->kern.gamma_store : d->kern.gamma_sum;
+  auto l1 = P.mode == kSchedStored ? d->kern.gamma_store : P.l1_kernel;
   for_i_slices(d->N, [&](int i0, int ni) {
     p.i_base = i0;
     l1<<<dim3(d->kern.l1_W == 2 ? (unsigned)((lanes + 2 * kLatticeThreads - 1) / (2 * kLatticeThreads)) : gx_flat, ni),
@@ -440,6 +445,7 @@ int bsidmap_decode_batch_opts(bsidmap_decoder* d, int F, const uint32_t* rx, con
   const Layout l = layout(d, P.chunk, P.mode);
   if ((rc = ensure_ws(d, l.total))) return rc;
   if ((rc = set_smem(d, P.ab_warp ? (const void*)P.ab_warp : (const void*)k_alpha_beta, P.ab_smem))) return rc;
+  if ((rc = set_smem(d, (const void*)P.l1_kernel, P.l1_smem))) return rc;
   if (P.mode == kSchedLocal) {
     if ((rc = set_smem(d, (const void*)d->kern.local_fwd, P.local_smem))) return rc;
     if ((rc = set_smem(d, (const void*)d->kern.local_bwd, P.local_smem))) return rc;

@@ -297,6 +297,7 @@ __global__ void __launch_bounds__(kLatticeThreads) k_gamma_dump(const DecodePara
 // Kernel table for one lattice core.
 struct CoreKernels {
   void (*gamma_sum)(const DecodeParams);
+  void (*gamma_sum_k3)(const DecodeParams);  // pass 1 with 3 hoisted rows (large q); nullptr = none
   void (*gamma_store)(const DecodeParams);
   void (*app)(const DecodeParams);
   void (*app_stored)(const DecodeParams);
@@ -314,6 +315,7 @@ template <class Core>
 CoreKernels make_core_kernels(long nodes) {
   CoreKernels k;
   k.gamma_sum = k_gamma_sum<Core, false>;
+  k.gamma_sum_k3 = nullptr;
   k.gamma_store = k_gamma_sum<Core, true>;
   k.app = k_app<Core>;
   k.app_stored = k_app_stored<Core::Mn>;

@@ -120,6 +120,181 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Pass 1 with the last K lattice rows hoisted out of the symbol loop.  The rows are linear in
+// the row they read and rows n-K+1..n depend only on the codeword's last K bits, so
+//   Gamma_i(m', .) = sum_cls Last_cls( sum_{D : C_i(D) ends in cls} P(D) G_{n-K}(m', ., D) ):
+// the symbols are visited class by class (a per-CTA counting sort of C_i by its last K bits)
+// and the last K rows run once per class instead of once per symbol.  Exact algebra; the
+// node count of the algorithm is unchanged (the roofline still counts 5 flops per node).
+template <int K>
+__host__ __device__ __forceinline__ size_t cls_smem(int q, int Mn, int lanes_pairs) {
+  return (size_t)q * 4 + (size_t)((q * 2 + 15) / 16) * 16 + 64 + (size_t)Mn * lanes_pairs * 8;
+}
+
+// Warp 0 of the CTA sorts C_i(0..q-1) by class (stable): s_C[k] = codeword, s_D[k] = its symbol,
+// s_start[c] = first position of class c (s_start[NC] = q).  Call before a __syncthreads.
+template <int K>
+__device__ __forceinline__ void class_order(const DecodeParams& p, int i, uint32_t* s_C, uint16_t* s_D, int* s_start) {
+  constexpr int NC = 1 << K;
+  const int lane = threadIdx.x & 31;
+  if ((threadIdx.x >> 5) != 0) return;
+  const uint32_t* Ci = p.C + (size_t)i * p.q;
+  const int sh = p.n - K;
+  int cnt[NC];
+#pragma unroll
+  for (int c = 0; c < NC; c++) cnt[c] = 0;
+  for (int b = 0; b < p.q; b += 32) {
+    const int D = b + lane;
+    const int cl = D < p.q ? (int)((Ci[D] >> sh) & (NC - 1)) : -1;
+#pragma unroll
+    for (int c = 0; c < NC; c++) cnt[c] += __popc(__ballot_sync(0xffffffffu, cl == c));
+  }
+  int off[NC];
+  int run = 0;
+#pragma unroll
+  for (int c = 0; c < NC; c++) {
+    off[c] = run;
+    if (lane == 0) s_start[c] = run;
+    run += cnt[c];
+  }
+  if (lane == 0) s_start[NC] = p.q;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int b = 0; b < p.q; b += 32) {
+    const int D = b + lane;
+    const uint32_t w = D < p.q ? Ci[D] : 0u;
+    const int cl = D < p.q ? (int)((w >> sh) & (NC - 1)) : -1;
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+      const uint32_t m = __ballot_sync(0xffffffffu, cl == c);
+      if (cl == c) {
+        const int pos = off[c] + __popc(m & lt);
+        s_C[pos] = w;
+        s_D[pos] = (uint16_t)D;
+      }
+      off[c] += __popc(m);
+    }
+  }
+}
+
+template <class Core, int K>
+__global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_x2_cls(const DecodeParams p) {
+  constexpr int MN = Core::Mn;
+  constexpr int NC = 1 << K;
+  extern __shared__ __align__(128) unsigned char smem[];
+  f32x2* s_res = reinterpret_cast<f32x2*>(smem);                      // [MN][128] per-lane result
+  uint32_t* s_C = reinterpret_cast<uint32_t*>(s_res + MN * kLatticeThreads);
+  int* s_start = reinterpret_cast<int*>(s_C + p.q);
+  uint16_t* s_D = reinterpret_cast<uint16_t*>(s_start + 16);
+  const int i = blockIdx.y + p.i_base;
+  class_order<K>(p, i, s_C, s_D, s_start);
+  __syncthreads();
+
+  const long ga = (long)blockIdx.x * (2 * blockDim.x) + threadIdx.x;
+  const LaneGeom A = lane_geom_at(p, i, ga), B = lane_geom_at(p, i, ga + blockDim.x);
+  f32x2 acc[MN];
+#pragma unroll
+  for (int e = 0; e < MN; e++) acc[e] = 0ull;
+  if (__any_sync(0xffffffffu, A.active || B.active)) {
+    typename Core::Lane lane;
+    Core::init(lane, A.active ? load_window(p, A.f, A.s, A.rho) : 0ull,
+               B.active ? load_window(p, B.f, B.s, B.rho) : 0ull, p);
+    const float* pa = p.priors ? p.priors + ((size_t)A.f * p.N + i) * p.q : nullptr;
+    const float* pb = p.priors ? p.priors + ((size_t)B.f * p.N + i) * p.q : nullptr;
+    f32x2* res = s_res + threadIdx.x;  // res[e * 128]
+    bool first = true;
+    int k = 0;
+#pragma unroll 1
+    for (int c = 0; c < NC; c++) {
+      const int kend = s_start[c + 1];
+      if (k == kend) continue;
+#pragma unroll
+      for (int e = 0; e < MN; e++) acc[e] = 0ull;
+      for (; k < kend; k++) {
+        const int D = s_D[k];
+        const f32x2 P = pa ? pk(__ldg(pa + D), __ldg(pb + D)) : pk(1.f, 1.f);
+        f32x2 fo[MN];
+        Core::template run_prefix<K, BSIDMAP_L1_PAIRS>(lane, s_C[k], p, fo);
+#pragma unroll
+        for (int e = 0; e < MN; e++) acc[e] = ffma2(P, fo[e], acc[e]);
+      }
+      Core::template apply_last_rows<K>(lane, (uint32_t)c, p, acc);
+#pragma unroll
+      for (int e = 0; e < MN; e++) {
+        if (!first) acc[e] = fadd2(acc[e], res[e * kLatticeThreads]);
+        res[e * kLatticeThreads] = acc[e];
+      }
+      first = false;
+    }
+  }
+  const float sc = p.priors ? 1.f : 1.f / p.q;
+  if (A.in) {
+    float* out = p.Gsum + ((size_t)A.f * p.N + i) * MN * p.Mtp + A.mi;
+#pragma unroll
+    for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, A, e) ? sc * lo_of(acc[e]) : 0.f;
+  }
+  if (B.in) {
+    float* out = p.Gsum + ((size_t)B.f * p.N + i) * MN * p.Mtp + B.mi;
+#pragma unroll
+    for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, B, e) ? sc * hi_of(acc[e]) : 0.f;
+  }
+}
+
+// Scalar-core version (one window per lane, flat geometry) for the register-heavy shapes.
+template <class Core, int K>
+__global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_sum_cls(const DecodeParams p) {
+  constexpr int MN = Core::Mn;
+  constexpr int NC = 1 << K;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* s_res = reinterpret_cast<float*>(smem);  // [MN][128]
+  uint32_t* s_C = reinterpret_cast<uint32_t*>(smem + (size_t)MN * kLatticeThreads * 8);
+  int* s_start = reinterpret_cast<int*>(s_C + p.q);
+  uint16_t* s_D = reinterpret_cast<uint16_t*>(s_start + 16);
+  const int i = blockIdx.y + p.i_base;
+  class_order<K>(p, i, s_C, s_D, s_start);
+  __syncthreads();
+
+  const LaneGeom G = lane_geom(p, i);
+  float acc[MN];
+#pragma unroll
+  for (int e = 0; e < MN; e++) acc[e] = 0.f;
+  if (__any_sync(0xffffffffu, G.active)) {
+    typename Core::Lane lane;
+    Core::init(lane, G.active ? load_window(p, G.f, G.s, G.rho) : 0ull, p);
+    const float* pri = p.priors ? p.priors + ((size_t)G.f * p.N + i) * p.q : nullptr;
+    float* res = s_res + threadIdx.x;
+    bool first = true;
+    int k = 0;
+#pragma unroll 1
+    for (int c = 0; c < NC; c++) {
+      const int kend = s_start[c + 1];
+      if (k == kend) continue;
+#pragma unroll
+      for (int e = 0; e < MN; e++) acc[e] = 0.f;
+      for (; k < kend; k++) {
+        const float P = pri ? __ldg(pri + s_D[k]) : 1.f;
+        float fo[MN];
+        Core::template run_prefix<K>(lane, s_C[k], p, fo);
+#pragma unroll
+        for (int e = 0; e < MN; e++) acc[e] = fmaf(P, fo[e], acc[e]);
+      }
+      Core::template apply_last_rows<K>(lane, (uint32_t)c, p, acc);
+#pragma unroll
+      for (int e = 0; e < MN; e++) {
+        if (!first) acc[e] += res[e * kLatticeThreads];
+        res[e * kLatticeThreads] = acc[e];
+      }
+      first = false;
+    }
+  }
+  if (G.in) {
+    const float sc = p.priors ? 1.f : 1.f / p.q;
+    float* out = p.Gsum + ((size_t)G.f * p.N + i) * MN * p.Mtp + G.mi;
+#pragma unroll
+    for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, G, e) ? sc * acc[e] : 0.f;
+  }
+}
+
 // beta_{i+1}(m'+k) of one window, scaled by 2^-E (E = exponent of its corridor max),
 // as FP32 in [0, 2); returns w = alpha_i(m') 2^E (FP64) so that w * bt = alpha * beta exactly.
 template <int MN>
@@ -388,7 +563,8 @@ CoreKernels make_core_kernels_x2(long nodes);  // defined in k_local_x2.cuh (nee
 template <class Core>
 CoreKernels make_core_kernels_x2_base(long nodes) {
   CoreKernels k;
-  k.gamma_sum = k_gamma_sum_x2<Core, false>;
+  k.gamma_sum = k_gamma_sum_x2_cls<Core, 2>;
+  k.gamma_sum_k3 = k_gamma_sum_x2_cls<Core, 3>;
   k.gamma_store = k_gamma_sum_x2<Core, true>;
   k.app = k_app_x2<Core>;
   k.app_stored = k_app_stored<Core::Mn>;

@@ -102,6 +102,19 @@ struct SpecCore {
     }
   }
 
+  // Rows 1..n-K and the last K rows for a class (see SpecCoreX2::run_prefix / apply_last_rows).
+  template <int K>
+  __device__ __forceinline__ static void run_prefix(const Lane& L, uint32_t x, const DecodeParams& p, float (&f)[MN]) {
+#pragma unroll
+    for (int e = 0; e < MN; e++) f[e] = p.lc.row0[e];
+    if constexpr (NN - K >= 1) rows<1, NN - K>(f, x, L, p.lc);
+  }
+  template <int K>
+  __device__ __forceinline__ static void apply_last_rows(const Lane& L, uint32_t cls, const DecodeParams& p,
+                                                         float (&f)[MN]) {
+    rows<NN - K + 1, NN>(f, cls << (NN - K), L, p.lc);
+  }
+
   // Rows 1..n-1 only (see SpecCoreX2::run_penultimate / last_row_weights).
   __device__ __forceinline__ static void run_penultimate(const Lane& L, uint32_t x, const DecodeParams& p,
                                                          float (&f)[MN]) {

@@ -28,6 +28,11 @@ __device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
   return d;
 }
+__device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 __device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
   f32x2 d;
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
@@ -107,6 +112,21 @@ struct SpecCoreX2 {
 #pragma unroll
     for (int e = 0; e < MN; e++) f[e] = pk(p.lc.row0[e], p.lc.row0[e]);
     rows<1, kPairs, NN - 1>(f, x, L, pk(p.lc.a, p.lc.a));
+  }
+
+  // Rows 1..n-K (the rows that depend on codeword bits other than the last K) and, separately,
+  // the last K rows for the class cls = (x_{n-K+1}..x_n) applied to any vector f: the lattice rows
+  // are linear in the row they read, so sum_D P(D) G_n(D) = sum_cls Last_cls(sum_{D in cls} P(D) G_{n-K}(D)).
+  template <int K, bool kPairs = false>
+  __device__ __forceinline__ static void run_prefix(const Lane& L, uint32_t x, const DecodeParams& p, f32x2 (&f)[MN]) {
+#pragma unroll
+    for (int e = 0; e < MN; e++) f[e] = pk(p.lc.row0[e], p.lc.row0[e]);
+    rows<1, kPairs, NN - K>(f, x, L, pk(p.lc.a, p.lc.a));
+  }
+  template <int K>
+  __device__ __forceinline__ static void apply_last_rows(const Lane& L, uint32_t cls, const DecodeParams& p,
+                                                         f32x2 (&f)[MN]) {
+    rows<NN - K + 1, false, NN>(f, cls << (NN - K), L, pk(p.lc.a, p.lc.a));
   }
 
   // w1 (x_n = 1), w0 (x_n = 0) of run_penultimate from the corridor weights bt[e] of both windows.
