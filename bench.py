@@ -250,7 +250,7 @@ def main():
     value = total_frames / (max_ms / 1e3)
 
     # roofline of the dominant kernel: lattice pass 1 vs pass 2, whichever takes longer on average
-    ph = np.array(phases)  # [steps][5]
+    ph = np.array(phases)  # [steps][6]: init, pass 1, exposed alpha/beta, pass 2, finalize, alpha/beta busy
     mean_ph = ph.mean(0)
     dominant = 1 if mean_ph[1] >= mean_ph[3] else 3
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -323,7 +323,8 @@ def main():
                          "flops_per_launch": flops_pass, "launch_ms": float(mean_ph[dominant])},
             "phase_ms": {"init": float(mean_ph[0]), "lattice_pass1": float(mean_ph[1]),
                          "alpha_beta": float(mean_ph[2]), "lattice_pass2": float(mean_ph[3]),
-                         "finalize": float(mean_ph[4])},
+                         "finalize": float(mean_ph[4]),
+                         "alpha_beta_busy": float(mean_ph[5]) if len(mean_ph) > 5 else float(mean_ph[2])},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

@@ -148,8 +148,15 @@ int bsidmap_set_mode(bsidmap_decoder *d, int mode);
  * Per-phase device timing of the next decodes (CUDA events on the decode stream).
  * bsidmap_phase_times writes up to n_max entries of the LAST decode_batch, in ms:
  *   [0] status init + accumulator clear, [1] lattice pass 1 (gamma / Gamma),
- *   [2] alpha/beta recursions, [3] lattice pass 2 / stored APP, [4] finalize.
- * and returns the number written.  It synchronises the decode stream.
+ *   [2] alpha/beta recursions, [3] lattice pass 2 / stored APP, [4] finalize,
+ *   [5] alpha/beta busy time,
+ * and returns the number written.  It synchronises the decode stream.  In the Gamma-sum
+ * schedule the batch is split into sub-batches whose alpha/beta recursions run on a
+ * high-priority side stream, overlapped with the lattice passes of the other sub-batches
+ * (automatic: 2 sub-batches when the alpha/beta grid cannot fill the GPU, else off; the
+ * environment variable BSIDMAP_AB_SUB read at create overrides it, 1 = off);
+ * then [1] and [3] span all sub-batches' lattice launches, [2] is the exposed part of
+ * alpha/beta on the decode stream and [5] its busy time on the side stream.
  */
 int bsidmap_set_timing(bsidmap_decoder *d, int enable);
 int bsidmap_phase_times(bsidmap_decoder *d, float *ms, int n_max);

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <set>
 #include <string>
@@ -52,6 +53,7 @@ using namespace bsidmap;
 namespace {
 constexpr int kPhases = 5;
 constexpr int kHostSub = 8;  // sub-batches of the host-buffer pipeline
+constexpr int kMaxAbSub = 4;  // sub-batches of the alpha/beta-overlapped Gamma-sum pipeline
 std::string g_err;  // failures without a decoder (create)
 }  // namespace
 
@@ -79,6 +81,15 @@ struct bsidmap_decoder {
   size_t budget_cache = 0;
   int budget_frames = -1, budget_mode = -1;
   std::vector<std::pair<const void*, size_t>> smem_set;
+  // alpha/beta overlap: sub-batch k's alpha/beta recursions run on a high-priority side
+  // stream while the lattice passes of the other sub-batches run on the decode stream
+  int ab_sub = 0;                       // sub-batches per chunk (0 = automatic, 1 = no overlap)
+  int num_sms = 148;
+  int app_kp = -1;                      // pass-2 prefix length override (-1 = automatic)
+  cudaStream_t s_ab = nullptr;
+  cudaEvent_t ev_p1[kMaxAbSub] = {}, ev_ab[kMaxAbSub] = {};
+  cudaEvent_t ev_abt[2] = {};           // alpha/beta stream busy time (timed decodes)
+  bool ab_overlapped = false;           // last decode used the side stream
   // timing
   bool timing = false;
   cudaEvent_t ev[kPhases + 1] = {};
@@ -147,6 +158,9 @@ struct Plan {
   bool direct_L;                         // APP pass writes normalised L rows itself
   size_t local_smem;                     // k_local_fwd / k_local_bwd dynamic smem
   void (*l1_kernel)(const DecodeParams);  // pass-1 kernel of the recompute schedules
+  int ab_sub;                              // sub-batches of the alpha/beta-overlapped pipeline
+  void (*app_kernel)(const DecodeParams);  // pass-2 kernel (prefix-sharing instance where available)
+  int app_kp;                              // its prefix length (0 = none)
 };
 
 size_t budget(const bsidmap_decoder* d) {
@@ -210,6 +224,24 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   P->local_smem = (size_t)kLocalWarps * local_warp_smem(d->Mn, d->q);
   // pass 1: hoist the last K lattice rows out of the symbol loop (K = 3 for q > 24, else 2)
   P->l1_kernel = (d->q > 24 && d->kern.gamma_sum_k3) ? d->kern.gamma_sum_k3 : d->kern.gamma_sum;
+  // pass 2: share lattice rows 1..KP between symbols with equal first KP codeword bits
+  P->app_kp = (mode == kSchedStored) ? 0 : app_prefix_bits(d->q, d->n);
+  if (d->app_kp >= 0) P->app_kp = (d->app_kp == 0 || d->app_kp > d->n - 2) ? 0 : std::min(4, std::max(2, d->app_kp));
+  P->app_kernel = (mode == kSchedStored) ? d->kern.app_stored : d->kern.app;
+  if (P->app_kp > 0 && d->kern.app_pre[P->app_kp - 2])
+    P->app_kernel = d->kern.app_pre[P->app_kp - 2];
+  else
+    P->app_kp = 0;
+  // alpha/beta overlap (Gamma-sum only): measured on B200 it only pays where the alpha/beta grid
+  // cannot fill the GPU (one CTA per frame and direction, 2F <= #SMs: C5 at 32 frames/GPU,
+  // 401 vs 424 ms); with a full grid the recursions compete with the lattice passes for issue
+  // slots and the step time is unchanged (C2, C4) or worse (C3: 212 vs 208 ms) -- tools/exp_ab.sh
+  if (mode != kSchedGammaSum)
+    P->ab_sub = 1;
+  else if (d->ab_sub > 0)
+    P->ab_sub = std::min(kMaxAbSub, d->ab_sub);
+  else
+    P->ab_sub = (!P->ab_warp && 2L * chunk <= d->num_sms) ? 2 : 1;
   P->l1_smem = (d->kern.gamma_sum_k3 && mode != kSchedStored)
                    ? (size_t)d->Mn * kLatticeThreads * 8 + (size_t)d->q * 6 + 64 + 16
                    : (size_t)d->q * 4;
@@ -276,14 +308,78 @@ void for_i_slices(int N, Fn fn) {
   for (int i0 = 0; i0 < N; i0 += 65535) fn(i0, std::min(65535, N - i0));
 }
 
-int run_chunk(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s, bool first_chunk, bool last_chunk) {
+
+// The per-frame slice [f0, f0 + nf) of a chunk's parameters (every per-frame array offset).
+DecodeParams sub_params(const DecodeParams& p, int f0, int nf) {
+  DecodeParams s = p;
+  const size_t N = (size_t)p.N, q = (size_t)p.q, Mt = (size_t)p.Mt;
+  s.F = nf;
+  s.rx_off += f0;
+  s.rho += f0;
+  if (s.priors) s.priors += (size_t)f0 * N * q;
+  if (s.alpha0) s.alpha0 += (size_t)f0 * Mt;
+  if (s.betaN) s.betaN += (size_t)f0 * Mt;
+  s.status += f0;
+  if (s.Gsum) s.Gsum += (size_t)f0 * N * p.Mn * p.Mtp;
+  if (s.gamma) s.gamma += (size_t)f0 * N * q * p.Mn * Mt;
+  s.alpha += (size_t)f0 * (N + 1) * Mt;
+  if (s.beta) s.beta += (size_t)f0 * (N + 1) * Mt;
+  if (s.Lacc) s.Lacc += (size_t)f0 * N * q;
+  s.L += (size_t)f0 * N * q;
+  return s;
+}
+
+int ensure_ab_stream(bsidmap_decoder* d) {
+  if (d->s_ab) return BSIDMAP_OK;
+  int lo = 0, hi = 0;
+  cudaError_t e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&d->s_ab, cudaStreamNonBlocking, hi);
+  for (int k = 0; e == cudaSuccess && k < kMaxAbSub; k++) {
+    e = cudaEventCreateWithFlags(&d->ev_p1[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_ab[k], cudaEventDisableTiming);
+  }
+  for (int k = 0; e == cudaSuccess && k < 2; k++) e = cudaEventCreate(&d->ev_abt[k]);
+  if (e != cudaSuccess) return cuda_fail(d, e, "alpha/beta stream");
+  return BSIDMAP_OK;
+}
+
+void launch_pass1(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s) {
   const long lanes = (long)p.F * d->Mt;
-  const bool tiled = d->kern.W == 2;
-  // packed-pair kernels: 4 frame-aligned 64-slot warp tiles per CTA; scalar kernels: 128 flat windows per CTA
+  const unsigned gx_flat = (unsigned)((lanes + kLatticeThreads - 1) / kLatticeThreads);
+  auto l1 = P.mode == kSchedStored ? d->kern.gamma_store : P.l1_kernel;
+  for_i_slices(d->N, [&](int i0, int ni) {
+    p.i_base = i0;
+    l1<<<dim3(d->kern.l1_W == 2 ? (unsigned)((lanes + 2 * kLatticeThreads - 1) / (2 * kLatticeThreads)) : gx_flat, ni),
+         kLatticeThreads, P.l1_smem, s>>>(p);
+    d->launches++;
+  });
+}
+
+void launch_alpha_beta(bsidmap_decoder* d, const Plan& P, const DecodeParams& p, cudaStream_t s) {
+  if (P.ab_warp) {
+    const long tasks = 2L * p.F, per = kAbWarpThreads / 32;
+    P.ab_warp<<<(unsigned)((tasks + per - 1) / per), kAbWarpThreads, P.ab_smem, s>>>(p);
+  } else {
+    k_alpha_beta<<<dim3(p.F, 2), P.ab_threads, P.ab_smem, s>>>(p, P.ab_stages);
+  }
+  d->launches++;
+}
+
+void launch_pass2(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s) {
+  const long lanes = (long)p.F * d->Mt;
   const unsigned gx_tile =
       (unsigned)(((long)p.F * tiles_per_frame_w(d->Mt, d->kern.app_W) + kX2Warps - 1) / kX2Warps);
   const unsigned gx_flat = (unsigned)((lanes + kLatticeThreads - 1) / kLatticeThreads);
-  const unsigned gx = tiled ? gx_tile : gx_flat;
+  const unsigned gx = d->kern.W == 2 ? gx_tile : gx_flat;
+  auto l2 = P.app_kernel;
+  for_i_slices(d->N, [&](int i0, int ni) {
+    p.i_base = i0;
+    l2<<<dim3(P.mode == kSchedStored ? gx_flat : gx, ni), kLatticeThreads, P.app_smem, s>>>(p);
+    d->launches++;
+  });
+}
+
+int run_chunk(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s, bool first_chunk, bool last_chunk) {
   if (first_chunk) record(d, 0, s);
   k_frame_init<<<(p.F + 255) / 256, 256, 0, s>>>(p);
   d->launches += 1;
@@ -303,31 +399,42 @@ int run_chunk(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s,
     return BSIDMAP_OK;
   }
   if (!P.direct_L) cudaMemsetAsync(p.Lacc, 0, (size_t)p.F * d->N * d->q * sizeof(double), s);
-  if (first_chunk) record(d, 1, s);
-  auto l1 = P.mode == kSchedStored ? d->kern.gamma_store : P.l1_kernel;
-  for_i_slices(d->N, [&](int i0, int ni) {
-    p.i_base = i0;
-    l1<<<dim3(d->kern.l1_W == 2 ? (unsigned)((lanes + 2 * kLatticeThreads - 1) / (2 * kLatticeThreads)) : gx_flat, ni),
-         kLatticeThreads, P.l1_smem, s>>>(p);
-    d->launches++;
-  });
-  p.i_base = 0;
-  if (first_chunk) record(d, 2, s);
-  if (P.ab_warp) {
-    const long tasks = 2L * p.F, per = kAbWarpThreads / 32;
-    P.ab_warp<<<(unsigned)((tasks + per - 1) / per), kAbWarpThreads, P.ab_smem, s>>>(p);
+  const int S = std::min(P.ab_sub, p.F);
+  if (S > 1) {
+    // Sub-batch pipeline: pass 1 of every sub-batch on `s`; the alpha/beta recursions of
+    // sub-batch k (HBM/latency-bound) on the high-priority side stream as soon as its Gamma
+    // is written, overlapping the (FP32-bound) lattice passes of the other sub-batches;
+    // pass 2 of sub-batch k waits for its alpha/beta rows.
+    int rc = ensure_ab_stream(d);
+    if (rc) return rc;
+    if (first_chunk) record(d, 1, s);
+    for (int k = 0; k < S; k++) {
+      const int f0 = (int)((long)p.F * k / S), f1 = (int)((long)p.F * (k + 1) / S);
+      const DecodeParams sp = sub_params(p, f0, f1 - f0);
+      launch_pass1(d, P, sp, s);
+      cudaEventRecord(d->ev_p1[k], s);
+      cudaStreamWaitEvent(d->s_ab, d->ev_p1[k], 0);
+      if (first_chunk && k == 0 && d->timing) cudaEventRecord(d->ev_abt[0], d->s_ab);
+      launch_alpha_beta(d, P, sp, d->s_ab);
+      if (first_chunk && k == S - 1 && d->timing) cudaEventRecord(d->ev_abt[1], d->s_ab);
+      cudaEventRecord(d->ev_ab[k], d->s_ab);
+    }
+    if (first_chunk) record(d, 2, s);
+    for (int k = 0; k < S; k++) {
+      const int f0 = (int)((long)p.F * k / S), f1 = (int)((long)p.F * (k + 1) / S);
+      cudaStreamWaitEvent(s, d->ev_ab[k], 0);
+      if (first_chunk && k == 0) record(d, 3, s);  // phase 2 = the exposed part of alpha/beta
+      launch_pass2(d, P, sub_params(p, f0, f1 - f0), s);
+    }
+    if (first_chunk) d->ab_overlapped = true;
   } else {
-    k_alpha_beta<<<dim3(p.F, 2), P.ab_threads, P.ab_smem, s>>>(p, P.ab_stages);
+    if (first_chunk) record(d, 1, s);
+    launch_pass1(d, P, p, s);
+    if (first_chunk) record(d, 2, s);
+    launch_alpha_beta(d, P, p, s);
+    if (first_chunk) record(d, 3, s);
+    launch_pass2(d, P, p, s);
   }
-  d->launches++;
-  if (first_chunk) record(d, 3, s);
-  auto l2 = P.mode == kSchedStored ? d->kern.app_stored : d->kern.app;
-  for_i_slices(d->N, [&](int i0, int ni) {
-    p.i_base = i0;
-    l2<<<dim3(P.mode == kSchedStored ? gx_flat : gx, ni), kLatticeThreads, P.app_smem, s>>>(p);
-    d->launches++;
-  });
-  p.i_base = 0;
   if (first_chunk) record(d, 4, s);
   if (!P.direct_L) {
     const long rows = (long)p.F * d->N;
@@ -389,6 +496,8 @@ int bsidmap_create(bsidmap_decoder** out, int q, int n, int N, const uint32_t* c
   d->mt_lo = mt_lo; d->mt_hi = mt_hi; d->Mt = mt_hi - mt_lo + 1;
   d->Pi = Pi; d->Pd = Pd; d->Ps = Ps;
   d->mode = mode;
+  if (const char* v = std::getenv("BSIDMAP_AB_SUB")) d->ab_sub = std::max(1, std::atoi(v));
+  if (const char* v = std::getenv("BSIDMAP_APP_KP")) d->app_kp = std::max(0, std::atoi(v));
   // lattice constants (eqn:F, Q-dot); row 0 = insertions only, F_{0,j} = 2^s (Pi/2)^j
   const double Pt = 1.0 - Pi - Pd;
   // G = F / Pd^r grows by at most Pd^-n over the lattice: keep 2^s Pd^-n q M_n below FLT_MAX / 2^10
@@ -413,6 +522,7 @@ int bsidmap_create(bsidmap_decoder** out, int q, int n, int N, const uint32_t* c
     return fail(nullptr, BSIDMAP_EPLAN, "no lattice core for M_n = " + std::to_string(Mn));
   }
   cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&d->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e == cudaSuccess) e = cudaMalloc(&d->d_C, sizeof(uint32_t) * (size_t)N * q);
   if (e == cudaSuccess) e = cudaMemcpy(d->d_C, codebook_host, sizeof(uint32_t) * (size_t)N * q, cudaMemcpyHostToDevice);
   for (int k = 0; e == cudaSuccess && k <= kPhases; k++) e = cudaEventCreate(&d->ev[k]);
@@ -437,6 +547,7 @@ int bsidmap_decode_batch_opts(bsidmap_decoder* d, int F, const uint32_t* rx, con
   if (rc) return rc;
   d->launches = 0;
   d->ev_valid = false;
+  d->ab_overlapped = false;
   if (F == 0) return BSIDMAP_OK;
   cudaSetDevice(d->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -449,8 +560,7 @@ int bsidmap_decode_batch_opts(bsidmap_decoder* d, int F, const uint32_t* rx, con
   if (P.mode == kSchedLocal) {
     if ((rc = set_smem(d, (const void*)d->kern.local_fwd, P.local_smem))) return rc;
     if ((rc = set_smem(d, (const void*)d->kern.local_bwd, P.local_smem))) return rc;
-  } else if ((rc = set_smem(d, (const void*)(P.mode == kSchedStored ? d->kern.app_stored : d->kern.app),
-                            P.app_smem))) {
+  } else if ((rc = set_smem(d, (const void*)P.app_kernel, P.app_smem))) {
     return rc;
   }
   for (int c = 0; c < P.nchunks; c++) {
@@ -555,6 +665,13 @@ void bsidmap_destroy(bsidmap_decoder* d) {
   if (d->ws) cudaFree(d->ws);
   if (d->hs) cudaFree(d->hs);
   if (d->s_copy) cudaStreamDestroy(d->s_copy);
+  if (d->s_ab) cudaStreamDestroy(d->s_ab);
+  for (int k = 0; k < kMaxAbSub; k++) {
+    if (d->ev_p1[k]) cudaEventDestroy(d->ev_p1[k]);
+    if (d->ev_ab[k]) cudaEventDestroy(d->ev_ab[k]);
+  }
+  for (int k = 0; k < 2; k++)
+    if (d->ev_abt[k]) cudaEventDestroy(d->ev_abt[k]);
   for (int k = 0; k < kHostSub; k++)
     if (d->ev_sub[k]) cudaEventDestroy(d->ev_sub[k]);
   if (d->d_C) cudaFree(d->d_C);
@@ -600,6 +717,13 @@ int bsidmap_phase_times(bsidmap_decoder* d, float* ms, int n_max) {
     // phases 0-3 are the first chunk; the last phase runs to the end of the last chunk
     cudaEventElapsedTime(&ms[k], d->ev[k], d->ev[k + 1]);
   }
+  if (k < n_max) {  // [5]: alpha/beta busy time (on the side stream when overlapped)
+    if (d->ab_overlapped)
+      cudaEventElapsedTime(&ms[k], d->ev_abt[0], d->ev_abt[1]);
+    else
+      ms[k] = ms[2];
+    k++;
+  }
   return k;
 }
 
@@ -615,12 +739,13 @@ int bsidmap_plan_info(bsidmap_decoder* d, int F, char* buf, size_t len) {
       buf, len,
       "{\"mode\": \"%s\", \"frames\": %d, \"chunk\": %d, \"chunks\": %d, \"core\": \"%s\", "
       "\"lattice_grid\": [%ld, %d], \"lattice_block\": %d, \"alpha_beta_grid\": [%d, 2], \"alpha_beta_block\": %d, "
-      "\"workspace_bytes\": %zu, \"windows_per_lane\": %d, \"q\": %d, \"n\": %d, \"N\": %d, \"Mn\": %d, \"Mtau\": %d}",
+      "\"workspace_bytes\": %zu, \"windows_per_lane\": %d, \"q\": %d, \"n\": %d, \"N\": %d, \"Mn\": %d, \"Mtau\": %d, "
+      "\"alpha_beta_overlap_subbatches\": %d, \"app_prefix_bits\": %d}",
       sched_name(P.mode), F, P.chunk, P.nchunks, d->spec ? "spec" : "generic",
       d->kern.W == 2 ? ((long)P.chunk * tiles_per_frame(d->Mt) + kX2Warps - 1) / kX2Warps
                      : (lanes + kLatticeThreads - 1) / kLatticeThreads,
       d->N, kLatticeThreads, P.chunk, P.ab_warp ? kAbWarpThreads : P.ab_threads,
-      layout(d, P.chunk, P.mode).total, d->kern.W, d->q, d->n, d->N, d->Mn, d->Mt);
+      layout(d, P.chunk, P.mode).total, d->kern.W, d->q, d->n, d->N, d->Mn, d->Mt, std::min(P.ab_sub, P.chunk), P.app_kp);
   return nb;
 }
 

@@ -13,7 +13,10 @@
       out->gamma_sum_k3 = k_gamma_sum_cls<SpecCore<NN, LO, MN>, 3>;                     \
       out->gamma_store = k_gamma_sum<SpecCore<NN, LO, MN>, true>;                       \
       out->l1_W = 1;                                                                    \
-      out->app = k_app_x1<SpecCore<NN, LO, MN>>;                                        \
+      out->app = k_app_x1<SpecCore<NN, LO, MN>, 0>;                                     \
+      out->app_pre[0] = k_app_x1<SpecCore<NN, LO, MN>, 2>;                              \
+      out->app_pre[1] = k_app_x1<SpecCore<NN, LO, MN>, 3>;                              \
+      out->app_pre[2] = k_app_x1<SpecCore<NN, LO, MN>, 4>;                              \
       out->app_W = 1;                                                                   \
     }                                                                                   \
     return true;                                                                         \

@@ -300,6 +300,7 @@ struct CoreKernels {
   void (*gamma_sum_k3)(const DecodeParams);  // pass 1 with 3 hoisted rows (large q); nullptr = none
   void (*gamma_store)(const DecodeParams);
   void (*app)(const DecodeParams);
+  void (*app_pre[3])(const DecodeParams);  // APP with prefix sharing, KP = 2, 3, 4 first codeword bits (spec only)
   void (*app_stored)(const DecodeParams);
   void (*gamma_dump)(const DecodeParams);
   long nodes;  // corridor nodes per lattice (0 = generic core: computed on host)
@@ -318,6 +319,7 @@ CoreKernels make_core_kernels(long nodes) {
   k.gamma_sum_k3 = nullptr;
   k.gamma_store = k_gamma_sum<Core, true>;
   k.app = k_app<Core>;
+  k.app_pre[0] = k.app_pre[1] = k.app_pre[2] = nullptr;
   k.app_stored = k_app_stored<Core::Mn>;
   k.gamma_dump = k_gamma_dump<Core>;
   k.nodes = nodes;

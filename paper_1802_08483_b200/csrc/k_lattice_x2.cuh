@@ -134,13 +134,15 @@ __host__ __device__ __forceinline__ size_t cls_smem(int q, int Mn, int lanes_pai
 
 // Warp 0 of the CTA sorts C_i(0..q-1) by class (stable): s_C[k] = codeword, s_D[k] = its symbol,
 // s_start[c] = first position of class c (s_start[NC] = q).  Call before a __syncthreads.
+// sh = bit offset of the K class bits (default p.n - K: the last K codeword bits; 0: the first K).
 template <int K>
-__device__ __forceinline__ void class_order(const DecodeParams& p, int i, uint32_t* s_C, uint16_t* s_D, int* s_start) {
+__device__ __forceinline__ void class_order(const DecodeParams& p, int i, uint32_t* s_C, uint16_t* s_D, int* s_start,
+                                            int sh = -1) {
   constexpr int NC = 1 << K;
   const int lane = threadIdx.x & 31;
   if ((threadIdx.x >> 5) != 0) return;
   const uint32_t* Ci = p.C + (size_t)i * p.q;
-  const int sh = p.n - K;
+  if (sh < 0) sh = p.n - K;
   int cnt[NC];
 #pragma unroll
   for (int c = 0; c < NC; c++) cnt[c] = 0;
@@ -155,10 +157,10 @@ __device__ __forceinline__ void class_order(const DecodeParams& p, int i, uint32
 #pragma unroll
   for (int c = 0; c < NC; c++) {
     off[c] = run;
-    if (lane == 0) s_start[c] = run;
+    if (lane == 0 && s_start) s_start[c] = run;
     run += cnt[c];
   }
-  if (lane == 0) s_start[NC] = p.q;
+  if (lane == 0 && s_start) s_start[NC] = p.q;
   const uint32_t lt = (1u << lane) - 1u;
   for (int b = 0; b < p.q; b += 32) {
     const int D = b + lane;
@@ -331,21 +333,39 @@ __device__ __forceinline__ double app_weights_p2(const DecodeParams& p, const La
 // over the lanes once after the D loop instead of one shuffle chain per D
 __host__ __device__ __forceinline__ size_t app_stage_floats(int q) { return (size_t)q * 33; }
 __host__ __device__ __forceinline__ size_t app_x2_smem(int q, int Mn) {
-  return (size_t)kX2Warps * 2 * Mn * 32 * 8 + (size_t)q * 4 + (size_t)kX2Warps * (app_stage_floats(q) + q) * 4;
+  return (size_t)kX2Warps * 2 * Mn * 32 * 8 + (size_t)q * 4 + (size_t)kX2Warps * (app_stage_floats(q) + q) * 4 +
+         (size_t)((q * 2 + 15) / 16) * 16;
+}
+// Symbols are visited in order of their first KP codeword bits (class_order with sh = 0) so
+// that lattice rows 1..KP (run_head) are computed once per distinct prefix; KP = 0: natural order.
+// The prefix length that saves the most nodes for random codebooks: ~log2(q) - 1.
+__host__ __device__ __forceinline__ int app_prefix_bits(int q, int n) {
+  int kp = q <= 8 ? 2 : q <= 16 ? 3 : 4;
+  return kp <= n - 2 ? kp : 0;
 }
 // smem: s_w[kX2Warps][2][M_n][32] (f32x2: the scaled beta corridor of each lane's two windows with
 //       the last lattice row folded in, one table per value of x_n; smem, not registers) | s_C[q] |
 //       s_S[kX2Warps][q] (float) | staging [kX2Warps][q][33]
-template <class Core>
-__global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_APP_MINB) k_app_x2(const DecodeParams p) {
+// prefix sharing keeps the head row live across the symbol loop (+2 M_n registers)
+#ifndef BSIDMAP_APP_MINB_PRE
+#define BSIDMAP_APP_MINB_PRE (Core::kMinBlocks > 2 ? 4 : 2)
+#endif
+template <class Core, int KP>
+__global__ void __launch_bounds__(kLatticeThreads, KP > 0 ? BSIDMAP_APP_MINB_PRE : BSIDMAP_APP_MINB)
+    k_app_x2(const DecodeParams p) {
   constexpr int MN = Core::Mn;
   extern __shared__ __align__(128) unsigned char smem[];
   f32x2* s_bt = reinterpret_cast<f32x2*>(smem);
   uint32_t* s_C = reinterpret_cast<uint32_t*>(s_bt + kX2Warps * 2 * MN * 32);
   float* s_S = reinterpret_cast<float*>(s_C + p.q);
   float* s_stage = s_S + kX2Warps * p.q;
+  uint16_t* s_D = reinterpret_cast<uint16_t*>(s_stage + (size_t)kX2Warps * app_stage_floats(p.q));
   const int i = blockIdx.y + p.i_base;
-  for (int t = threadIdx.x; t < p.q; t += blockDim.x) s_C[t] = p.C[(size_t)i * p.q + t];
+  if constexpr (KP > 0) {
+    class_order<KP>(p, i, s_C, s_D, nullptr, 0);
+  } else {
+    for (int t = threadIdx.x; t < p.q; t += blockDim.x) s_C[t] = p.C[(size_t)i * p.q + t];
+  }
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -385,10 +405,19 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_APP_MINB) k_app_x2(co
                            [&](int e) -> f32x2& { return wt[(MN + e) * 32]; });
     const float* pri = p.priors ? p.priors + ((size_t)f * p.N + i) * p.q : nullptr;
     const int nb = p.n - 1;
-    for (int D = 0; D < p.q; D++) {
-      const uint32_t x = s_C[D];
+    f32x2 fh[MN];  // rows 1..KP of the current prefix
+    for (int k = 0; k < p.q; k++) {
+      const uint32_t x = s_C[k];
       f32x2 fo[MN];
-      Core::template run_penultimate<BSIDMAP_APP_PAIRS>(lane_t, x, p, fo);
+      if constexpr (KP > 0) {
+        if (k == 0 || ((x ^ s_C[k - 1]) & ((1u << KP) - 1u)) != 0u)
+          Core::template run_head<KP, BSIDMAP_APP_PAIRS>(lane_t, x, p, fh);
+#pragma unroll
+        for (int e = 0; e < MN; e++) fo[e] = fh[e];
+        Core::template run_tail<KP, BSIDMAP_APP_PAIRS>(lane_t, x, p, fo);
+      } else {
+        Core::template run_penultimate<BSIDMAP_APP_PAIRS>(lane_t, x, p, fo);
+      }
       // t(m', D) = sum_k G_n(m', k, D) bt(m', k) = sum_e G_{n-1}[e] w_{x_n}[e]  (two chains)
       const f32x2* W = wt + (((x >> nb) & 1u) ? 0 : MN * 32);
       f32x2 t0 = 0ull, t1 = 0ull;
@@ -397,6 +426,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_APP_MINB) k_app_x2(co
         t0 = ffma2(fo[e], W[e * 32], t0);
         if (e + 1 < MN) t1 = ffma2(fo[e + 1], W[(e + 1) * 32], t1);
       }
+      const int D = KP > 0 ? (int)s_D[k] : k;
       stg[D * 33 + lane] = fmaf(wa, lo_of(t0) + lo_of(t1), wb * (hi_of(t0) + hi_of(t1)));
     }
     __syncwarp();
@@ -434,18 +464,27 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_APP_MINB) k_app_x2(co
 // pair core is register-bound (C3, C5) -- also wastes fewer slots (C3: 9 x 32 vs 5 x 64 for 267).
 __host__ __device__ __forceinline__ int tiles_per_frame_w(int Mt, int W) { return (Mt + 32 * W - 1) / (32 * W); }
 __host__ __device__ __forceinline__ size_t app_x1_smem(int q) {
-  return (size_t)q * 4 + (size_t)kX2Warps * (app_stage_floats(q) + q) * 4;
+  return (size_t)q * 4 + (size_t)kX2Warps * (app_stage_floats(q) + q) * 4 + (size_t)((q * 2 + 15) / 16) * 16;
 }
 
-template <class Core>
-__global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_app_x1(const DecodeParams p) {
+#ifndef BSIDMAP_APP1_MINB_PRE
+#define BSIDMAP_APP1_MINB_PRE 3
+#endif
+template <class Core, int KP>
+__global__ void __launch_bounds__(kLatticeThreads, KP > 0 ? BSIDMAP_APP1_MINB_PRE : kLatticeMinBlocks)
+    k_app_x1(const DecodeParams p) {
   constexpr int MN = Core::Mn;
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t* s_C = reinterpret_cast<uint32_t*>(smem);
   float* s_S = reinterpret_cast<float*>(s_C + p.q);
   float* s_stage = s_S + kX2Warps * p.q;
+  uint16_t* s_D = reinterpret_cast<uint16_t*>(s_stage + (size_t)kX2Warps * app_stage_floats(p.q));
   const int i = blockIdx.y + p.i_base;
-  for (int t = threadIdx.x; t < p.q; t += blockDim.x) s_C[t] = p.C[(size_t)i * p.q + t];
+  if constexpr (KP > 0) {
+    class_order<KP>(p, i, s_C, s_D, nullptr, 0);
+  } else {
+    for (int t = threadIdx.x; t < p.q; t += blockDim.x) s_C[t] = p.C[(size_t)i * p.q + t];
+  }
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -474,10 +513,19 @@ __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_app_x1(c
     Core::last_row_weights(lane_t, bt, w1, w0);
     const float* pri = p.priors ? p.priors + ((size_t)f * p.N + i) * p.q : nullptr;
     const int nb = p.n - 1;
-    for (int D = 0; D < p.q; D++) {
-      const uint32_t x = s_C[D];
+    float fh[MN];  // rows 1..KP of the current prefix
+    for (int k = 0; k < p.q; k++) {
+      const uint32_t x = s_C[k];
+      const int D = KP > 0 ? (int)s_D[k] : k;
       float fo[MN];
-      Core::run_penultimate(lane_t, x, p, fo);
+      if constexpr (KP > 0) {
+        if (k == 0 || ((x ^ s_C[k - 1]) & ((1u << KP) - 1u)) != 0u) Core::template run_head<KP>(lane_t, x, p, fh);
+#pragma unroll
+        for (int e = 0; e < MN; e++) fo[e] = fh[e];
+        Core::template run_tail<KP>(lane_t, x, p, fo);
+      } else {
+        Core::run_penultimate(lane_t, x, p, fo);
+      }
       float t0 = 0.f, t1 = 0.f;
       if ((x >> nb) & 1u) {
 #pragma unroll
@@ -566,7 +614,10 @@ CoreKernels make_core_kernels_x2_base(long nodes) {
   k.gamma_sum = k_gamma_sum_x2_cls<Core, 2>;
   k.gamma_sum_k3 = k_gamma_sum_x2_cls<Core, 3>;
   k.gamma_store = k_gamma_sum_x2<Core, true>;
-  k.app = k_app_x2<Core>;
+  k.app = k_app_x2<Core, 0>;
+  k.app_pre[0] = k_app_x2<Core, 2>;
+  k.app_pre[1] = k_app_x2<Core, 3>;
+  k.app_pre[2] = k_app_x2<Core, 4>;
   k.app_stored = k_app_stored<Core::Mn>;
   k.gamma_dump = k_gamma_dump_x2<Core>;
   k.nodes = nodes;

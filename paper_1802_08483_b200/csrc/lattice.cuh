@@ -115,6 +115,19 @@ struct SpecCore {
     rows<NN - K + 1, NN>(f, cls << (NN - K), L, p.lc);
   }
 
+  // Rows 1..KP (shared by symbols with the same first KP codeword bits) and rows KP+1..n-1
+  // (see SpecCoreX2::run_head / run_tail).
+  template <int KP>
+  __device__ __forceinline__ static void run_head(const Lane& L, uint32_t x, const DecodeParams& p, float (&f)[MN]) {
+#pragma unroll
+    for (int e = 0; e < MN; e++) f[e] = p.lc.row0[e];
+    rows<1, KP>(f, x, L, p.lc);
+  }
+  template <int KP>
+  __device__ __forceinline__ static void run_tail(const Lane& L, uint32_t x, const DecodeParams& p, float (&f)[MN]) {
+    if constexpr (KP + 1 <= NN - 1) rows<KP + 1, NN - 1>(f, x, L, p.lc);
+  }
+
   // Rows 1..n-1 only (see SpecCoreX2::run_penultimate / last_row_weights).
   __device__ __forceinline__ static void run_penultimate(const Lane& L, uint32_t x, const DecodeParams& p,
                                                          float (&f)[MN]) {

@@ -114,6 +114,21 @@ struct SpecCoreX2 {
     rows<1, kPairs, NN - 1>(f, x, L, pk(p.lc.a, p.lc.a));
   }
 
+  // Prefix sharing (pass 2): rows 1..KP depend only on the codeword's first KP bits, so symbols
+  // visited in order of those bits share them -- run_head once per distinct prefix, run_tail
+  // (rows KP+1..n-1) per symbol from a copy of the head's row.  Same operations, same order:
+  // bit-identical to run_penultimate.
+  template <int KP, bool kPairs = false>
+  __device__ __forceinline__ static void run_head(const Lane& L, uint32_t x, const DecodeParams& p, f32x2 (&f)[MN]) {
+#pragma unroll
+    for (int e = 0; e < MN; e++) f[e] = pk(p.lc.row0[e], p.lc.row0[e]);
+    rows<1, kPairs, KP>(f, x, L, pk(p.lc.a, p.lc.a));
+  }
+  template <int KP, bool kPairs = false>
+  __device__ __forceinline__ static void run_tail(const Lane& L, uint32_t x, const DecodeParams& p, f32x2 (&f)[MN]) {
+    rows<KP + 1, kPairs, NN - 1>(f, x, L, pk(p.lc.a, p.lc.a));
+  }
+
   // Rows 1..n-K (the rows that depend on codeword bits other than the last K) and, separately,
   // the last K rows for the class cls = (x_{n-K+1}..x_n) applied to any vector f: the lattice rows
   // are linear in the row they read, so sum_D P(D) G_n(D) = sum_cls Last_cls(sum_{D in cls} P(D) G_{n-K}(D)).

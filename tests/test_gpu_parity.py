@@ -240,6 +240,25 @@ def test_chunked_equals_unchunked_and_host_path():
     np.testing.assert_allclose(L3.numpy(), L1, rtol=1e-5, atol=1e-30)
 
 
+@pytest.mark.parametrize("name,frames", [("C2", 37), ("C3", 5)])
+def test_alpha_beta_overlap_subbatches_bit_identical(name, frames, monkeypatch):
+    """The alpha/beta-overlapped sub-batch pipeline (side stream) changes only
+    the launch order: every frame's arithmetic is the same, so L must be bit-identical to the
+    single-stream schedule, and still match the oracle."""
+    cfg = small_cfg(name)
+    b = bsidgen.make_batch(cfg, 11, frames)
+    outs = []
+    for sub in ("1", "3", "4"):
+        monkeypatch.setenv("BSIDMAP_AB_SUB", sub)
+        d, L, st = run_gpu(cfg, b, 3)
+        assert d.plan(frames)["alpha_beta_overlap_subbatches"] == min(int(sub), frames)
+        outs.append((L, st))
+    for L, st in outs[1:]:
+        np.testing.assert_array_equal(st, outs[0][1])
+        np.testing.assert_array_equal(L, outs[0][0])
+    assert_parity(outs[1][0], outs[1][1], run_oracle(cfg, b, range(3)), range(3))
+
+
 def test_modes_agree_and_plan():
     cfg = small_cfg("C2")
     b = bsidgen.make_batch(cfg, 0, 16)
