@@ -17,6 +17,7 @@
 
 #include "../../include/bsidmap.h"
 #include "k_local_x2.cuh"
+#include "k_lattice_x4.cuh"
 
 namespace bsidmap {
 __global__ void k_frame_init(const DecodeParams p);
@@ -86,6 +87,7 @@ struct bsidmap_decoder {
   int ab_sub = 0;                       // sub-batches per chunk (0 = automatic, 1 = no overlap)
   int num_sms = 148;
   int app_kp = -1;                      // pass-2 prefix length override (-1 = automatic)
+  int app_x4 = -1;                      // four-window APP kernel (-1 = automatic, 0 = off)
   cudaStream_t s_ab = nullptr;
   cudaEvent_t ev_p1[kMaxAbSub] = {}, ev_ab[kMaxAbSub] = {};
   cudaEvent_t ev_abt[2] = {};           // alpha/beta stream busy time (timed decodes)
@@ -161,6 +163,7 @@ struct Plan {
   int ab_sub;                              // sub-batches of the alpha/beta-overlapped pipeline
   void (*app_kernel)(const DecodeParams);  // pass-2 kernel (prefix-sharing instance where available)
   int app_kp;                              // its prefix length (0 = none)
+  int app_w4;                              // 1: app_kernel is the four-window k_app_x4 (half-warp tiles)
 };
 
 size_t budget(const bsidmap_decoder* d) {
@@ -232,6 +235,14 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
     P->app_kernel = d->kern.app_pre[P->app_kp - 2];
   else
     P->app_kp = 0;
+  // four windows per lane where the shape has an X4 instance (measured faster)
+  P->app_w4 = 0;
+  if (mode == kSchedGammaSum && d->kern.app_x4 && d->app_x4 != 0) {
+    P->app_kernel = d->kern.app_x4;
+    P->app_kp = 0;
+    P->app_w4 = 1;
+    P->app_smem = app_x4_smem(d->q, d->Mn);
+  }
   // alpha/beta overlap (Gamma-sum only): measured on B200 it only pays where the alpha/beta grid
   // cannot fill the GPU (one CTA per frame and direction, 2F <= #SMs: C5 at 32 frames/GPU,
   // 401 vs 424 ms); with a full grid the recursions compete with the lattice passes for issue
@@ -368,7 +379,8 @@ void launch_alpha_beta(bsidmap_decoder* d, const Plan& P, const DecodeParams& p,
 void launch_pass2(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s) {
   const long lanes = (long)p.F * d->Mt;
   const unsigned gx_tile =
-      (unsigned)(((long)p.F * tiles_per_frame_w(d->Mt, d->kern.app_W) + kX2Warps - 1) / kX2Warps);
+      P.app_w4 ? (unsigned)(((long)p.F * tiles_per_frame(d->Mt) + 2 * kX2Warps - 1) / (2 * kX2Warps))
+               : (unsigned)(((long)p.F * tiles_per_frame_w(d->Mt, d->kern.app_W) + kX2Warps - 1) / kX2Warps);
   const unsigned gx_flat = (unsigned)((lanes + kLatticeThreads - 1) / kLatticeThreads);
   const unsigned gx = d->kern.W == 2 ? gx_tile : gx_flat;
   auto l2 = P.app_kernel;
@@ -498,6 +510,7 @@ int bsidmap_create(bsidmap_decoder** out, int q, int n, int N, const uint32_t* c
   d->mode = mode;
   if (const char* v = std::getenv("BSIDMAP_AB_SUB")) d->ab_sub = std::max(1, std::atoi(v));
   if (const char* v = std::getenv("BSIDMAP_APP_KP")) d->app_kp = std::max(0, std::atoi(v));
+  if (const char* v = std::getenv("BSIDMAP_APP_X4")) d->app_x4 = std::atoi(v);
   // lattice constants (eqn:F, Q-dot); row 0 = insertions only, F_{0,j} = 2^s (Pi/2)^j
   const double Pt = 1.0 - Pi - Pd;
   // G = F / Pd^r grows by at most Pd^-n over the lattice: keep 2^s Pd^-n q M_n below FLT_MAX / 2^10
@@ -740,12 +753,12 @@ int bsidmap_plan_info(bsidmap_decoder* d, int F, char* buf, size_t len) {
       "{\"mode\": \"%s\", \"frames\": %d, \"chunk\": %d, \"chunks\": %d, \"core\": \"%s\", "
       "\"lattice_grid\": [%ld, %d], \"lattice_block\": %d, \"alpha_beta_grid\": [%d, 2], \"alpha_beta_block\": %d, "
       "\"workspace_bytes\": %zu, \"windows_per_lane\": %d, \"q\": %d, \"n\": %d, \"N\": %d, \"Mn\": %d, \"Mtau\": %d, "
-      "\"alpha_beta_overlap_subbatches\": %d, \"app_prefix_bits\": %d}",
+      "\"alpha_beta_overlap_subbatches\": %d, \"app_prefix_bits\": %d, \"app_windows_per_lane\": %d}",
       sched_name(P.mode), F, P.chunk, P.nchunks, d->spec ? "spec" : "generic",
       d->kern.W == 2 ? ((long)P.chunk * tiles_per_frame(d->Mt) + kX2Warps - 1) / kX2Warps
                      : (lanes + kLatticeThreads - 1) / kLatticeThreads,
       d->N, kLatticeThreads, P.chunk, P.ab_warp ? kAbWarpThreads : P.ab_threads,
-      layout(d, P.chunk, P.mode).total, d->kern.W, d->q, d->n, d->N, d->Mn, d->Mt, std::min(P.ab_sub, P.chunk), P.app_kp);
+      layout(d, P.chunk, P.mode).total, d->kern.W, d->q, d->n, d->N, d->Mn, d->Mt, std::min(P.ab_sub, P.chunk), P.app_kp, P.app_w4 ? 4 : d->kern.app_W);
   return nb;
 }
 

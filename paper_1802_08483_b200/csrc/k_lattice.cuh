@@ -301,6 +301,7 @@ struct CoreKernels {
   void (*gamma_store)(const DecodeParams);
   void (*app)(const DecodeParams);
   void (*app_pre[3])(const DecodeParams);  // APP with prefix sharing, KP = 2, 3, 4 first codeword bits (spec only)
+  void (*app_x4)(const DecodeParams);      // APP on four windows per lane (SpecCoreX4; small corridors only)
   void (*app_stored)(const DecodeParams);
   void (*gamma_dump)(const DecodeParams);
   long nodes;  // corridor nodes per lattice (0 = generic core: computed on host)
@@ -320,6 +321,7 @@ CoreKernels make_core_kernels(long nodes) {
   k.gamma_store = k_gamma_sum<Core, true>;
   k.app = k_app<Core>;
   k.app_pre[0] = k.app_pre[1] = k.app_pre[2] = nullptr;
+  k.app_x4 = nullptr;
   k.app_stored = k_app_stored<Core::Mn>;
   k.gamma_dump = k_gamma_dump<Core>;
   k.nodes = nodes;

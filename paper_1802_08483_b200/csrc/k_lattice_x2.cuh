@@ -53,8 +53,8 @@ __device__ __forceinline__ int exp2_of(double x) {  // floor(log2 x) for normal 
 #define BSIDMAP_L1_MINB Core::kMinBlocks
 #endif
 // row pairs (ILP) in pass 1 only where the register budget allows 3 CTAs/SM
-#ifndef BSIDMAP_L1_PAIRS
-#define BSIDMAP_L1_PAIRS (Core::kMinBlocks > 2)
+#ifndef BSIDMAP_L1_GROUP
+#define BSIDMAP_L1_GROUP (Core::kMinBlocks > 2 ? 2 : 1)
 #endif
 template <class Core, bool kStoreGamma>
 __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_x2(const DecodeParams p) {
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_
     for (int D = 0; D < p.q; D++) {
       const f32x2 P = pa ? pk(__ldg(pa + D), __ldg(pb + D)) : pk(1.f, 1.f);
       f32x2 fo[MN];
-      Core::template run<BSIDMAP_L1_PAIRS>(lane, s_C[D], p, fo);
+      Core::template run<BSIDMAP_L1_GROUP>(lane, s_C[D], p, fo);
 #pragma unroll
       for (int e = 0; e < MN; e++) acc[e] = ffma2(P, fo[e], acc[e]);
       if constexpr (kStoreGamma) {
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_
         const int D = s_D[k];
         const f32x2 P = pa ? pk(__ldg(pa + D), __ldg(pb + D)) : pk(1.f, 1.f);
         f32x2 fo[MN];
-        Core::template run_prefix<K, BSIDMAP_L1_PAIRS>(lane, s_C[k], p, fo);
+        Core::template run_prefix<K, BSIDMAP_L1_GROUP>(lane, s_C[k], p, fo);
 #pragma unroll
         for (int e = 0; e < MN; e++) acc[e] = ffma2(P, fo[e], acc[e]);
       }
@@ -318,13 +318,43 @@ __device__ __forceinline__ double app_weights_p2(const DecodeParams& p, const La
   return (G.active && bm > 0.0) ? p.alpha[((size_t)G.f * (p.N + 1) + i) * p.Mt + G.mi] * pow2d(E) : 0.0;
 }
 
+// The same for the two windows m'_a = m', m'_b = m' + 1 of a lane (B.mi = A.mi + 1): their
+// corridors share M_n - 1 states, so M_n + 1 loads serve both; the corridor maximum's exponent
+// comes from the high words (for doubles >= 0 the integer order of the high word is the order
+// of the value's exponent), one integer max per state instead of an FP64 compare-and-select.
+template <int MN>
+__device__ __forceinline__ void app_weights_pair(const DecodeParams& p, const LaneGeom& A, const LaneGeom& B, int i,
+                                                 float (&ba)[MN], float (&bb)[MN], double& da, double& db) {
+  double bv[MN + 1];
+  const double* brow = p.beta + ((size_t)A.f * (p.N + 1) + (i + 1)) * p.Mt;
+  const int m0 = A.mi + p.mn_lo;
+#pragma unroll
+  for (int u = 0; u < MN + 1; u++) bv[u] = __ldg(brow + min(max(m0 + u, 0), p.Mt - 1));
+  int ha = 0, hb = 0;
+#pragma unroll
+  for (int e = 0; e < MN; e++) {
+    if ((A.vmask >> e) & 1u) ha = max(ha, __double2hiint(bv[e]));
+    if ((B.vmask >> e) & 1u) hb = max(hb, __double2hiint(bv[e + 1]));
+  }
+  const int Ea = ha > 0 ? (ha >> 20) - 1023 : 0, Eb = hb > 0 ? (hb >> 20) - 1023 : 0;
+  const double sa = pow2d(-Ea), sb = pow2d(-Eb);
+#pragma unroll
+  for (int e = 0; e < MN; e++) {
+    ba[e] = ((A.vmask >> e) & 1u) ? (float)(bv[e] * sa) : 0.f;
+    bb[e] = ((B.vmask >> e) & 1u) ? (float)(bv[e + 1] * sb) : 0.f;
+  }
+  const double* arow = p.alpha + ((size_t)A.f * (p.N + 1) + i) * p.Mt;
+  da = (A.active && ha > 0) ? arow[A.mi] * pow2d(Ea) : 0.0;
+  db = (B.active && hb > 0) ? arow[B.mi] * pow2d(Eb) : 0.0;
+}
+
 // APP pass: 5 CTAs/SM (102 registers; the beta corridor lives in smem) with row pairs measured
 // fastest on B200 for C2 (tools/exp_app.sh: 17.06 ms vs 17.3-18.0 ms for 3-4 CTAs/SM)
 #ifndef BSIDMAP_APP_MINB
 #define BSIDMAP_APP_MINB (Core::kMinBlocks > 2 ? 5 : 2)
 #endif
-#ifndef BSIDMAP_APP_PAIRS
-#define BSIDMAP_APP_PAIRS (Core::kMinBlocks > 2)
+#ifndef BSIDMAP_APP_GROUP
+#define BSIDMAP_APP_GROUP (Core::kMinBlocks > 2 ? 2 : 1)
 #endif
 #ifndef BSIDMAP_APP_BT_SMEM
 #define BSIDMAP_APP_BT_SMEM 1
@@ -384,7 +414,8 @@ __global__ void __launch_bounds__(kLatticeThreads, KP > 0 ? BSIDMAP_APP_MINB_PRE
   f32x2 bt[MN];
   {
     float ba[MN], bb[MN];
-    const double da = app_weights_p2<MN>(p, A, i, ba), db = app_weights_p2<MN>(p, B, i, bb);
+    double da, db;
+    app_weights_pair<MN>(p, A, B, i, ba, bb, da, db);
 #pragma unroll
     for (int e = 0; e < MN; e++) bt[e] = pk(ba[e], bb[e]);
     // common power-of-two scale of the tile's weights (max exponent over the warp)
@@ -411,12 +442,12 @@ __global__ void __launch_bounds__(kLatticeThreads, KP > 0 ? BSIDMAP_APP_MINB_PRE
       f32x2 fo[MN];
       if constexpr (KP > 0) {
         if (k == 0 || ((x ^ s_C[k - 1]) & ((1u << KP) - 1u)) != 0u)
-          Core::template run_head<KP, BSIDMAP_APP_PAIRS>(lane_t, x, p, fh);
+          Core::template run_head<KP, BSIDMAP_APP_GROUP>(lane_t, x, p, fh);
 #pragma unroll
         for (int e = 0; e < MN; e++) fo[e] = fh[e];
-        Core::template run_tail<KP, BSIDMAP_APP_PAIRS>(lane_t, x, p, fo);
+        Core::template run_tail<KP, BSIDMAP_APP_GROUP>(lane_t, x, p, fo);
       } else {
-        Core::template run_penultimate<BSIDMAP_APP_PAIRS>(lane_t, x, p, fo);
+        Core::template run_penultimate<BSIDMAP_APP_GROUP>(lane_t, x, p, fo);
       }
       // t(m', D) = sum_k G_n(m', k, D) bt(m', k) = sum_e G_{n-1}[e] w_{x_n}[e]  (two chains)
       const f32x2* W = wt + (((x >> nb) & 1u) ? 0 : MN * 32);
@@ -618,6 +649,7 @@ CoreKernels make_core_kernels_x2_base(long nodes) {
   k.app_pre[0] = k_app_x2<Core, 2>;
   k.app_pre[1] = k_app_x2<Core, 3>;
   k.app_pre[2] = k_app_x2<Core, 4>;
+  k.app_x4 = nullptr;
   k.app_stored = k_app_stored<Core::Mn>;
   k.gamma_dump = k_gamma_dump_x2<Core>;
   k.nodes = nodes;

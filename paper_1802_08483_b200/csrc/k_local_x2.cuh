@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kLocalWarps * 32, BSIDMAP_APP_MINB) k_local_bw
       const float* pri = p.priors ? p.priors + ((size_t)f * N + i) * p.q : nullptr;
       for (int D = 0; D < p.q; D++) {
         f32x2 fo[MN];
-        Core::template run<BSIDMAP_APP_PAIRS>(lt, sC[D], p, fo);
+        Core::template run<BSIDMAP_APP_GROUP>(lt, sC[D], p, fo);
         f32x2 t0 = 0ull, t1 = 0ull;
 #pragma unroll
         for (int e = 0; e < MN; e += 2) {

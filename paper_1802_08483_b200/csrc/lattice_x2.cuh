@@ -82,61 +82,74 @@ struct SpecCoreX2 {
     }
   }
 
-  // Rows are issued in pairs: a 4-way branch on (x_R, x_{R+1}) puts rows R and R+1 in one
-  // basic block so their insertion chains interleave (row R+1 node e needs row R nodes e, e+1).
-  template <int R, bool kPairs, int RLAST = NN>
+  // Rows are issued in groups of G (1, 2 or 3): a 2^G-way branch on (x_R .. x_{R+G-1}) puts the
+  // group's rows in one basic block so their insertion chains interleave (row R+1 node e needs
+  // row R nodes e, e+1) and the per-row dispatch cost is paid once per group.
+  template <int R, int G, int RLAST = NN>
   __device__ __forceinline__ static void rows(f32x2 (&f)[MN], uint32_t x, const Lane& L, f32x2 a2) {
-    if constexpr (kPairs && R + 1 <= RLAST) {
+    if constexpr (G >= 3 && R + 2 <= RLAST) {
+      switch ((x >> (R - 1)) & 7u) {
+        case 0u: row<R>(f, L.q0, a2); row<R + 1>(f, L.q0, a2); row<R + 2>(f, L.q0, a2); break;
+        case 1u: row<R>(f, L.q1, a2); row<R + 1>(f, L.q0, a2); row<R + 2>(f, L.q0, a2); break;
+        case 2u: row<R>(f, L.q0, a2); row<R + 1>(f, L.q1, a2); row<R + 2>(f, L.q0, a2); break;
+        case 3u: row<R>(f, L.q1, a2); row<R + 1>(f, L.q1, a2); row<R + 2>(f, L.q0, a2); break;
+        case 4u: row<R>(f, L.q0, a2); row<R + 1>(f, L.q0, a2); row<R + 2>(f, L.q1, a2); break;
+        case 5u: row<R>(f, L.q1, a2); row<R + 1>(f, L.q0, a2); row<R + 2>(f, L.q1, a2); break;
+        case 6u: row<R>(f, L.q0, a2); row<R + 1>(f, L.q1, a2); row<R + 2>(f, L.q1, a2); break;
+        default: row<R>(f, L.q1, a2); row<R + 1>(f, L.q1, a2); row<R + 2>(f, L.q1, a2); break;
+      }
+      rows<R + 3, G, RLAST>(f, x, L, a2);
+    } else if constexpr (G >= 2 && R + 1 <= RLAST) {
       switch ((x >> (R - 1)) & 3u) {
         case 0u: row<R>(f, L.q0, a2); row<R + 1>(f, L.q0, a2); break;
         case 1u: row<R>(f, L.q1, a2); row<R + 1>(f, L.q0, a2); break;
         case 2u: row<R>(f, L.q0, a2); row<R + 1>(f, L.q1, a2); break;
         default: row<R>(f, L.q1, a2); row<R + 1>(f, L.q1, a2); break;
       }
-      rows<R + 2, kPairs, RLAST>(f, x, L, a2);
+      rows<R + 2, G, RLAST>(f, x, L, a2);
     } else if constexpr (R <= RLAST) {
       if ((x >> (R - 1)) & 1u)
         row<R>(f, L.q1, a2);
       else
         row<R>(f, L.q0, a2);
-      rows<R + 1, kPairs, RLAST>(f, x, L, a2);
+      rows<R + 1, G, RLAST>(f, x, L, a2);
     }
   }
 
   // Rows 1..n-1 only: f[e] <- G_{n-1} in diagonal coordinates.  A consumer that only needs
   // t = sum_k bt(k) G_n(k) folds the last row (eqn:F_lastrow) into its weights:
   // t = sum_e G_{n-1}[e] w_{x_n}[e], w_x[e] = bt[e-1] + bt[e] (Q/Pd)(y_{n+k_e} | x)  (last_row_weights).
-  template <bool kPairs = false>
+  template <int G = 1>
   __device__ __forceinline__ static void run_penultimate(const Lane& L, uint32_t x, const DecodeParams& p,
                                                          f32x2 (&f)[MN]) {
 #pragma unroll
     for (int e = 0; e < MN; e++) f[e] = pk(p.lc.row0[e], p.lc.row0[e]);
-    rows<1, kPairs, NN - 1>(f, x, L, pk(p.lc.a, p.lc.a));
+    rows<1, G, NN - 1>(f, x, L, pk(p.lc.a, p.lc.a));
   }
 
   // Prefix sharing (pass 2): rows 1..KP depend only on the codeword's first KP bits, so symbols
   // visited in order of those bits share them -- run_head once per distinct prefix, run_tail
   // (rows KP+1..n-1) per symbol from a copy of the head's row.  Same operations, same order:
   // bit-identical to run_penultimate.
-  template <int KP, bool kPairs = false>
+  template <int KP, int G = 1>
   __device__ __forceinline__ static void run_head(const Lane& L, uint32_t x, const DecodeParams& p, f32x2 (&f)[MN]) {
 #pragma unroll
     for (int e = 0; e < MN; e++) f[e] = pk(p.lc.row0[e], p.lc.row0[e]);
-    rows<1, kPairs, KP>(f, x, L, pk(p.lc.a, p.lc.a));
+    rows<1, G, KP>(f, x, L, pk(p.lc.a, p.lc.a));
   }
-  template <int KP, bool kPairs = false>
+  template <int KP, int G = 1>
   __device__ __forceinline__ static void run_tail(const Lane& L, uint32_t x, const DecodeParams& p, f32x2 (&f)[MN]) {
-    rows<KP + 1, kPairs, NN - 1>(f, x, L, pk(p.lc.a, p.lc.a));
+    rows<KP + 1, G, NN - 1>(f, x, L, pk(p.lc.a, p.lc.a));
   }
 
   // Rows 1..n-K (the rows that depend on codeword bits other than the last K) and, separately,
   // the last K rows for the class cls = (x_{n-K+1}..x_n) applied to any vector f: the lattice rows
   // are linear in the row they read, so sum_D P(D) G_n(D) = sum_cls Last_cls(sum_{D in cls} P(D) G_{n-K}(D)).
-  template <int K, bool kPairs = false>
+  template <int K, int G = 1>
   __device__ __forceinline__ static void run_prefix(const Lane& L, uint32_t x, const DecodeParams& p, f32x2 (&f)[MN]) {
 #pragma unroll
     for (int e = 0; e < MN; e++) f[e] = pk(p.lc.row0[e], p.lc.row0[e]);
-    rows<1, kPairs, NN - K>(f, x, L, pk(p.lc.a, p.lc.a));
+    rows<1, G, NN - K>(f, x, L, pk(p.lc.a, p.lc.a));
   }
   template <int K>
   __device__ __forceinline__ static void apply_last_rows(const Lane& L, uint32_t cls, const DecodeParams& p,
@@ -164,12 +177,12 @@ struct SpecCoreX2 {
   }
 
   // f[e] <- (window a, window b) lattice outputs for k = m_n^- + e (times lc.out_scale)
-  // kPairs: issue rows in pairs (more ILP, more registers)
-  template <bool kPairs = false>
+  // G: rows per dispatch group (more ILP, more code)
+  template <int G = 1>
   __device__ __forceinline__ static void run(const Lane& L, uint32_t x, const DecodeParams& p, f32x2 (&f)[MN]) {
 #pragma unroll
     for (int e = 0; e < MN; e++) f[e] = pk(p.lc.row0[e], p.lc.row0[e]);
-    rows<1, kPairs>(f, x, L, pk(p.lc.a, p.lc.a));
+    rows<1, G>(f, x, L, pk(p.lc.a, p.lc.a));
   }
 
   static constexpr long nodes() { return (long)NN * MN - (long)LO * (LO - 1) / 2; }
