@@ -235,9 +235,10 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
     P->app_kernel = d->kern.app_pre[P->app_kp - 2];
   else
     P->app_kp = 0;
-  // four windows per lane where the shape has an X4 instance (measured faster)
+  // four windows per lane (k_app_x4) only on request: measured slower on B200 (C2 pass 2 41.9 vs
+  // 61.5 TF/s: 3 CTAs/SM with spills against 5) -- tools/exp_x4.sh
   P->app_w4 = 0;
-  if (mode == kSchedGammaSum && d->kern.app_x4 && d->app_x4 != 0) {
+  if (mode == kSchedGammaSum && d->kern.app_x4 && d->app_x4 > 0) {
     P->app_kernel = d->kern.app_x4;
     P->app_kp = 0;
     P->app_w4 = 1;
