@@ -359,6 +359,10 @@ void launch_pass1(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_
   const long lanes = (long)p.F * d->Mt;
   const unsigned gx_flat = (unsigned)((lanes + kLatticeThreads - 1) / kLatticeThreads);
   auto l1 = P.mode == kSchedStored ? d->kern.gamma_store : P.l1_kernel;
+  if (P.mode != kSchedStored && p.priors) {  // the non-uniform-prior instance of the pass-1 kernel
+    if (l1 == d->kern.gamma_sum && d->kern.gamma_sum_pri) l1 = d->kern.gamma_sum_pri;
+    if (l1 == d->kern.gamma_sum_k3 && d->kern.gamma_sum_k3_pri) l1 = d->kern.gamma_sum_k3_pri;
+  }
   for_i_slices(d->N, [&](int i0, int ni) {
     p.i_base = i0;
     l1<<<dim3(d->kern.l1_W == 2 ? (unsigned)((lanes + 2 * kLatticeThreads - 1) / (2 * kLatticeThreads)) : gx_flat, ni),

@@ -11,8 +11,10 @@
     *out = make_core_kernels_x2<SpecCoreX2<NN, LO, MN>>(SpecCoreX2<NN, LO, MN>::nodes()); \
     out->app_x4 = app_x4_kernel<NN, LO, MN>();                                            \
     if (SpecCoreX2<NN, LO, MN>::kMinBlocks <= 2 && MN <= 20) { /* measured: scalar pass 1 wins (C3, C5) */ \
-      out->gamma_sum = k_gamma_sum_cls<SpecCore<NN, LO, MN>, 2>;                        \
-      out->gamma_sum_k3 = k_gamma_sum_cls<SpecCore<NN, LO, MN>, 3>;                     \
+      out->gamma_sum = k_gamma_sum_cls<SpecCore<NN, LO, MN>, 2, false>;                 \
+      out->gamma_sum_k3 = k_gamma_sum_cls<SpecCore<NN, LO, MN>, 3, false>;              \
+      out->gamma_sum_pri = k_gamma_sum_cls<SpecCore<NN, LO, MN>, 2, true>;              \
+      out->gamma_sum_k3_pri = k_gamma_sum_cls<SpecCore<NN, LO, MN>, 3, true>;           \
       out->gamma_store = k_gamma_sum<SpecCore<NN, LO, MN>, true>;                       \
       out->l1_W = 1;                                                                    \
       out->app = k_app_x1<SpecCore<NN, LO, MN>, 0>;                                     \

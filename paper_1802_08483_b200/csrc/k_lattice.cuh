@@ -298,6 +298,8 @@ __global__ void __launch_bounds__(kLatticeThreads) k_gamma_dump(const DecodePara
 struct CoreKernels {
   void (*gamma_sum)(const DecodeParams);
   void (*gamma_sum_k3)(const DecodeParams);  // pass 1 with 3 hoisted rows (large q); nullptr = none
+  void (*gamma_sum_pri)(const DecodeParams);     // the same two with non-uniform priors (nullptr: the
+  void (*gamma_sum_k3_pri)(const DecodeParams);  // plain kernels read priors themselves)
   void (*gamma_store)(const DecodeParams);
   void (*app)(const DecodeParams);
   void (*app_pre[3])(const DecodeParams);  // APP with prefix sharing, KP = 2, 3, 4 first codeword bits (spec only)
@@ -318,6 +320,7 @@ CoreKernels make_core_kernels(long nodes) {
   CoreKernels k;
   k.gamma_sum = k_gamma_sum<Core, false>;
   k.gamma_sum_k3 = nullptr;
+  k.gamma_sum_pri = k.gamma_sum_k3_pri = nullptr;
   k.gamma_store = k_gamma_sum<Core, true>;
   k.app = k_app<Core>;
   k.app_pre[0] = k.app_pre[1] = k.app_pre[2] = nullptr;

@@ -179,7 +179,7 @@ __device__ __forceinline__ void class_order(const DecodeParams& p, int i, uint32
   }
 }
 
-template <class Core, int K>
+template <class Core, int K, bool kPri = true>
 __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_x2_cls(const DecodeParams p) {
   constexpr int MN = Core::Mn;
   constexpr int NC = 1 << K;
@@ -213,12 +213,17 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_
 #pragma unroll
       for (int e = 0; e < MN; e++) acc[e] = 0ull;
       for (; k < kend; k++) {
-        const int D = s_D[k];
-        const f32x2 P = pa ? pk(__ldg(pa + D), __ldg(pb + D)) : pk(1.f, 1.f);
         f32x2 fo[MN];
         Core::template run_prefix<K, BSIDMAP_L1_GROUP>(lane, s_C[k], p, fo);
+        if constexpr (kPri) {  // P(D_i = D) of the two windows' frames
+          const int D = s_D[k];
+          const f32x2 P = pk(__ldg(pa + D), __ldg(pb + D));
 #pragma unroll
-        for (int e = 0; e < MN; e++) acc[e] = ffma2(P, fo[e], acc[e]);
+          for (int e = 0; e < MN; e++) acc[e] = ffma2(P, fo[e], acc[e]);
+        } else {  // uniform priors: the common factor 1/q is applied at the store
+#pragma unroll
+          for (int e = 0; e < MN; e++) acc[e] = fadd2(fo[e], acc[e]);
+        }
       }
       Core::template apply_last_rows<K>(lane, (uint32_t)c, p, acc);
 #pragma unroll
@@ -243,7 +248,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_
 }
 
 // Scalar-core version (one window per lane, flat geometry) for the register-heavy shapes.
-template <class Core, int K>
+template <class Core, int K, bool kPri = true>
 __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_sum_cls(const DecodeParams p) {
   constexpr int MN = Core::Mn;
   constexpr int NC = 1 << K;
@@ -274,11 +279,16 @@ __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_su
 #pragma unroll
       for (int e = 0; e < MN; e++) acc[e] = 0.f;
       for (; k < kend; k++) {
-        const float P = pri ? __ldg(pri + s_D[k]) : 1.f;
         float fo[MN];
         Core::template run_prefix<K>(lane, s_C[k], p, fo);
+        if constexpr (kPri) {
+          const float P = __ldg(pri + s_D[k]);
 #pragma unroll
-        for (int e = 0; e < MN; e++) acc[e] = fmaf(P, fo[e], acc[e]);
+          for (int e = 0; e < MN; e++) acc[e] = fmaf(P, fo[e], acc[e]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < MN; e++) acc[e] += fo[e];
+        }
       }
       Core::template apply_last_rows<K>(lane, (uint32_t)c, p, acc);
 #pragma unroll
@@ -642,8 +652,10 @@ CoreKernels make_core_kernels_x2(long nodes);  // defined in k_local_x2.cuh (nee
 template <class Core>
 CoreKernels make_core_kernels_x2_base(long nodes) {
   CoreKernels k;
-  k.gamma_sum = k_gamma_sum_x2_cls<Core, 2>;
-  k.gamma_sum_k3 = k_gamma_sum_x2_cls<Core, 3>;
+  k.gamma_sum = k_gamma_sum_x2_cls<Core, 2, false>;
+  k.gamma_sum_k3 = k_gamma_sum_x2_cls<Core, 3, false>;
+  k.gamma_sum_pri = k_gamma_sum_x2_cls<Core, 2, true>;
+  k.gamma_sum_k3_pri = k_gamma_sum_x2_cls<Core, 3, true>;
   k.gamma_store = k_gamma_sum_x2<Core, true>;
   k.app = k_app_x2<Core, 0>;
   k.app_pre[0] = k_app_x2<Core, 2>;
