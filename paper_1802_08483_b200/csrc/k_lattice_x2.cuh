@@ -20,6 +20,20 @@
 namespace bsidmap {
 
 constexpr int kTileSlots = 64;
+
+// Symbol-loop codeword prefetch: x of iteration k + 1 is read from shared memory during
+// iteration k, so the warp-uniform row branches of the next lattice do not wait on it.
+struct XPrefetch {
+  const uint32_t* s;
+  int last;
+  uint32_t nxt;
+  __device__ __forceinline__ XPrefetch(const uint32_t* s_C, int k0, int q) : s(s_C), last(q - 1), nxt(s_C[k0]) {}
+  __device__ __forceinline__ uint32_t take(int k) {
+    const uint32_t x = nxt;
+    nxt = s[min(k + 1, last)];
+    return x;
+  }
+};
 constexpr int kX2Warps = kLatticeThreads / 32;
 
 __host__ __device__ __forceinline__ int tiles_per_frame(int Mt) { return (Mt + kTileSlots - 1) / kTileSlots; }
@@ -206,6 +220,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_
     f32x2* res = s_res + threadIdx.x;  // res[e * 128]
     bool first = true;
     int k = 0;
+    XPrefetch xs(s_C, 0, p.q);
 #pragma unroll 1
     for (int c = 0; c < NC; c++) {
       const int kend = s_start[c + 1];
@@ -214,7 +229,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_
       for (int e = 0; e < MN; e++) acc[e] = 0ull;
       for (; k < kend; k++) {
         f32x2 fo[MN];
-        Core::template run_prefix<K, BSIDMAP_L1_GROUP>(lane, s_C[k], p, fo);
+        Core::template run_prefix<K, BSIDMAP_L1_GROUP>(lane, xs.take(k), p, fo);
         if constexpr (kPri) {  // P(D_i = D) of the two windows' frames
           const int D = s_D[k];
           const f32x2 P = pk(__ldg(pa + D), __ldg(pb + D));
@@ -272,6 +287,7 @@ __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_su
     float* res = s_res + threadIdx.x;
     bool first = true;
     int k = 0;
+    XPrefetch xs(s_C, 0, p.q);
 #pragma unroll 1
     for (int c = 0; c < NC; c++) {
       const int kend = s_start[c + 1];
@@ -280,7 +296,7 @@ __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_su
       for (int e = 0; e < MN; e++) acc[e] = 0.f;
       for (; k < kend; k++) {
         float fo[MN];
-        Core::template run_prefix<K>(lane, s_C[k], p, fo);
+        Core::template run_prefix<K>(lane, xs.take(k), p, fo);
         if constexpr (kPri) {
           const float P = __ldg(pri + s_D[k]);
 #pragma unroll
@@ -447,12 +463,15 @@ __global__ void __launch_bounds__(kLatticeThreads, KP > 0 ? BSIDMAP_APP_MINB_PRE
     const float* pri = p.priors ? p.priors + ((size_t)f * p.N + i) * p.q : nullptr;
     const int nb = p.n - 1;
     f32x2 fh[MN];  // rows 1..KP of the current prefix
+    XPrefetch xs(s_C, 0, p.q);
+    uint32_t xprev = 0u;
     for (int k = 0; k < p.q; k++) {
-      const uint32_t x = s_C[k];
+      const uint32_t x = xs.take(k);
       f32x2 fo[MN];
       if constexpr (KP > 0) {
-        if (k == 0 || ((x ^ s_C[k - 1]) & ((1u << KP) - 1u)) != 0u)
+        if (k == 0 || ((x ^ xprev) & ((1u << KP) - 1u)) != 0u)
           Core::template run_head<KP, BSIDMAP_APP_GROUP>(lane_t, x, p, fh);
+        xprev = x;
 #pragma unroll
         for (int e = 0; e < MN; e++) fo[e] = fh[e];
         Core::template run_tail<KP, BSIDMAP_APP_GROUP>(lane_t, x, p, fo);
@@ -555,12 +574,15 @@ __global__ void __launch_bounds__(kLatticeThreads, KP > 0 ? BSIDMAP_APP1_MINB_PR
     const float* pri = p.priors ? p.priors + ((size_t)f * p.N + i) * p.q : nullptr;
     const int nb = p.n - 1;
     float fh[MN];  // rows 1..KP of the current prefix
+    XPrefetch xs(s_C, 0, p.q);
+    uint32_t xprev = 0u;
     for (int k = 0; k < p.q; k++) {
-      const uint32_t x = s_C[k];
+      const uint32_t x = xs.take(k);
       const int D = KP > 0 ? (int)s_D[k] : k;
       float fo[MN];
       if constexpr (KP > 0) {
-        if (k == 0 || ((x ^ s_C[k - 1]) & ((1u << KP) - 1u)) != 0u) Core::template run_head<KP>(lane_t, x, p, fh);
+        if (k == 0 || ((x ^ xprev) & ((1u << KP) - 1u)) != 0u) Core::template run_head<KP>(lane_t, x, p, fh);
+        xprev = x;
 #pragma unroll
         for (int e = 0; e < MN; e++) fo[e] = fh[e];
         Core::template run_tail<KP>(lane_t, x, p, fo);

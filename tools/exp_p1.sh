@@ -1,7 +1,7 @@
 #!/bin/bash
 # pass-1 / pass-2 variants (kernel tuning); each variant rebuilds the library
 CFGS="C2:65536 C4:512 C3:2048 C5:32 C1:16384"
-for V in "" "-DBSIDMAP_L1_GROUP=1" "-DBSIDMAP_L1_MINB=2"; do
+for V in "" "-DBSIDMAP_LATTICE_MIN_BLOCKS=3"; do
   make clean >/dev/null; make -j$(nproc) EXTRA="$V" >/dev/null 2>&1 || { echo "build failed: $V"; continue; }
   KTAG="[$V]" python tools/ktime.py $CFGS
 done
