@@ -17,6 +17,7 @@ from paper_1802_08483_b200 import Decoder  # noqa: E402
 # per-GPU batches: C1 one frame (latency), C2 65536 (1 GPU), C3/C4/C5 = 8-GPU batch / 8
 BATCH = {"C1": 1, "C2": 65536, "C3": 2048, "C4": 512, "C5": 32}
 PEAK = 148 * 128 * 2 * 1.965e9 / 1e12
+PEAKS = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
 
 
 def run(name, mode, steps):
@@ -49,11 +50,20 @@ def run(name, mode, steps):
     p2 = flops / (phm[3] / 1e3) / 1e12
     plan = d.plan(F)
     ser = float((np.argmax(L.cpu().numpy(), 2) != b.msg).mean())
+    extra = {}
+    if plan["mode"] == "stored":
+        # stored variant: HBM-bound on the gamma round trip; phases 1-3 are the first chunk
+        hbm = json.load(open(PEAKS)).get("hbm_gbs") if os.path.exists(PEAKS) else None
+        gb = plan["chunk"] * cfg.N * cfg.q * cfg.Mn * cfg.Mt * 4 / 1e9
+        extra = {"chunk_frames": plan["chunk"], "gamma_gb_per_chunk": gb,
+                 "pass1_gamma_write_gbs": gb / (phm[1] / 1e3), "app_gamma_read_gbs": gb / (phm[3] / 1e3),
+                 "app_hbm_frac": (gb / (phm[3] / 1e3)) / hbm if hbm else None, "hbm_peak_gbs": hbm,
+                 "note": "phases 1-3 time the first chunk; phase 4 runs to the end of the last chunk"}
     return {"config": name, "frames": F, "mode": plan["mode"], "core": plan["core"], "ms_per_batch": ms,
             "frames_per_s": F / ms * 1e3, "symbols_per_s": F * cfg.N / ms * 1e3,
             "phase_ms": [float(x) for x in phm], "pass1_tflops": p1, "pass2_tflops": p2,
             "pass1_frac": p1 / PEAK, "pass2_frac": p2 / PEAK, "frames_ok": float((st.cpu().numpy() == 0).mean()),
-            "symbol_error_rate": ser}
+            "symbol_error_rate": ser, **extra}
 
 
 def run_next(steps):
