@@ -18,11 +18,10 @@
 #include "../../include/bsidmap.h"
 #include "k_local_x2.cuh"
 #include "k_lattice_x4.cuh"
+#include "k_alphabeta_cta.cuh"
 
 namespace bsidmap {
 __global__ void k_frame_init(const DecodeParams p);
-__global__ void k_alpha_beta(const DecodeParams p, int stages);
-size_t ab_cta_smem(int Mn, int Mtp, int stages);
 __global__ void k_finalize(const DecodeParams p);
 __global__ void k_zero_failed(const DecodeParams p);
 __global__ void k_extrinsic(const DecodeParams p, float* E);
@@ -157,6 +156,7 @@ struct Plan {
   int ab_stages;    // k_alpha_beta TMA ring depth
   size_t ab_smem, app_smem, l1_smem;
   void (*ab_warp)(const DecodeParams);  // warp-per-task alpha/beta kernel or nullptr
+  void (*ab_cta)(const DecodeParams, int);  // CTA-per-task alpha/beta kernel (spec M_n instance or generic)
   bool direct_L;                         // APP pass writes normalised L rows itself
   size_t local_smem;                     // k_local_fwd / k_local_bwd dynamic smem
   void (*l1_kernel)(const DecodeParams);  // pass-1 kernel of the recompute schedules
@@ -208,6 +208,7 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
       return fail(d, BSIDMAP_EPLAN, "M_n x M_tau too large for the shared-memory Gamma ring of the alpha/beta kernel");
   }
   P->ab_warp = nullptr;
+  P->ab_cta = d->kern.ab_cta ? d->kern.ab_cta : k_alpha_beta_cta<0>;
   const int spt = (d->Mt + 31) / 32;
   const int spt_k = spt == 3 ? 4 : spt;
   const size_t ab_warp_bytes = (size_t)(kAbWarpThreads / 32) * ab_warp_smem(spt_k, d->Mn, (d->Mt + 3) & ~3);
@@ -376,7 +377,7 @@ void launch_alpha_beta(bsidmap_decoder* d, const Plan& P, const DecodeParams& p,
     const long tasks = 2L * p.F, per = kAbWarpThreads / 32;
     P.ab_warp<<<(unsigned)((tasks + per - 1) / per), kAbWarpThreads, P.ab_smem, s>>>(p);
   } else {
-    k_alpha_beta<<<dim3(p.F, 2), P.ab_threads, P.ab_smem, s>>>(p, P.ab_stages);
+    P.ab_cta<<<dim3(p.F, 2), P.ab_threads, P.ab_smem, s>>>(p, P.ab_stages);
   }
   d->launches++;
 }
@@ -573,7 +574,7 @@ int bsidmap_decode_batch_opts(bsidmap_decoder* d, int F, const uint32_t* rx, con
   if ((rc = make_plan(d, F, &P))) return rc;
   const Layout l = layout(d, P.chunk, P.mode);
   if ((rc = ensure_ws(d, l.total))) return rc;
-  if ((rc = set_smem(d, P.ab_warp ? (const void*)P.ab_warp : (const void*)k_alpha_beta, P.ab_smem))) return rc;
+  if ((rc = set_smem(d, P.ab_warp ? (const void*)P.ab_warp : (const void*)P.ab_cta, P.ab_smem))) return rc;
   if ((rc = set_smem(d, (const void*)P.l1_kernel, P.l1_smem))) return rc;
   if (P.mode == kSchedLocal) {
     if ((rc = set_smem(d, (const void*)d->kern.local_fwd, P.local_smem))) return rc;

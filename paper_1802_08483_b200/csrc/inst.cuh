@@ -3,6 +3,7 @@
 #pragma once
 #include "k_local_x2.cuh"
 #include "k_lattice_x4.cuh"
+#include "k_alphabeta_cta.cuh"
 
 #define BSIDMAP_SPEC_UNIT(IDX, NN, LO, MN)                                               \
   namespace bsidmap {                                                                    \
@@ -10,6 +11,7 @@
     if (n != NN || lo != LO || Mn != MN) return false;                                   \
     *out = make_core_kernels_x2<SpecCoreX2<NN, LO, MN>>(SpecCoreX2<NN, LO, MN>::nodes()); \
     out->app_x4 = app_x4_kernel<NN, LO, MN>();                                            \
+    out->ab_cta = k_alpha_beta_cta<MN>;                                                   \
     if (SpecCoreX2<NN, LO, MN>::kMinBlocks <= 2 && MN <= 20) { /* measured: scalar pass 1 wins (C3, C5) */ \
       out->gamma_sum = k_gamma_sum_cls<SpecCore<NN, LO, MN>, 2, false>;                 \
       out->gamma_sum_k3 = k_gamma_sum_cls<SpecCore<NN, LO, MN>, 3, false>;              \

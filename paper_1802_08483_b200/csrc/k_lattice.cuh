@@ -311,13 +311,14 @@ struct CoreKernels {
   int l1_W;    // windows per lane of the pass-1 kernel (the scalar core may serve pass 1 of a pair core)
   int app_W;   // windows per lane of the tiled APP kernel (32 * app_W states per warp tile)
   void (*ab_warp[3])(const DecodeParams);  // warp-per-task alpha/beta for M_tau <= 32, 64, 128 (spec only)
+  void (*ab_cta)(const DecodeParams, int);  // CTA-per-task alpha/beta with compile-time M_n (spec only)
   void (*local_fwd)(const DecodeParams);   // fused local schedule, M_tau <= 64 (spec only)
   void (*local_bwd)(const DecodeParams);
 };
 
 template <class Core>
 CoreKernels make_core_kernels(long nodes) {
-  CoreKernels k;
+  CoreKernels k{};
   k.gamma_sum = k_gamma_sum<Core, false>;
   k.gamma_sum_k3 = nullptr;
   k.gamma_sum_pri = k.gamma_sum_k3_pri = nullptr;
@@ -333,6 +334,7 @@ CoreKernels make_core_kernels(long nodes) {
   k.app_W = 1;
   k.ab_warp[0] = k.ab_warp[1] = k.ab_warp[2] = nullptr;
   k.local_fwd = k.local_bwd = nullptr;
+  k.ab_cta = nullptr;
   return k;
 }
 

@@ -673,7 +673,7 @@ CoreKernels make_core_kernels_x2(long nodes);  // defined in k_local_x2.cuh (nee
 
 template <class Core>
 CoreKernels make_core_kernels_x2_base(long nodes) {
-  CoreKernels k;
+  CoreKernels k{};
   k.gamma_sum = k_gamma_sum_x2_cls<Core, 2, false>;
   k.gamma_sum_k3 = k_gamma_sum_x2_cls<Core, 3, false>;
   k.gamma_sum_pri = k_gamma_sum_x2_cls<Core, 2, true>;
