@@ -63,6 +63,8 @@ struct bsidmap_decoder {
   double Pi = 0, Pd = 0, Ps = 0;
   int mode = BSIDMAP_MODE_AUTO;
   uint32_t* d_C = nullptr;
+  void* d_orders = nullptr;  // symbol visiting orders (DecodeParams::Cp/Dp/Cs/Ds/Cst), one allocation
+  size_t ord_off[8] = {};    // byte offsets: Cp, Dp, Cs2, Ds2, Cst2, Cs3, Ds3, Cst3
   CoreKernels kern{};
   bool spec = false;
   LatticeConst lc{};
@@ -295,6 +297,14 @@ void fill_params(const bsidmap_decoder* d, DecodeParams* p) {
   p->mt_lo = d->mt_lo; p->mt_hi = d->mt_hi; p->Mt = d->Mt;
   p->Mtp = (d->Mt + 3) & ~3;
   p->C = d->d_C;
+  const char* ob = static_cast<const char*>(d->d_orders);
+  p->Cp = reinterpret_cast<const uint32_t*>(ob + d->ord_off[0]);
+  p->Dp = reinterpret_cast<const uint16_t*>(ob + d->ord_off[1]);
+  for (int k = 0; k < 2; k++) {
+    p->Cs[k] = reinterpret_cast<const uint32_t*>(ob + d->ord_off[2 + 3 * k]);
+    p->Ds[k] = reinterpret_cast<const uint16_t*>(ob + d->ord_off[3 + 3 * k]);
+    p->Cst[k] = reinterpret_cast<const int*>(ob + d->ord_off[4 + 3 * k]);
+  }
   p->lc = d->lc;
 }
 
@@ -467,6 +477,59 @@ int run_chunk(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s,
   return BSIDMAP_OK;
 }
 
+// Symbol visiting orders of every C_i, computed once per decoder (they depend on the codebook only):
+//  - lexicographic in (x_1, x_2, ..., x_n) -- the APP pass shares lattice rows 1..KP between
+//    consecutive symbols with equal first KP bits (every prefix length is contiguous in this order);
+//  - grouped by the class of the last K bits (K = 2, 3), stable -- pass 1 runs the last K rows once
+//    per class.
+cudaError_t upload_orders(bsidmap_decoder* d, const uint32_t* C) {
+  const int N = d->N, q = d->q, n = d->n;
+  const size_t nq = (size_t)N * q;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  size_t off = 0;
+  d->ord_off[0] = off; off = al(off + nq * 4);
+  d->ord_off[1] = off; off = al(off + nq * 2);
+  for (int k = 0; k < 2; k++) {
+    const int NC = 1 << (k + 2);
+    d->ord_off[2 + 3 * k] = off; off = al(off + nq * 4);
+    d->ord_off[3 + 3 * k] = off; off = al(off + nq * 2);
+    d->ord_off[4 + 3 * k] = off; off = al(off + (size_t)N * (NC + 1) * 4);
+  }
+  std::vector<char> h(off, 0);
+  auto rev = [n](uint32_t w) {  // bit t -> bit n-1-t: x_1 becomes the most significant
+    uint32_t r = 0;
+    for (int t = 0; t < n; t++) r |= ((w >> t) & 1u) << (n - 1 - t);
+    return r;
+  };
+  std::vector<int> idx(q);
+  for (int i = 0; i < N; i++) {
+    const uint32_t* Ci = C + (size_t)i * q;
+    for (int D = 0; D < q; D++) idx[D] = D;
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return rev(Ci[a]) < rev(Ci[b]); });
+    for (int k = 0; k < q; k++) {
+      reinterpret_cast<uint32_t*>(h.data() + d->ord_off[0])[(size_t)i * q + k] = Ci[idx[k]];
+      reinterpret_cast<uint16_t*>(h.data() + d->ord_off[1])[(size_t)i * q + k] = (uint16_t)idx[k];
+    }
+    for (int kk = 0; kk < 2; kk++) {
+      const int K = kk + 2, NC = 1 << K, sh = n - K;
+      auto cls = [&](int D) { return sh >= 0 ? (int)((Ci[D] >> sh) & (uint32_t)(NC - 1)) : 0; };
+      for (int D = 0; D < q; D++) idx[D] = D;
+      std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return cls(a) < cls(b); });
+      int* st = reinterpret_cast<int*>(h.data() + d->ord_off[4 + 3 * kk]) + (size_t)i * (NC + 1);
+      for (int c = 0; c <= NC; c++) st[c] = q;
+      for (int k = q - 1; k >= 0; k--) {
+        reinterpret_cast<uint32_t*>(h.data() + d->ord_off[2 + 3 * kk])[(size_t)i * q + k] = Ci[idx[k]];
+        reinterpret_cast<uint16_t*>(h.data() + d->ord_off[3 + 3 * kk])[(size_t)i * q + k] = (uint16_t)idx[k];
+        st[cls(idx[k])] = k;
+      }
+      for (int c = NC - 1; c >= 0; c--) st[c] = std::min(st[c], st[c + 1]);  // empty classes
+    }
+  }
+  cudaError_t e = cudaMalloc(&d->d_orders, off);
+  if (e == cudaSuccess) e = cudaMemcpy(d->d_orders, h.data(), off, cudaMemcpyHostToDevice);
+  return e;
+}
+
 int check_inputs(bsidmap_decoder* d, int F, const void* rx, const void* off, const void* rho, const void* L,
                  const void* st) {
   if (!d) return fail(nullptr, BSIDMAP_EINVAL, "decoder is NULL");
@@ -544,6 +607,7 @@ int bsidmap_create(bsidmap_decoder** out, int q, int n, int N, const uint32_t* c
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&d->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e == cudaSuccess) e = cudaMalloc(&d->d_C, sizeof(uint32_t) * (size_t)N * q);
   if (e == cudaSuccess) e = cudaMemcpy(d->d_C, codebook_host, sizeof(uint32_t) * (size_t)N * q, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = upload_orders(d, codebook_host);
   for (int k = 0; e == cudaSuccess && k <= kPhases; k++) e = cudaEventCreate(&d->ev[k]);
   if (e != cudaSuccess) {
     std::string m = std::string("device setup: ") + cudaGetErrorString(e);
@@ -694,6 +758,7 @@ void bsidmap_destroy(bsidmap_decoder* d) {
   for (int k = 0; k < kHostSub; k++)
     if (d->ev_sub[k]) cudaEventDestroy(d->ev_sub[k]);
   if (d->d_C) cudaFree(d->d_C);
+  if (d->d_orders) cudaFree(d->d_orders);
   for (int k = 0; k <= kPhases; k++)
     if (d->ev[k]) cudaEventDestroy(d->ev[k]);
   delete d;

@@ -42,6 +42,12 @@ struct DecodeParams {
   int Mtp;                    // row stride of Gsum: M_tau rounded up to a multiple of 4 (16-byte rows for TMA)
   int F;                      // frames in this chunk
   const uint32_t* C;          // [N][q] codebook, decoder-owned (bit t = t-th transmitted bit)
+  // Symbol visiting orders of C_i, prepared once at create (decoder-owned, [N][q]):
+  const uint32_t* Cp;         // codewords in lexicographic order of (x_1, x_2, ..): every prefix group contiguous
+  const uint16_t* Dp;         //   their symbols D
+  const uint32_t* Cs[2];      // codewords grouped by the class of their last K = 2, 3 bits (stable)
+  const uint16_t* Ds[2];      //   their symbols D
+  const int* Cst[2];          //   [N][2^K + 1] first position of each class (last entry q)
   const uint32_t* rx;         // packed received words, caller-owned
   const int64_t* rx_off;      // [F] word offset of each frame in rx
   const int32_t* rho;         // [F] received length

@@ -146,65 +146,15 @@ __host__ __device__ __forceinline__ size_t cls_smem(int q, int Mn, int lanes_pai
   return (size_t)q * 4 + (size_t)((q * 2 + 15) / 16) * 16 + 64 + (size_t)Mn * lanes_pairs * 8;
 }
 
-// Warp 0 of the CTA sorts C_i(0..q-1) by class (stable): s_C[k] = codeword, s_D[k] = its symbol,
-// s_start[c] = first position of class c (s_start[NC] = q).  Call before a __syncthreads.
-// sh = bit offset of the K class bits (default p.n - K: the last K codeword bits; 0: the first K).
-template <int K>
-__device__ __forceinline__ void class_order(const DecodeParams& p, int i, uint32_t* s_C, uint16_t* s_D, int* s_start,
-                                            int sh = -1) {
-  constexpr int NC = 1 << K;
-  const int lane = threadIdx.x & 31;
-  if ((threadIdx.x >> 5) != 0) return;
-  const uint32_t* Ci = p.C + (size_t)i * p.q;
-  if (sh < 0) sh = p.n - K;
-  int cnt[NC];
-#pragma unroll
-  for (int c = 0; c < NC; c++) cnt[c] = 0;
-  for (int b = 0; b < p.q; b += 32) {
-    const int D = b + lane;
-    const int cl = D < p.q ? (int)((Ci[D] >> sh) & (NC - 1)) : -1;
-#pragma unroll
-    for (int c = 0; c < NC; c++) cnt[c] += __popc(__ballot_sync(0xffffffffu, cl == c));
-  }
-  int off[NC];
-  int run = 0;
-#pragma unroll
-  for (int c = 0; c < NC; c++) {
-    off[c] = run;
-    if (lane == 0 && s_start) s_start[c] = run;
-    run += cnt[c];
-  }
-  if (lane == 0 && s_start) s_start[NC] = p.q;
-  const uint32_t lt = (1u << lane) - 1u;
-  for (int b = 0; b < p.q; b += 32) {
-    const int D = b + lane;
-    const uint32_t w = D < p.q ? Ci[D] : 0u;
-    const int cl = D < p.q ? (int)((w >> sh) & (NC - 1)) : -1;
-#pragma unroll
-    for (int c = 0; c < NC; c++) {
-      const uint32_t m = __ballot_sync(0xffffffffu, cl == c);
-      if (cl == c) {
-        const int pos = off[c] + __popc(m & lt);
-        s_C[pos] = w;
-        s_D[pos] = (uint16_t)D;
-      }
-      off[c] += __popc(m);
-    }
-  }
-}
-
 template <class Core, int K, bool kPri = true>
 __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_x2_cls(const DecodeParams p) {
   constexpr int MN = Core::Mn;
   constexpr int NC = 1 << K;
   extern __shared__ __align__(128) unsigned char smem[];
-  f32x2* s_res = reinterpret_cast<f32x2*>(smem);                      // [MN][128] per-lane result
-  uint32_t* s_C = reinterpret_cast<uint32_t*>(s_res + MN * kLatticeThreads);
-  int* s_start = reinterpret_cast<int*>(s_C + p.q);
-  uint16_t* s_D = reinterpret_cast<uint16_t*>(s_start + 16);
+  f32x2* s_res = reinterpret_cast<f32x2*>(smem);  // [MN][128] per-lane result (private column, no barrier)
   const int i = blockIdx.y + p.i_base;
-  class_order<K>(p, i, s_C, s_D, s_start);
-  __syncthreads();
+  const uint32_t* Ci = p.Cs[K - 2] + (size_t)i * p.q;  // C_i grouped by the class of its last K bits
+  const uint16_t* Di = p.Ds[K - 2] + (size_t)i * p.q;
 
   const long ga = (long)blockIdx.x * (2 * blockDim.x) + threadIdx.x;
   const LaneGeom A = lane_geom_at(p, i, ga), B = lane_geom_at(p, i, ga + blockDim.x);
@@ -217,36 +167,42 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_
                B.active ? load_window(p, B.f, B.s, B.rho) : 0ull, p);
     const float* pa = p.priors ? p.priors + ((size_t)A.f * p.N + i) * p.q : nullptr;
     const float* pb = p.priors ? p.priors + ((size_t)B.f * p.N + i) * p.q : nullptr;
-    f32x2* res = s_res + threadIdx.x;  // res[e * 128]
+    f32x2* res = s_res + threadIdx.x;  // res[e * 128]: the sum over the finished classes
     bool first = true;
-    int k = 0;
-    XPrefetch xs(s_C, 0, p.q);
-#pragma unroll 1
-    for (int c = 0; c < NC; c++) {
-      const int kend = s_start[c + 1];
-      if (k == kend) continue;
+    const int sh = p.n - K;
+    XPrefetch xs(Ci, 0, p.q);
+    uint32_t cur = (Ci[0] >> sh) & (NC - 1);
+    // one pass over C_i in class order; the class boundary is seen in the (warp-uniform) codeword
+    for (int k = 0; k < p.q; k++) {
+      const uint32_t x = xs.take(k);
+      const uint32_t c = (x >> sh) & (NC - 1);
+      if (c != cur) {  // close class `cur`: its last K rows once, added to the finished classes
+        Core::template apply_last_rows<K>(lane, cur, p, acc);
 #pragma unroll
-      for (int e = 0; e < MN; e++) acc[e] = 0ull;
-      for (; k < kend; k++) {
-        f32x2 fo[MN];
-        Core::template run_prefix<K, BSIDMAP_L1_GROUP>(lane, xs.take(k), p, fo);
-        if constexpr (kPri) {  // P(D_i = D) of the two windows' frames
-          const int D = s_D[k];
-          const f32x2 P = pk(__ldg(pa + D), __ldg(pb + D));
-#pragma unroll
-          for (int e = 0; e < MN; e++) acc[e] = ffma2(P, fo[e], acc[e]);
-        } else {  // uniform priors: the common factor 1/q is applied at the store
-#pragma unroll
-          for (int e = 0; e < MN; e++) acc[e] = fadd2(fo[e], acc[e]);
+        for (int e = 0; e < MN; e++) {
+          if (!first) acc[e] = fadd2(acc[e], res[e * kLatticeThreads]);
+          res[e * kLatticeThreads] = acc[e];
+          acc[e] = 0ull;
         }
+        first = false;
+        cur = c;
       }
-      Core::template apply_last_rows<K>(lane, (uint32_t)c, p, acc);
+      f32x2 fo[MN];
+      Core::template run_prefix<K, BSIDMAP_L1_GROUP>(lane, x, p, fo);
+      if constexpr (kPri) {  // P(D_i = D) of the two windows' frames
+        const int D = Di[k];
+        const f32x2 P = pk(__ldg(pa + D), __ldg(pb + D));
 #pragma unroll
-      for (int e = 0; e < MN; e++) {
-        if (!first) acc[e] = fadd2(acc[e], res[e * kLatticeThreads]);
-        res[e * kLatticeThreads] = acc[e];
+        for (int e = 0; e < MN; e++) acc[e] = ffma2(P, fo[e], acc[e]);
+      } else {  // uniform priors: the common factor 1/q is applied at the store
+#pragma unroll
+        for (int e = 0; e < MN; e++) acc[e] = fadd2(fo[e], acc[e]);
       }
-      first = false;
+    }
+    Core::template apply_last_rows<K>(lane, cur, p, acc);
+    if (!first) {
+#pragma unroll
+      for (int e = 0; e < MN; e++) acc[e] = fadd2(acc[e], res[e * kLatticeThreads]);
     }
   }
   const float sc = p.priors ? 1.f : 1.f / p.q;
@@ -268,13 +224,11 @@ __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_su
   constexpr int MN = Core::Mn;
   constexpr int NC = 1 << K;
   extern __shared__ __align__(128) unsigned char smem[];
-  float* s_res = reinterpret_cast<float*>(smem);  // [MN][128]
-  uint32_t* s_C = reinterpret_cast<uint32_t*>(smem + (size_t)MN * kLatticeThreads * 8);
-  int* s_start = reinterpret_cast<int*>(s_C + p.q);
-  uint16_t* s_D = reinterpret_cast<uint16_t*>(s_start + 16);
+  float* s_res = reinterpret_cast<float*>(smem);  // [MN][128] per-lane result (private column, no barrier)
   const int i = blockIdx.y + p.i_base;
-  class_order<K>(p, i, s_C, s_D, s_start);
-  __syncthreads();
+  const uint32_t* Ci = p.Cs[K - 2] + (size_t)i * p.q;
+  const uint16_t* Di = p.Ds[K - 2] + (size_t)i * p.q;
+  const int* cst = p.Cst[K - 2] + (size_t)i * (NC + 1);
 
   const LaneGeom G = lane_geom(p, i);
   float acc[MN];
@@ -284,13 +238,14 @@ __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_su
     typename Core::Lane lane;
     Core::init(lane, G.active ? load_window(p, G.f, G.s, G.rho) : 0ull, p);
     const float* pri = p.priors ? p.priors + ((size_t)G.f * p.N + i) * p.q : nullptr;
-    float* res = s_res + threadIdx.x;
+    float* res = s_res + threadIdx.x;  // the sum over the finished classes
     bool first = true;
     int k = 0;
-    XPrefetch xs(s_C, 0, p.q);
+    XPrefetch xs(Ci, 0, p.q);
+    // class by class (measured faster than the single loop of k_gamma_sum_x2_cls for this core)
 #pragma unroll 1
     for (int c = 0; c < NC; c++) {
-      const int kend = s_start[c + 1];
+      const int kend = cst[c + 1];
       if (k == kend) continue;
 #pragma unroll
       for (int e = 0; e < MN; e++) acc[e] = 0.f;
@@ -298,7 +253,7 @@ __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_su
         float fo[MN];
         Core::template run_prefix<K>(lane, xs.take(k), p, fo);
         if constexpr (kPri) {
-          const float P = __ldg(pri + s_D[k]);
+          const float P = __ldg(pri + Di[k]);
 #pragma unroll
           for (int e = 0; e < MN; e++) acc[e] = fmaf(P, fo[e], acc[e]);
         } else {
@@ -389,10 +344,9 @@ __device__ __forceinline__ void app_weights_pair(const DecodeParams& p, const La
 // over the lanes once after the D loop instead of one shuffle chain per D
 __host__ __device__ __forceinline__ size_t app_stage_floats(int q) { return (size_t)q * 33; }
 __host__ __device__ __forceinline__ size_t app_x2_smem(int q, int Mn) {
-  return (size_t)kX2Warps * 2 * Mn * 32 * 8 + (size_t)q * 4 + (size_t)kX2Warps * (app_stage_floats(q) + q) * 4 +
-         (size_t)((q * 2 + 15) / 16) * 16;
+  return (size_t)kX2Warps * 2 * Mn * 32 * 8 + (size_t)kX2Warps * (app_stage_floats(q) + q) * 4;
 }
-// Symbols are visited in order of their first KP codeword bits (class_order with sh = 0) so
+// Symbols are visited in lexicographic codeword order (DecodeParams::Cp, prepared at create) so
 // that lattice rows 1..KP (run_head) are computed once per distinct prefix; KP = 0: natural order.
 // The prefix length that saves the most nodes for random codebooks: ~log2(q) - 1.
 __host__ __device__ __forceinline__ int app_prefix_bits(int q, int n) {
@@ -400,7 +354,7 @@ __host__ __device__ __forceinline__ int app_prefix_bits(int q, int n) {
   return kp <= n - 2 ? kp : 0;
 }
 // smem: s_w[kX2Warps][2][M_n][32] (f32x2: the scaled beta corridor of each lane's two windows with
-//       the last lattice row folded in, one table per value of x_n; smem, not registers) | s_C[q] |
+//       the last lattice row folded in, one table per value of x_n; smem, not registers) |
 //       s_S[kX2Warps][q] (float) | staging [kX2Warps][q][33]
 // prefix sharing keeps the head row live across the symbol loop (+2 M_n registers)
 #ifndef BSIDMAP_APP_MINB_PRE
@@ -412,17 +366,13 @@ __global__ void __launch_bounds__(kLatticeThreads, KP > 0 ? BSIDMAP_APP_MINB_PRE
   constexpr int MN = Core::Mn;
   extern __shared__ __align__(128) unsigned char smem[];
   f32x2* s_bt = reinterpret_cast<f32x2*>(smem);
-  uint32_t* s_C = reinterpret_cast<uint32_t*>(s_bt + kX2Warps * 2 * MN * 32);
-  float* s_S = reinterpret_cast<float*>(s_C + p.q);
+  float* s_S = reinterpret_cast<float*>(s_bt + kX2Warps * 2 * MN * 32);
   float* s_stage = s_S + kX2Warps * p.q;
-  uint16_t* s_D = reinterpret_cast<uint16_t*>(s_stage + (size_t)kX2Warps * app_stage_floats(p.q));
   const int i = blockIdx.y + p.i_base;
-  if constexpr (KP > 0) {
-    class_order<KP>(p, i, s_C, s_D, nullptr, 0);
-  } else {
-    for (int t = threadIdx.x; t < p.q; t += blockDim.x) s_C[t] = p.C[(size_t)i * p.q + t];
-  }
-  __syncthreads();
+  // KP > 0: symbols in lexicographic codeword order (prefix groups contiguous); every smem array
+  // below is per warp, so the kernel has no block barrier
+  const uint32_t* Ci = (KP > 0 ? p.Cp : p.C) + (size_t)i * p.q;
+  const uint16_t* Di = p.Dp + (size_t)i * p.q;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int T = tiles_per_frame(p.Mt);
@@ -463,7 +413,7 @@ __global__ void __launch_bounds__(kLatticeThreads, KP > 0 ? BSIDMAP_APP_MINB_PRE
     const float* pri = p.priors ? p.priors + ((size_t)f * p.N + i) * p.q : nullptr;
     const int nb = p.n - 1;
     f32x2 fh[MN];  // rows 1..KP of the current prefix
-    XPrefetch xs(s_C, 0, p.q);
+    XPrefetch xs(Ci, 0, p.q);
     uint32_t xprev = 0u;
     for (int k = 0; k < p.q; k++) {
       const uint32_t x = xs.take(k);
@@ -486,7 +436,7 @@ __global__ void __launch_bounds__(kLatticeThreads, KP > 0 ? BSIDMAP_APP_MINB_PRE
         t0 = ffma2(fo[e], W[e * 32], t0);
         if (e + 1 < MN) t1 = ffma2(fo[e + 1], W[(e + 1) * 32], t1);
       }
-      const int D = KP > 0 ? (int)s_D[k] : k;
+      const int D = KP > 0 ? (int)Di[k] : k;
       stg[D * 33 + lane] = fmaf(wa, lo_of(t0) + lo_of(t1), wb * (hi_of(t0) + hi_of(t1)));
     }
     __syncwarp();
@@ -524,7 +474,7 @@ __global__ void __launch_bounds__(kLatticeThreads, KP > 0 ? BSIDMAP_APP_MINB_PRE
 // pair core is register-bound (C3, C5) -- also wastes fewer slots (C3: 9 x 32 vs 5 x 64 for 267).
 __host__ __device__ __forceinline__ int tiles_per_frame_w(int Mt, int W) { return (Mt + 32 * W - 1) / (32 * W); }
 __host__ __device__ __forceinline__ size_t app_x1_smem(int q) {
-  return (size_t)q * 4 + (size_t)kX2Warps * (app_stage_floats(q) + q) * 4 + (size_t)((q * 2 + 15) / 16) * 16;
+  return (size_t)kX2Warps * (app_stage_floats(q) + q) * 4;
 }
 
 #ifndef BSIDMAP_APP1_MINB_PRE
@@ -535,17 +485,11 @@ __global__ void __launch_bounds__(kLatticeThreads, KP > 0 ? BSIDMAP_APP1_MINB_PR
     k_app_x1(const DecodeParams p) {
   constexpr int MN = Core::Mn;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint32_t* s_C = reinterpret_cast<uint32_t*>(smem);
-  float* s_S = reinterpret_cast<float*>(s_C + p.q);
+  float* s_S = reinterpret_cast<float*>(smem);
   float* s_stage = s_S + kX2Warps * p.q;
-  uint16_t* s_D = reinterpret_cast<uint16_t*>(s_stage + (size_t)kX2Warps * app_stage_floats(p.q));
   const int i = blockIdx.y + p.i_base;
-  if constexpr (KP > 0) {
-    class_order<KP>(p, i, s_C, s_D, nullptr, 0);
-  } else {
-    for (int t = threadIdx.x; t < p.q; t += blockDim.x) s_C[t] = p.C[(size_t)i * p.q + t];
-  }
-  __syncthreads();
+  const uint32_t* Ci = (KP > 0 ? p.Cp : p.C) + (size_t)i * p.q;
+  const uint16_t* Di = p.Dp + (size_t)i * p.q;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int T = tiles_per_frame_w(p.Mt, 1);
@@ -574,11 +518,11 @@ __global__ void __launch_bounds__(kLatticeThreads, KP > 0 ? BSIDMAP_APP1_MINB_PR
     const float* pri = p.priors ? p.priors + ((size_t)f * p.N + i) * p.q : nullptr;
     const int nb = p.n - 1;
     float fh[MN];  // rows 1..KP of the current prefix
-    XPrefetch xs(s_C, 0, p.q);
+    XPrefetch xs(Ci, 0, p.q);
     uint32_t xprev = 0u;
     for (int k = 0; k < p.q; k++) {
       const uint32_t x = xs.take(k);
-      const int D = KP > 0 ? (int)s_D[k] : k;
+      const int D = KP > 0 ? (int)Di[k] : k;
       float fo[MN];
       if constexpr (KP > 0) {
         if (k == 0 || ((x ^ xprev) & ((1u << KP) - 1u)) != 0u) Core::template run_head<KP>(lane_t, x, p, fh);
