@@ -341,3 +341,25 @@ def test_full_c5_frame_properties():
     _, L2, st2 = run_gpu(cfg, b2, 2)
     assert (st2 == 0).all()
     np.testing.assert_allclose(L2, L, rtol=1e-5, atol=1e-30)
+
+
+# ----------------------------------------------- bench launch configuration, full sizes
+
+@pytest.mark.parametrize("name,frames,picks", [
+    ("C2", 65536, [0, 1, 31, 4097, 16383, 16384, 32768, 40000, 50001, 65534, 65535]),
+    ("C3", 2048, [0, 1023, 2047]),
+    ("C4", 512, [0, 511]),
+])
+def test_bench_batch_sampled_parity(name, frames, picks):
+    """The bench's per-GPU batch (C2: bench.py's default launch, one decode_batch of 65536
+    frames; C3/C4: the 8-GPU configs' per-GPU batch) decoded in ONE call, and frames sampled
+    across it (first/last, tile, warp, sub-batch and chunk boundaries) checked one by one
+    against the FP64 oracle at the north-star tolerance."""
+    if os.environ.get("BSIDMAP_SKIP_LARGE"):
+        pytest.skip("large test disabled")
+    cfg = small_cfg(name)
+    b = bsidgen.make_batch(cfg, 0, frames)
+    d, L, st = run_gpu(cfg, b, 0)
+    assert (st == 0).all()
+    np.testing.assert_allclose(L.sum(2), 1.0, atol=1e-5)
+    assert_parity(L, st, run_oracle(cfg, b, picks), picks)

@@ -1,0 +1,7 @@
+#!/bin/bash
+# C3 / C5 (register-heavy shapes): scalar core vs pair core at 2 CTAs/SM
+for V in "" "-DBSIDMAP_SCALAR_MN_MAX=16"; do
+  make clean >/dev/null; make -j$(nproc) EXTRA="$V" >/dev/null 2>&1 || { echo "build failed: $V"; continue; }
+  KTAG="[$V]" python tools/ktime.py C3:2048 C5:32
+done
+make clean >/dev/null; make -j$(nproc) >/dev/null 2>&1
