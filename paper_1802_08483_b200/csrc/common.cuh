@@ -64,6 +64,7 @@ struct DecodeParams {
   double* dbg_gamma;          // debug dump [F][M_tau][M_n][q] (true scale) or nullptr
   int dbg_i;                  // symbol index of the debug dump
   int i_base;                 // first symbol index of this launch (blockIdx.y offset)
+  int i_end;                  // one past the last symbol index of this launch (multi-step kernels)
   LatticeConst lc;
 };
 
@@ -86,6 +87,42 @@ __device__ __forceinline__ uint64_t load_window(const DecodeParams& p, int f, in
   const uint32_t lo = __funnelshift_r(a, b, sh);
   const uint32_t hi = __funnelshift_r(b, c, sh);
   return (uint64_t)lo | ((uint64_t)hi << 32);
+}
+
+// Frame-constant part of a window's geometry (the lattice kernels that walk several symbol
+// indices i for the same windows load it once) and the raw received words of a window.
+struct WinBase {
+  int f, mi, mp, rho, nwords;
+  bool in, ok;
+  const uint32_t* w;
+};
+__device__ __forceinline__ WinBase win_base(const DecodeParams& p, long g) {
+  WinBase b;
+  b.in = g < (long)p.F * p.Mt;
+  b.f = b.in ? (int)(g / p.Mt) : 0;
+  b.mi = b.in ? (int)(g - (long)b.f * p.Mt) : 0;
+  b.mp = p.mt_lo + b.mi;
+  b.rho = b.in ? p.rho[b.f] : 0;
+  b.ok = b.in && p.status[b.f] == kFrameOk;
+  b.w = p.rx + (b.in ? p.rx_off[b.f] : 0);
+  b.nwords = (b.rho + 31) >> 5;
+  return b;
+}
+struct Win3 {
+  uint32_t a, b, c;
+};
+// the three words holding bits s .. s+63 (0 past the frame end; s < 0 reads from 0: inactive windows)
+__device__ __forceinline__ Win3 win_words(const WinBase& b, int s) {
+  const int w0 = max(s, 0) >> 5;
+  Win3 r;
+  r.a = (w0 < b.nwords) ? __ldg(b.w + w0) : 0u;
+  r.b = (w0 + 1 < b.nwords) ? __ldg(b.w + w0 + 1) : 0u;
+  r.c = (w0 + 2 < b.nwords) ? __ldg(b.w + w0 + 2) : 0u;
+  return r;
+}
+__device__ __forceinline__ uint64_t win_bits(const Win3& r, int s) {
+  const int sh = max(s, 0) & 31;
+  return (uint64_t)__funnelshift_r(r.a, r.b, sh) | ((uint64_t)__funnelshift_r(r.b, r.c, sh) << 32);
 }
 
 }  // namespace bsidmap

@@ -146,75 +146,103 @@ __host__ __device__ __forceinline__ size_t cls_smem(int q, int Mn, int lanes_pai
   return (size_t)q * 4 + (size_t)((q * 2 + 15) / 16) * 16 + 64 + (size_t)Mn * lanes_pairs * 8;
 }
 
+// Symbol indices per CTA of the pass-1 kernels: the windows' frame geometry is loaded once and the
+// received words of step i + 1 are prefetched while step i computes.
+#ifndef BSIDMAP_L1_STEPS
+#define BSIDMAP_L1_STEPS 8
+#endif
+constexpr int kL1Steps = BSIDMAP_L1_STEPS;
+
+__device__ __forceinline__ LaneGeom geom_step(const DecodeParams& p, const WinBase& b, int i) {
+  LaneGeom G;
+  G.in = b.in;
+  G.f = b.f;
+  G.mi = b.mi;
+  G.mp = b.mp;
+  G.s = p.n * i + b.mp;  // window start n i + m' (eqn:gamma)
+  G.rho = b.rho;
+  G.active = b.ok && G.s >= 0 && G.s <= G.rho;
+  G.vmask = valid_mask(p, G);
+  return G;
+}
+
 template <class Core, int K, bool kPri = true>
 __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_x2_cls(const DecodeParams p) {
   constexpr int MN = Core::Mn;
   constexpr int NC = 1 << K;
   extern __shared__ __align__(128) unsigned char smem[];
   f32x2* s_res = reinterpret_cast<f32x2*>(smem);  // [MN][128] per-lane result (private column, no barrier)
-  const int i = blockIdx.y + p.i_base;
-  const uint32_t* Ci = p.Cs[K - 2] + (size_t)i * p.q;  // C_i grouped by the class of its last K bits
-  const uint16_t* Di = p.Ds[K - 2] + (size_t)i * p.q;
-
   const long ga = (long)blockIdx.x * (2 * blockDim.x) + threadIdx.x;
-  const LaneGeom A = lane_geom_at(p, i, ga), B = lane_geom_at(p, i, ga + blockDim.x);
-  f32x2 acc[MN];
+  const WinBase ba = win_base(p, ga), bb = win_base(p, ga + blockDim.x);
+  const int i0 = p.i_base + blockIdx.y * kL1Steps, i1 = min(i0 + kL1Steps, p.i_end);
+  Win3 na = win_words(ba, p.n * i0 + ba.mp), nb = win_words(bb, p.n * i0 + bb.mp);
+#pragma unroll 1
+  for (int i = i0; i < i1; i++) {
+    const LaneGeom A = geom_step(p, ba, i), B = geom_step(p, bb, i);
+    const Win3 wa = na, wb = nb;
+    if (i + 1 < i1) {  // prefetch the next step's received words
+      na = win_words(ba, A.s + p.n);
+      nb = win_words(bb, B.s + p.n);
+    }
+    const uint32_t* Ci = p.Cs[K - 2] + (size_t)i * p.q;  // C_i grouped by the class of its last K bits
+    const uint16_t* Di = p.Ds[K - 2] + (size_t)i * p.q;
+    f32x2 acc[MN];
 #pragma unroll
-  for (int e = 0; e < MN; e++) acc[e] = 0ull;
-  if (__any_sync(0xffffffffu, A.active || B.active)) {
-    typename Core::Lane lane;
-    Core::init(lane, A.active ? load_window(p, A.f, A.s, A.rho) : 0ull,
-               B.active ? load_window(p, B.f, B.s, B.rho) : 0ull, p);
-    const float* pa = p.priors ? p.priors + ((size_t)A.f * p.N + i) * p.q : nullptr;
-    const float* pb = p.priors ? p.priors + ((size_t)B.f * p.N + i) * p.q : nullptr;
-    f32x2* res = s_res + threadIdx.x;  // res[e * 128]: the sum over the finished classes
-    bool first = true;
-    const int sh = p.n - K;
-    XPrefetch xs(Ci, 0, p.q);
-    uint32_t cur = (Ci[0] >> sh) & (NC - 1);
-    // one pass over C_i in class order; the class boundary is seen in the (warp-uniform) codeword
-    for (int k = 0; k < p.q; k++) {
-      const uint32_t x = xs.take(k);
-      const uint32_t c = (x >> sh) & (NC - 1);
-      if (c != cur) {  // close class `cur`: its last K rows once, added to the finished classes
-        Core::template apply_last_rows<K>(lane, cur, p, acc);
+    for (int e = 0; e < MN; e++) acc[e] = 0ull;
+    if (__any_sync(0xffffffffu, A.active || B.active)) {
+      typename Core::Lane lane;
+      Core::init(lane, A.active ? win_bits(wa, A.s) : 0ull, B.active ? win_bits(wb, B.s) : 0ull, p);
+      const float* pa = p.priors ? p.priors + ((size_t)A.f * p.N + i) * p.q : nullptr;
+      const float* pb = p.priors ? p.priors + ((size_t)B.f * p.N + i) * p.q : nullptr;
+      f32x2* res = s_res + threadIdx.x;  // res[e * 128]: the sum over the finished classes
+      bool first = true;
+      const int sh = p.n - K;
+      XPrefetch xs(Ci, 0, p.q);
+      uint32_t cur = (Ci[0] >> sh) & (NC - 1);
+      // one pass over C_i in class order; the class boundary is seen in the (warp-uniform) codeword
+      for (int k = 0; k < p.q; k++) {
+        const uint32_t x = xs.take(k);
+        const uint32_t c = (x >> sh) & (NC - 1);
+        if (c != cur) {  // close class `cur`: its last K rows once, added to the finished classes
+          Core::template apply_last_rows<K>(lane, cur, p, acc);
 #pragma unroll
-        for (int e = 0; e < MN; e++) {
-          if (!first) acc[e] = fadd2(acc[e], res[e * kLatticeThreads]);
-          res[e * kLatticeThreads] = acc[e];
-          acc[e] = 0ull;
+          for (int e = 0; e < MN; e++) {
+            if (!first) acc[e] = fadd2(acc[e], res[e * kLatticeThreads]);
+            res[e * kLatticeThreads] = acc[e];
+            acc[e] = 0ull;
+          }
+          first = false;
+          cur = c;
         }
-        first = false;
-        cur = c;
+        f32x2 fo[MN];
+        Core::template run_prefix<K, BSIDMAP_L1_GROUP>(lane, x, p, fo);
+        if constexpr (kPri) {  // P(D_i = D) of the two windows' frames
+          const int D = Di[k];
+          const f32x2 P = pk(__ldg(pa + D), __ldg(pb + D));
+#pragma unroll
+          for (int e = 0; e < MN; e++) acc[e] = ffma2(P, fo[e], acc[e]);
+        } else {  // uniform priors: the common factor 1/q is applied at the store
+#pragma unroll
+          for (int e = 0; e < MN; e++) acc[e] = fadd2(fo[e], acc[e]);
+        }
       }
-      f32x2 fo[MN];
-      Core::template run_prefix<K, BSIDMAP_L1_GROUP>(lane, x, p, fo);
-      if constexpr (kPri) {  // P(D_i = D) of the two windows' frames
-        const int D = Di[k];
-        const f32x2 P = pk(__ldg(pa + D), __ldg(pb + D));
+      Core::template apply_last_rows<K>(lane, cur, p, acc);
+      if (!first) {
 #pragma unroll
-        for (int e = 0; e < MN; e++) acc[e] = ffma2(P, fo[e], acc[e]);
-      } else {  // uniform priors: the common factor 1/q is applied at the store
-#pragma unroll
-        for (int e = 0; e < MN; e++) acc[e] = fadd2(fo[e], acc[e]);
+        for (int e = 0; e < MN; e++) acc[e] = fadd2(acc[e], res[e * kLatticeThreads]);
       }
     }
-    Core::template apply_last_rows<K>(lane, cur, p, acc);
-    if (!first) {
+    const float sc = p.priors ? 1.f : 1.f / p.q;
+    if (A.in) {
+      float* out = p.Gsum + ((size_t)A.f * p.N + i) * MN * p.Mtp + A.mi;
 #pragma unroll
-      for (int e = 0; e < MN; e++) acc[e] = fadd2(acc[e], res[e * kLatticeThreads]);
+      for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, A, e) ? sc * lo_of(acc[e]) : 0.f;
     }
-  }
-  const float sc = p.priors ? 1.f : 1.f / p.q;
-  if (A.in) {
-    float* out = p.Gsum + ((size_t)A.f * p.N + i) * MN * p.Mtp + A.mi;
+    if (B.in) {
+      float* out = p.Gsum + ((size_t)B.f * p.N + i) * MN * p.Mtp + B.mi;
 #pragma unroll
-    for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, A, e) ? sc * lo_of(acc[e]) : 0.f;
-  }
-  if (B.in) {
-    float* out = p.Gsum + ((size_t)B.f * p.N + i) * MN * p.Mtp + B.mi;
-#pragma unroll
-    for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, B, e) ? sc * hi_of(acc[e]) : 0.f;
+      for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, B, e) ? sc * hi_of(acc[e]) : 0.f;
+    }
   }
 }
 
