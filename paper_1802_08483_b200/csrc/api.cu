@@ -375,7 +375,7 @@ void launch_pass1(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_
     if (l1 == d->kern.gamma_sum_k3 && d->kern.gamma_sum_k3_pri) l1 = d->kern.gamma_sum_k3_pri;
   }
   // the pair-core class kernels walk kL1Steps symbol indices per CTA
-  const bool multi = P.mode != kSchedStored && d->kern.l1_W == 2;
+  const bool multi = P.mode != kSchedStored && d->kern.l1_steps;
   for_i_slices(d->N, [&](int i0, int ni) {
     p.i_base = i0;
     p.i_end = i0 + ni;

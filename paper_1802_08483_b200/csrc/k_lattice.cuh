@@ -309,6 +309,7 @@ struct CoreKernels {
   long nodes;  // corridor nodes per lattice (0 = generic core: computed on host)
   int W;       // windows per lane (1 scalar core, 2 packed-pair core)
   int l1_W;    // windows per lane of the pass-1 kernel (the scalar core may serve pass 1 of a pair core)
+  bool l1_steps;  // the pass-1 (non-stored) kernels walk kL1Steps symbol indices per CTA
   int app_W;   // windows per lane of the tiled APP kernel (32 * app_W states per warp tile)
   void (*ab_warp[3])(const DecodeParams);  // warp-per-task alpha/beta for M_tau <= 32, 64, 128 (spec only)
   void (*ab_cta)(const DecodeParams, int);  // CTA-per-task alpha/beta with compile-time M_n (spec only)
@@ -335,6 +336,7 @@ CoreKernels make_core_kernels(long nodes) {
   k.ab_warp[0] = k.ab_warp[1] = k.ab_warp[2] = nullptr;
   k.local_fwd = k.local_bwd = nullptr;
   k.ab_cta = nullptr;
+  k.l1_steps = false;
   return k;
 }
 

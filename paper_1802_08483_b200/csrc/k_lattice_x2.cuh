@@ -253,56 +253,62 @@ __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_su
   constexpr int NC = 1 << K;
   extern __shared__ __align__(128) unsigned char smem[];
   float* s_res = reinterpret_cast<float*>(smem);  // [MN][128] per-lane result (private column, no barrier)
-  const int i = blockIdx.y + p.i_base;
-  const uint32_t* Ci = p.Cs[K - 2] + (size_t)i * p.q;
-  const uint16_t* Di = p.Ds[K - 2] + (size_t)i * p.q;
-  const int* cst = p.Cst[K - 2] + (size_t)i * (NC + 1);
-
-  const LaneGeom G = lane_geom(p, i);
-  float acc[MN];
-#pragma unroll
-  for (int e = 0; e < MN; e++) acc[e] = 0.f;
-  if (__any_sync(0xffffffffu, G.active)) {
-    typename Core::Lane lane;
-    Core::init(lane, G.active ? load_window(p, G.f, G.s, G.rho) : 0ull, p);
-    const float* pri = p.priors ? p.priors + ((size_t)G.f * p.N + i) * p.q : nullptr;
-    float* res = s_res + threadIdx.x;  // the sum over the finished classes
-    bool first = true;
-    int k = 0;
-    XPrefetch xs(Ci, 0, p.q);
-    // class by class (measured faster than the single loop of k_gamma_sum_x2_cls for this core)
+  const WinBase wb = win_base(p, (long)blockIdx.x * blockDim.x + threadIdx.x);
+  const int i0 = p.i_base + blockIdx.y * kL1Steps, i1 = min(i0 + kL1Steps, p.i_end);
+  Win3 nw = win_words(wb, p.n * i0 + wb.mp);
 #pragma unroll 1
-    for (int c = 0; c < NC; c++) {
-      const int kend = cst[c + 1];
-      if (k == kend) continue;
+  for (int i = i0; i < i1; i++) {
+    const LaneGeom G = geom_step(p, wb, i);
+    const Win3 ww = nw;
+    if (i + 1 < i1) nw = win_words(wb, G.s + p.n);  // prefetch the next step's received words
+    const uint32_t* Ci = p.Cs[K - 2] + (size_t)i * p.q;
+    const uint16_t* Di = p.Ds[K - 2] + (size_t)i * p.q;
+    const int* cst = p.Cst[K - 2] + (size_t)i * (NC + 1);
+    float acc[MN];
 #pragma unroll
-      for (int e = 0; e < MN; e++) acc[e] = 0.f;
-      for (; k < kend; k++) {
-        float fo[MN];
-        Core::template run_prefix<K>(lane, xs.take(k), p, fo);
-        if constexpr (kPri) {
-          const float P = __ldg(pri + Di[k]);
+    for (int e = 0; e < MN; e++) acc[e] = 0.f;
+    if (__any_sync(0xffffffffu, G.active)) {
+      typename Core::Lane lane;
+      Core::init(lane, G.active ? win_bits(ww, G.s) : 0ull, p);
+      const float* pri = p.priors ? p.priors + ((size_t)G.f * p.N + i) * p.q : nullptr;
+      float* res = s_res + threadIdx.x;  // the sum over the finished classes
+      bool first = true;
+      int k = 0;
+      XPrefetch xs(Ci, 0, p.q);
+      // class by class (measured faster than the single loop of k_gamma_sum_x2_cls for this core)
+#pragma unroll 1
+      for (int c = 0; c < NC; c++) {
+        const int kend = cst[c + 1];
+        if (k == kend) continue;
 #pragma unroll
-          for (int e = 0; e < MN; e++) acc[e] = fmaf(P, fo[e], acc[e]);
-        } else {
+        for (int e = 0; e < MN; e++) acc[e] = 0.f;
+        for (; k < kend; k++) {
+          float fo[MN];
+          Core::template run_prefix<K>(lane, xs.take(k), p, fo);
+          if constexpr (kPri) {
+            const float P = __ldg(pri + Di[k]);
 #pragma unroll
-          for (int e = 0; e < MN; e++) acc[e] += fo[e];
+            for (int e = 0; e < MN; e++) acc[e] = fmaf(P, fo[e], acc[e]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < MN; e++) acc[e] += fo[e];
+          }
         }
-      }
-      Core::template apply_last_rows<K>(lane, (uint32_t)c, p, acc);
+        Core::template apply_last_rows<K>(lane, (uint32_t)c, p, acc);
 #pragma unroll
-      for (int e = 0; e < MN; e++) {
-        if (!first) acc[e] += res[e * kLatticeThreads];
-        res[e * kLatticeThreads] = acc[e];
+        for (int e = 0; e < MN; e++) {
+          if (!first) acc[e] += res[e * kLatticeThreads];
+          res[e * kLatticeThreads] = acc[e];
+        }
+        first = false;
       }
-      first = false;
     }
-  }
-  if (G.in) {
-    const float sc = p.priors ? 1.f : 1.f / p.q;
-    float* out = p.Gsum + ((size_t)G.f * p.N + i) * MN * p.Mtp + G.mi;
+    if (G.in) {
+      const float sc = p.priors ? 1.f : 1.f / p.q;
+      float* out = p.Gsum + ((size_t)G.f * p.N + i) * MN * p.Mtp + G.mi;
 #pragma unroll
-    for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, G, e) ? sc * acc[e] : 0.f;
+      for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, G, e) ? sc * acc[e] : 0.f;
+    }
   }
 }
 
@@ -661,6 +667,7 @@ CoreKernels make_core_kernels_x2_base(long nodes) {
   k.nodes = nodes;
   k.W = 2;
   k.l1_W = 2;
+  k.l1_steps = true;
   k.app_W = 2;
   k.ab_warp[0] = k_alpha_beta_warp<1, Core::Mn>;
   k.ab_warp[1] = k_alpha_beta_warp<2, Core::Mn>;
