@@ -197,10 +197,17 @@ def main():
     rank, world, local = dist_env()
     if world != args.gpus and rank == 0:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU (LOCAL_RANK); BSIDMAP_DIST_BACKEND=gloo and the modulo over the visible
+    # devices let the multi-rank path run with several ranks on one GPU (a functional check only)
+    backend = os.environ.get("BSIDMAP_DIST_BACKEND", "nccl")
+    dev = torch.device("cuda", local % max(1, torch.cuda.device_count()))
+    torch.cuda.set_device(dev)
+    local = dev.index
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     frames = args.frames or cfg.frames
     first, count = frame_range(rank, world, frames)
