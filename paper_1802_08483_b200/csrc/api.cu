@@ -89,6 +89,7 @@ struct bsidmap_decoder {
   int num_sms = 148;
   int app_kp = -1;                      // pass-2 prefix length override (-1 = automatic)
   int app_x4 = -1;                      // four-window APP kernel (-1 = automatic, 0 = off)
+  int app_ks = -1;                      // rows folded into the APP weights (-1 = automatic; BSIDMAP_APP_KS)
   cudaStream_t s_ab = nullptr;
   cudaEvent_t ev_p1[kMaxAbSub] = {}, ev_ab[kMaxAbSub] = {};
   cudaEvent_t ev_abt[2] = {};           // alpha/beta stream busy time (timed decodes)
@@ -166,6 +167,7 @@ struct Plan {
   void (*app_kernel)(const DecodeParams);  // pass-2 kernel (prefix-sharing instance where available)
   int app_kp;                              // its prefix length (0 = none)
   int app_w4;                              // 1: app_kernel is the four-window k_app_x4 (half-warp tiles)
+  int app_ks;                              // lattice rows folded into the APP weights (1 or 2)
 };
 
 size_t budget(const bsidmap_decoder* d) {
@@ -238,6 +240,16 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
     P->app_kernel = d->kern.app_pre[P->app_kp - 2];
   else
     P->app_kp = 0;
+  // last two lattice rows folded into the APP weights (pair core, four smem tables per lane)
+  P->app_ks = 1;
+  // automatic: only for the register-heavy pair cores (2 CTAs/SM anyway, so the two extra smem
+  // tables cost no occupancy): C4 pass 2 89.1 -> 84.9 ms; C2 (4 -> 3 CTAs/SM) 57.2 -> 69.7 ms
+  const int ks = d->app_ks > 0 ? d->app_ks : d->kern.app_ks_auto;
+  if (mode == kSchedGammaSum && d->kern.app_ks2 && ks == 2 && d->n >= 3) {
+    P->app_ks = 2;
+    P->app_kernel = P->app_kp > 0 ? d->kern.app_pre_ks2[P->app_kp - 2] : d->kern.app_ks2;
+    P->app_smem = app_x2_smem(d->q, d->Mn, 2);
+  }
   // four windows per lane (k_app_x4) only on request: measured slower on B200 (C2 pass 2 41.9 vs
   // 61.5 TF/s: 3 CTAs/SM with spills against 5) -- tools/exp_x4.sh
   P->app_w4 = 0;
@@ -584,6 +596,7 @@ int bsidmap_create(bsidmap_decoder** out, int q, int n, int N, const uint32_t* c
   if (const char* v = std::getenv("BSIDMAP_AB_SUB")) d->ab_sub = std::max(1, std::atoi(v));
   if (const char* v = std::getenv("BSIDMAP_APP_KP")) d->app_kp = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("BSIDMAP_APP_X4")) d->app_x4 = std::atoi(v);
+  if (const char* v = std::getenv("BSIDMAP_APP_KS")) d->app_ks = std::atoi(v) == 2 ? 2 : 1;
   // lattice constants (eqn:F, Q-dot); row 0 = insertions only, F_{0,j} = 2^s (Pi/2)^j
   const double Pt = 1.0 - Pi - Pd;
   // G = F / Pd^r grows by at most Pd^-n over the lattice: keep 2^s Pd^-n q M_n below FLT_MAX / 2^10
@@ -828,12 +841,13 @@ int bsidmap_plan_info(bsidmap_decoder* d, int F, char* buf, size_t len) {
       "{\"mode\": \"%s\", \"frames\": %d, \"chunk\": %d, \"chunks\": %d, \"core\": \"%s\", "
       "\"lattice_grid\": [%ld, %d], \"lattice_block\": %d, \"alpha_beta_grid\": [%d, 2], \"alpha_beta_block\": %d, "
       "\"workspace_bytes\": %zu, \"windows_per_lane\": %d, \"q\": %d, \"n\": %d, \"N\": %d, \"Mn\": %d, \"Mtau\": %d, "
-      "\"alpha_beta_overlap_subbatches\": %d, \"app_prefix_bits\": %d, \"app_windows_per_lane\": %d}",
+      "\"alpha_beta_overlap_subbatches\": %d, \"app_prefix_bits\": %d, \"app_windows_per_lane\": %d, "
+      "\"app_folded_rows\": %d}",
       sched_name(P.mode), F, P.chunk, P.nchunks, d->spec ? "spec" : "generic",
       d->kern.W == 2 ? ((long)P.chunk * tiles_per_frame(d->Mt) + kX2Warps - 1) / kX2Warps
                      : (lanes + kLatticeThreads - 1) / kLatticeThreads,
       d->N, kLatticeThreads, P.chunk, P.ab_warp ? kAbWarpThreads : P.ab_threads,
-      layout(d, P.chunk, P.mode).total, d->kern.W, d->q, d->n, d->N, d->Mn, d->Mt, std::min(P.ab_sub, P.chunk), P.app_kp, P.app_w4 ? 4 : d->kern.app_W);
+      layout(d, P.chunk, P.mode).total, d->kern.W, d->q, d->n, d->N, d->Mn, d->Mt, std::min(P.ab_sub, P.chunk), P.app_kp, P.app_w4 ? 4 : d->kern.app_W, P.app_ks);
   return nb;
 }
 

@@ -304,6 +304,9 @@ struct CoreKernels {
   void (*app)(const DecodeParams);
   void (*app_pre[3])(const DecodeParams);  // APP with prefix sharing, KP = 2, 3, 4 first codeword bits (spec only)
   void (*app_x4)(const DecodeParams);      // APP on four windows per lane (SpecCoreX4; small corridors only)
+  void (*app_ks2)(const DecodeParams);     // pair-core APP with the last two rows folded (KP = 0)
+  void (*app_pre_ks2[3])(const DecodeParams);  // ... with prefix sharing KP = 2, 3, 4
+  int app_ks_auto;                         // default folded rows of this core's APP kernel
   void (*app_stored)(const DecodeParams);
   void (*gamma_dump)(const DecodeParams);
   long nodes;  // corridor nodes per lattice (0 = generic core: computed on host)
@@ -327,6 +330,9 @@ CoreKernels make_core_kernels(long nodes) {
   k.app = k_app<Core>;
   k.app_pre[0] = k.app_pre[1] = k.app_pre[2] = nullptr;
   k.app_x4 = nullptr;
+  k.app_ks2 = nullptr;
+  k.app_ks_auto = 1;
+  k.app_pre_ks2[0] = k.app_pre_ks2[1] = k.app_pre_ks2[2] = nullptr;
   k.app_stored = k_app_stored<Core::Mn>;
   k.gamma_dump = k_gamma_dump<Core>;
   k.nodes = nodes;

@@ -377,8 +377,8 @@ __device__ __forceinline__ void app_weights_pair(const DecodeParams& p, const La
 // per-warp staging of the per-lane contributions c(lane, D): [q][33] floats (odd stride), reduced
 // over the lanes once after the D loop instead of one shuffle chain per D
 __host__ __device__ __forceinline__ size_t app_stage_floats(int q) { return (size_t)q * 33; }
-__host__ __device__ __forceinline__ size_t app_x2_smem(int q, int Mn) {
-  return (size_t)kX2Warps * 2 * Mn * 32 * 8 + (size_t)kX2Warps * (app_stage_floats(q) + q) * 4;
+__host__ __device__ __forceinline__ size_t app_x2_smem(int q, int Mn, int ks = 1) {
+  return (size_t)kX2Warps * (2 << (ks - 1)) * Mn * 32 * 8 + (size_t)kX2Warps * (app_stage_floats(q) + q) * 4;
 }
 // Symbols are visited in lexicographic codeword order (DecodeParams::Cp, prepared at create) so
 // that lattice rows 1..KP (run_head) are computed once per distinct prefix; KP = 0: natural order.
@@ -394,13 +394,22 @@ __host__ __device__ __forceinline__ int app_prefix_bits(int q, int n) {
 #ifndef BSIDMAP_APP_MINB_PRE
 #define BSIDMAP_APP_MINB_PRE (Core::kMinBlocks > 2 ? 4 : 2)
 #endif
-template <class Core, int KP>
-__global__ void __launch_bounds__(kLatticeThreads, KP > 0 ? BSIDMAP_APP_MINB_PRE : BSIDMAP_APP_MINB)
+// KS = lattice rows folded into the APP weights: 1 = the last row (two tables, by x_n); 2 = the
+// last two rows (four tables, by (x_{n-1}, x_n); row n-1 transposed by SpecCoreX2::row_transpose),
+// so each symbol runs rows 1..n-2 only.  Exact re-association (the rows are linear maps).
+#ifndef BSIDMAP_APP_MINB_KS2
+#define BSIDMAP_APP_MINB_KS2 (Core::kMinBlocks > 2 ? 3 : 2)
+#endif
+template <class Core, int KP, int KS = 1>
+__global__ void __launch_bounds__(kLatticeThreads, KS == 2 ? BSIDMAP_APP_MINB_KS2
+                                                           : (KP > 0 ? BSIDMAP_APP_MINB_PRE : BSIDMAP_APP_MINB))
     k_app_x2(const DecodeParams p) {
   constexpr int MN = Core::Mn;
+  constexpr int NT = 2 << (KS - 1);  // weight tables per lane
+  constexpr int RL = Core::NNr - KS;  // last lattice row run per symbol
   extern __shared__ __align__(128) unsigned char smem[];
   f32x2* s_bt = reinterpret_cast<f32x2*>(smem);
-  float* s_S = reinterpret_cast<float*>(s_bt + kX2Warps * 2 * MN * 32);
+  float* s_S = reinterpret_cast<float*>(s_bt + kX2Warps * NT * MN * 32);
   float* s_stage = s_S + kX2Warps * p.q;
   const int i = blockIdx.y + p.i_base;
   // KP > 0: symbols in lexicographic codeword order (prefix groups contiguous); every smem array
@@ -418,7 +427,8 @@ __global__ void __launch_bounds__(kLatticeThreads, KP > 0 ? BSIDMAP_APP_MINB_PRE
   const LaneGeom B = geom_fm(p, i, f, mia + 1, mia + 1 < p.Mt);
   const bool frame_ok = p.status[f] == kFrameOk;
 
-  f32x2* wt = s_bt + (size_t)warp * 2 * MN * 32 + lane;  // w1[e] at wt[e*32], w0[e] at wt[(MN+e)*32]
+  // KS = 1: w1[e] at wt[e*32], w0[e] at wt[(MN+e)*32]; KS = 2: table c = 2 [x_n = 0] + [x_{n-1} = 0]
+  f32x2* wt = s_bt + (size_t)warp * NT * MN * 32 + lane;
   float wa, wb;
   int Emax;
   f32x2 bt[MN];
@@ -442,8 +452,27 @@ __global__ void __launch_bounds__(kLatticeThreads, KP > 0 ? BSIDMAP_APP_MINB_PRE
     typename Core::Lane lane_t;
     Core::init(lane_t, A.active ? load_window(p, A.f, A.s, A.rho) : 0ull,
                B.active ? load_window(p, B.f, B.s, B.rho) : 0ull, p);
-    Core::last_row_weights(lane_t, [&](int e) { return bt[e]; }, [&](int e) -> f32x2& { return wt[e * 32]; },
-                           [&](int e) -> f32x2& { return wt[(MN + e) * 32]; });
+    if constexpr (KS == 1) {
+      Core::last_row_weights(lane_t, [&](int e) { return bt[e]; }, [&](int e) -> f32x2& { return wt[e * 32]; },
+                             [&](int e) -> f32x2& { return wt[(MN + e) * 32]; });
+    } else {
+      f32x2 w1[MN], w0[MN], wi[MN];
+      Core::last_row_weights(lane_t, [&](int e) { return bt[e]; }, [&](int e) -> f32x2& { return w1[e]; },
+                             [&](int e) -> f32x2& { return w0[e]; });
+      const f32x2 a2 = pk(p.lc.a, p.lc.a);
+      Core::template row_transpose<Core::NNr - 1>(w1, wi, lane_t.q1, a2);  // (x_{n-1}, x_n) = (1, 1)
+#pragma unroll
+      for (int e = 0; e < MN; e++) wt[e * 32] = wi[e];
+      Core::template row_transpose<Core::NNr - 1>(w1, wi, lane_t.q0, a2);  // (0, 1)
+#pragma unroll
+      for (int e = 0; e < MN; e++) wt[(MN + e) * 32] = wi[e];
+      Core::template row_transpose<Core::NNr - 1>(w0, wi, lane_t.q1, a2);  // (1, 0)
+#pragma unroll
+      for (int e = 0; e < MN; e++) wt[(2 * MN + e) * 32] = wi[e];
+      Core::template row_transpose<Core::NNr - 1>(w0, wi, lane_t.q0, a2);  // (0, 0)
+#pragma unroll
+      for (int e = 0; e < MN; e++) wt[(3 * MN + e) * 32] = wi[e];
+    }
     const float* pri = p.priors ? p.priors + ((size_t)f * p.N + i) * p.q : nullptr;
     const int nb = p.n - 1;
     f32x2 fh[MN];  // rows 1..KP of the current prefix
@@ -458,12 +487,13 @@ __global__ void __launch_bounds__(kLatticeThreads, KP > 0 ? BSIDMAP_APP_MINB_PRE
         xprev = x;
 #pragma unroll
         for (int e = 0; e < MN; e++) fo[e] = fh[e];
-        Core::template run_tail<KP, BSIDMAP_APP_GROUP>(lane_t, x, p, fo);
+        Core::template run_tail_to<KP, RL, BSIDMAP_APP_GROUP>(lane_t, x, p, fo);
       } else {
-        Core::template run_penultimate<BSIDMAP_APP_GROUP>(lane_t, x, p, fo);
+        Core::template run_to<RL, BSIDMAP_APP_GROUP>(lane_t, x, p, fo);
       }
-      // t(m', D) = sum_k G_n(m', k, D) bt(m', k) = sum_e G_{n-1}[e] w_{x_n}[e]  (two chains)
-      const f32x2* W = wt + (((x >> nb) & 1u) ? 0 : MN * 32);
+      // t(m', D) = sum_k G_n(m', k, D) bt(m', k) = sum_e G_{n-KS}[e] w[e]  (two chains)
+      const f32x2* W = KS == 1 ? wt + (((x >> nb) & 1u) ? 0 : MN * 32)
+                               : wt + (size_t)((((x >> nb) & 1u) ? 0 : 2) + (((x >> (nb - 1)) & 1u) ? 0 : 1)) * MN * 32;
       f32x2 t0 = 0ull, t1 = 0ull;
 #pragma unroll
       for (int e = 0; e < MN; e += 2) {
@@ -661,6 +691,11 @@ CoreKernels make_core_kernels_x2_base(long nodes) {
   k.app_pre[0] = k_app_x2<Core, 2>;
   k.app_pre[1] = k_app_x2<Core, 3>;
   k.app_pre[2] = k_app_x2<Core, 4>;
+  k.app_ks2 = k_app_x2<Core, 0, 2>;
+  k.app_ks_auto = Core::kMinBlocks <= 2 ? 2 : 1;
+  k.app_pre_ks2[0] = k_app_x2<Core, 2, 2>;
+  k.app_pre_ks2[1] = k_app_x2<Core, 3, 2>;
+  k.app_pre_ks2[2] = k_app_x2<Core, 4, 2>;
   k.app_x4 = nullptr;
   k.app_stored = k_app_stored<Core::Mn>;
   k.gamma_dump = k_gamma_dump_x2<Core>;

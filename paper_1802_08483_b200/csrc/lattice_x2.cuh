@@ -42,6 +42,7 @@ __device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
 template <int NN, int LO, int MN>
 struct SpecCoreX2 {
   static constexpr int Mn = MN;
+  static constexpr int NNr = NN;  // lattice rows n
   static constexpr int W = 2;
   static constexpr int J = NN + LO + MN - 1;  // last window column n + m_n^+
   static_assert(MN >= 1 && MN <= kMaxMn && LO <= 0 && LO + MN - 1 >= 0 && J <= kMaxWindow, "shape");
@@ -155,6 +156,45 @@ struct SpecCoreX2 {
   __device__ __forceinline__ static void apply_last_rows(const Lane& L, uint32_t cls, const DecodeParams& p,
                                                          f32x2 (&f)[MN]) {
     rows<NN - K + 1, false, NN>(f, cls << (NN - K), L, pk(p.lc.a, p.lc.a));
+  }
+
+  // Rows 1..RL, and rows KP+1..RL after a shared head (the APP pass with the last n - RL rows
+  // folded into its weights).
+  template <int RL, int G = 1>
+  __device__ __forceinline__ static void run_to(const Lane& L, uint32_t x, const DecodeParams& p, f32x2 (&f)[MN]) {
+#pragma unroll
+    for (int e = 0; e < MN; e++) f[e] = pk(p.lc.row0[e], p.lc.row0[e]);
+    rows<1, G, RL>(f, x, L, pk(p.lc.a, p.lc.a));
+  }
+  template <int KP, int RL, int G = 1>
+  __device__ __forceinline__ static void run_tail_to(const Lane& L, uint32_t x, const DecodeParams& p,
+                                                     f32x2 (&f)[MN]) {
+    rows<KP + 1, G, RL>(f, x, L, pk(p.lc.a, p.lc.a));
+  }
+
+  // Transpose of lattice row R (R < n) with Q-dot table Q: weights w on the row's outputs G_R ->
+  // weights wi on its input row G_{R-1}, so that sum_e w[e] G_R[e] = sum_e wi[e] G_{R-1}[e].
+  // Row R: v_e = [chain] a v_{e-1} + Q_j G_{R-1}[e] + G_{R-1}[e+1]  (j = R + m_n^- + e >= 1),
+  //        v_e = G_{R-1}[e+1] (j = 0), structurally zero (j < 0); the chain runs for e > 0, j >= 1.
+  // Backward: dv_e = w_e + a dv_{e+1} [chain at e+1]; wi_e = [j_e >= 1] dv_e Q_{j_e} + [j_{e-1} >= 0] dv_{e-1}.
+  template <int R>
+  __device__ __forceinline__ static void row_transpose(const f32x2 (&w)[MN], f32x2 (&wi)[MN], const f32x2 (&Q)[J + 1],
+                                                       f32x2 a2) {
+    static_assert(R < NN, "the last row is folded by last_row_weights");
+    f32x2 dv[MN];
+#pragma unroll
+    for (int e = MN - 1; e >= 0; e--) {
+      const int j = R + LO + e;
+      const int jn = j + 1;  // column of node e + 1
+      const bool chain_next = (e + 1 < MN) && (jn >= 1) && (e + 1 > 0);
+      dv[e] = (j < 0) ? 0ull : (chain_next ? ffma2(a2, dv[e + 1 < MN ? e + 1 : e], w[e]) : w[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < MN; e++) {
+      const int j = R + LO + e;
+      const f32x2 left = (e >= 1 && j - 1 >= 0) ? dv[e >= 1 ? e - 1 : 0] : 0ull;
+      wi[e] = (j >= 1) ? ffma2(dv[e], Q[j < 1 ? 1 : j], left) : left;
+    }
   }
 
   // w1 (x_n = 1), w0 (x_n = 0) of run_penultimate from the corridor weights bt[e] of both windows.
