@@ -248,7 +248,7 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   if (mode == kSchedGammaSum && d->kern.app_ks2 && ks == 2 && d->n >= 3) {
     P->app_ks = 2;
     P->app_kernel = P->app_kp > 0 ? d->kern.app_pre_ks2[P->app_kp - 2] : d->kern.app_ks2;
-    P->app_smem = app_x2_smem(d->q, d->Mn, 2);
+    P->app_smem = d->kern.app_W == 2 ? app_x2_smem(d->q, d->Mn, 2) : app_x1_smem(d->q, d->Mn, 2);
   }
   // four windows per lane (k_app_x4) only on request: measured slower on B200 (C2 pass 2 41.9 vs
   // 61.5 TF/s: 3 CTAs/SM with spills against 5) -- tools/exp_x4.sh

@@ -28,6 +28,12 @@
       out->app_pre[0] = k_app_x1<SpecCore<NN, LO, MN>, 2>;                              \
       out->app_pre[1] = k_app_x1<SpecCore<NN, LO, MN>, 3>;                              \
       out->app_pre[2] = k_app_x1<SpecCore<NN, LO, MN>, 4>;                              \
+      out->app_ks2 = k_app_x1<SpecCore<NN, LO, MN>, 0, 2>;                              \
+      out->app_pre_ks2[0] = k_app_x1<SpecCore<NN, LO, MN>, 2, 2>;                       \
+      out->app_pre_ks2[1] = k_app_x1<SpecCore<NN, LO, MN>, 3, 2>;                       \
+      out->app_pre_ks2[2] = k_app_x1<SpecCore<NN, LO, MN>, 4, 2>;                       \
+      /* fold two rows where the per-symbol tail is short (C3: 90.4 -> 85.6 ms; C5, n = 12: 110 -> 113) */ \
+      out->app_ks_auto = NN <= 10 ? 2 : 1;                                              \
       out->app_W = 1;                                                                   \
     }                                                                                   \
     return true;                                                                         \

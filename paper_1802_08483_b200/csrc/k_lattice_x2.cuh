@@ -537,20 +537,23 @@ __global__ void __launch_bounds__(kLatticeThreads, KS == 2 ? BSIDMAP_APP_MINB_KS
 // Scalar-core APP on frame-aligned 32-state warp tiles (one window per lane): used where the
 // pair core is register-bound (C3, C5) -- also wastes fewer slots (C3: 9 x 32 vs 5 x 64 for 267).
 __host__ __device__ __forceinline__ int tiles_per_frame_w(int Mt, int W) { return (Mt + 32 * W - 1) / (32 * W); }
-__host__ __device__ __forceinline__ size_t app_x1_smem(int q) {
-  return (size_t)kX2Warps * (app_stage_floats(q) + q) * 4;
+__host__ __device__ __forceinline__ size_t app_x1_smem(int q, int Mn = 0, int ks = 1) {
+  return (size_t)kX2Warps * (app_stage_floats(q) + q) * 4 + (ks == 2 ? (size_t)4 * Mn * kLatticeThreads * 4 : 0);
 }
 
 #ifndef BSIDMAP_APP1_MINB_PRE
 #define BSIDMAP_APP1_MINB_PRE 3
 #endif
-template <class Core, int KP>
-__global__ void __launch_bounds__(kLatticeThreads, KP > 0 ? BSIDMAP_APP1_MINB_PRE : kLatticeMinBlocks)
+// KS = 2: the last two rows folded into four per-lane weight tables in shared memory (see k_app_x2)
+template <class Core, int KP, int KS = 1>
+__global__ void __launch_bounds__(kLatticeThreads, (KP > 0 || KS == 2) ? BSIDMAP_APP1_MINB_PRE : kLatticeMinBlocks)
     k_app_x1(const DecodeParams p) {
   constexpr int MN = Core::Mn;
+  constexpr int RL = Core::NNr - KS;  // last lattice row run per symbol
   extern __shared__ __align__(128) unsigned char smem[];
   float* s_S = reinterpret_cast<float*>(smem);
   float* s_stage = s_S + kX2Warps * p.q;
+  float* s_w = s_stage + (size_t)kX2Warps * app_stage_floats(p.q) + threadIdx.x;  // KS = 2: [4][MN][128]
   const int i = blockIdx.y + p.i_base;
   const uint32_t* Ci = (KP > 0 ? p.Cp : p.C) + (size_t)i * p.q;
   const uint16_t* Di = p.Dp + (size_t)i * p.q;
@@ -579,6 +582,21 @@ __global__ void __launch_bounds__(kLatticeThreads, KP > 0 ? BSIDMAP_APP1_MINB_PR
     Core::init(lane_t, A.active ? load_window(p, A.f, A.s, A.rho) : 0ull, p);
     float w1[MN], w0[MN];  // last lattice row folded into the weights (one table per x_n)
     Core::last_row_weights(lane_t, bt, w1, w0);
+    if constexpr (KS == 2) {  // table c = 2 [x_n = 0] + [x_{n-1} = 0], entry e at s_w[(c MN + e) 128]
+      float wi[MN];
+      Core::template row_transpose<Core::NNr - 1>(w1, wi, lane_t.q1, p.lc.a);
+#pragma unroll
+      for (int e = 0; e < MN; e++) s_w[e * kLatticeThreads] = wi[e];
+      Core::template row_transpose<Core::NNr - 1>(w1, wi, lane_t.q0, p.lc.a);
+#pragma unroll
+      for (int e = 0; e < MN; e++) s_w[(MN + e) * kLatticeThreads] = wi[e];
+      Core::template row_transpose<Core::NNr - 1>(w0, wi, lane_t.q1, p.lc.a);
+#pragma unroll
+      for (int e = 0; e < MN; e++) s_w[(2 * MN + e) * kLatticeThreads] = wi[e];
+      Core::template row_transpose<Core::NNr - 1>(w0, wi, lane_t.q0, p.lc.a);
+#pragma unroll
+      for (int e = 0; e < MN; e++) s_w[(3 * MN + e) * kLatticeThreads] = wi[e];
+    }
     const float* pri = p.priors ? p.priors + ((size_t)f * p.N + i) * p.q : nullptr;
     const int nb = p.n - 1;
     float fh[MN];  // rows 1..KP of the current prefix
@@ -593,12 +611,19 @@ __global__ void __launch_bounds__(kLatticeThreads, KP > 0 ? BSIDMAP_APP1_MINB_PR
         xprev = x;
 #pragma unroll
         for (int e = 0; e < MN; e++) fo[e] = fh[e];
-        Core::template run_tail<KP>(lane_t, x, p, fo);
+        Core::template run_tail_to<KP, RL>(lane_t, x, p, fo);
       } else {
-        Core::run_penultimate(lane_t, x, p, fo);
+        Core::template run_to<RL>(lane_t, x, p, fo);
       }
       float t0 = 0.f, t1 = 0.f;
-      if ((x >> nb) & 1u) {
+      if constexpr (KS == 2) {
+        const float* W = s_w + (size_t)((((x >> nb) & 1u) ? 0 : 2) + (((x >> (nb - 1)) & 1u) ? 0 : 1)) * MN * kLatticeThreads;
+#pragma unroll
+        for (int e = 0; e < MN; e += 2) {
+          t0 = fmaf(fo[e], W[e * kLatticeThreads], t0);
+          if (e + 1 < MN) t1 = fmaf(fo[e + 1], W[(e + 1) * kLatticeThreads], t1);
+        }
+      } else if ((x >> nb) & 1u) {
 #pragma unroll
         for (int e = 0; e < MN; e += 2) {
           t0 = fmaf(fo[e], w1[e], t0);

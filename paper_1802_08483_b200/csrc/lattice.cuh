@@ -35,6 +35,7 @@ namespace bsidmap {
 template <int NN, int LO, int MN>
 struct SpecCore {
   static constexpr int Mn = MN;
+  static constexpr int NNr = NN;  // lattice rows n
   static constexpr int lo = LO;
   static constexpr int hi = LO + MN - 1;
   static constexpr int J = NN + LO + MN - 1;  // last window column n + m_n^+
@@ -126,6 +127,37 @@ struct SpecCore {
   template <int KP>
   __device__ __forceinline__ static void run_tail(const Lane& L, uint32_t x, const DecodeParams& p, float (&f)[MN]) {
     if constexpr (KP + 1 <= NN - 1) rows<KP + 1, NN - 1>(f, x, L, p.lc);
+  }
+
+  // Rows 1..RL, and rows KP+1..RL after a shared head (SpecCoreX2::run_to / run_tail_to).
+  template <int RL>
+  __device__ __forceinline__ static void run_to(const Lane& L, uint32_t x, const DecodeParams& p, float (&f)[MN]) {
+#pragma unroll
+    for (int e = 0; e < MN; e++) f[e] = p.lc.row0[e];
+    if constexpr (RL >= 1) rows<1, RL>(f, x, L, p.lc);
+  }
+  template <int KP, int RL>
+  __device__ __forceinline__ static void run_tail_to(const Lane& L, uint32_t x, const DecodeParams& p, float (&f)[MN]) {
+    if constexpr (KP + 1 <= RL) rows<KP + 1, RL>(f, x, L, p.lc);
+  }
+  // Transpose of lattice row R < n (SpecCoreX2::row_transpose): weights on G_R -> weights on G_{R-1}.
+  template <int R>
+  __device__ __forceinline__ static void row_transpose(const float (&w)[MN], float (&wi)[MN], const float (&Q)[J + 1],
+                                                       float a) {
+    static_assert(R < NN, "the last row is folded by last_row_weights");
+    float dv[MN];
+#pragma unroll
+    for (int e = MN - 1; e >= 0; e--) {
+      const int j = R + LO + e;
+      const bool chain_next = (e + 1 < MN) && (j + 1 >= 1);
+      dv[e] = (j < 0) ? 0.f : (chain_next ? fmaf(a, dv[e + 1 < MN ? e + 1 : e], w[e]) : w[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < MN; e++) {
+      const int j = R + LO + e;
+      const float left = (e >= 1 && j - 1 >= 0) ? dv[e >= 1 ? e - 1 : 0] : 0.f;
+      wi[e] = (j >= 1) ? fmaf(dv[e], Q[j < 1 ? 1 : j], left) : left;
+    }
   }
 
   // Rows 1..n-1 only (see SpecCoreX2::run_penultimate / last_row_weights).

@@ -277,12 +277,16 @@ def test_app_four_window_kernel(name, frames, mt, monkeypatch):
     assert_parity(L4, st4, run_oracle(cfg, b))
 
 
-@pytest.mark.parametrize("name,frames", [("C1", 9), ("C2", 7), ("C4", 2)])
+@pytest.mark.parametrize("name,frames", [("C1", 9), ("C2", 7), ("C4", 2), ("C3", 3), ("C5r", 2)])
 def test_app_two_folded_rows(name, frames, monkeypatch):
     """APP pass with the last TWO lattice rows folded into its weights (row n-1 transposed,
     SpecCoreX2::row_transpose; C4's row n-1 has structurally-zero and column-0 nodes) against the
     oracle and the one-row fold."""
-    cfg = small_cfg(name)
+    if name == "C5r":  # C5's shape (scalar core, priors) with N cut for the oracle
+        full = bsidgen.configs()["C5"]
+        cfg = small_cfg("C5", N=40, mn=full.mn, mt=full.mt)
+    else:
+        cfg = small_cfg(name)
     b = bsidgen.make_batch(cfg, 5, frames)
     monkeypatch.setenv("BSIDMAP_APP_KS", "2")
     d2, L2, st2 = run_gpu(cfg, b, 3)
@@ -292,7 +296,7 @@ def test_app_two_folded_rows(name, frames, monkeypatch):
     assert d1.plan(frames)["app_folded_rows"] == 1
     monkeypatch.delenv("BSIDMAP_APP_KS")
     auto = _dec().from_config(cfg, b.C, mode=3, device=0).plan(frames)["app_folded_rows"]
-    assert auto == (2 if name == "C4" else 1)  # register-heavy pair cores only
+    assert auto == (1 if name in ("C1", "C2", "C5r") else 2)  # register-heavy shapes with short tails
     np.testing.assert_array_equal(st2, st1)
     np.testing.assert_allclose(L2, L1, rtol=2e-5, atol=1e-30)
     assert_parity(L2, st2, run_oracle(cfg, b))
