@@ -386,14 +386,17 @@ void launch_pass1(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_
     if (l1 == d->kern.gamma_sum && d->kern.gamma_sum_pri) l1 = d->kern.gamma_sum_pri;
     if (l1 == d->kern.gamma_sum_k3 && d->kern.gamma_sum_k3_pri) l1 = d->kern.gamma_sum_k3_pri;
   }
-  // the pair-core class kernels walk kL1Steps symbol indices per CTA
+  // the class kernels walk up to kL1Steps symbol indices per CTA -- fewer where the grid would
+  // not fill the GPU (small batches: single-frame latency)
   const bool multi = P.mode != kSchedStored && d->kern.l1_steps;
+  const unsigned gx1 = d->kern.l1_W == 2 ? (unsigned)((lanes + 2 * kLatticeThreads - 1) / (2 * kLatticeThreads)) : gx_flat;
+  int steps = multi ? kL1Steps : 1;
+  while (steps > 1 && (long)gx1 * ((d->N + steps - 1) / steps) < 8L * d->num_sms) steps >>= 1;
+  p.i_steps = steps;
   for_i_slices(d->N, [&](int i0, int ni) {
     p.i_base = i0;
     p.i_end = i0 + ni;
-    const unsigned gy = multi ? (unsigned)((ni + kL1Steps - 1) / kL1Steps) : (unsigned)ni;
-    l1<<<dim3(d->kern.l1_W == 2 ? (unsigned)((lanes + 2 * kLatticeThreads - 1) / (2 * kLatticeThreads)) : gx_flat, gy),
-         kLatticeThreads, P.l1_smem, s>>>(p);
+    l1<<<dim3(gx1, (unsigned)((ni + steps - 1) / steps)), kLatticeThreads, P.l1_smem, s>>>(p);
     d->launches++;
   });
 }

@@ -65,6 +65,7 @@ struct DecodeParams {
   int dbg_i;                  // symbol index of the debug dump
   int i_base;                 // first symbol index of this launch (blockIdx.y offset)
   int i_end;                  // one past the last symbol index of this launch (multi-step kernels)
+  int i_steps;                // symbol indices per CTA of the multi-step kernels
   LatticeConst lc;
 };
 

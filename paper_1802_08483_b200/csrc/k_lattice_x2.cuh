@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_
   f32x2* s_res = reinterpret_cast<f32x2*>(smem);  // [MN][128] per-lane result (private column, no barrier)
   const long ga = (long)blockIdx.x * (2 * blockDim.x) + threadIdx.x;
   const WinBase ba = win_base(p, ga), bb = win_base(p, ga + blockDim.x);
-  const int i0 = p.i_base + blockIdx.y * kL1Steps, i1 = min(i0 + kL1Steps, p.i_end);
+  const int i0 = p.i_base + blockIdx.y * p.i_steps, i1 = min(i0 + p.i_steps, p.i_end);
   Win3 na = win_words(ba, p.n * i0 + ba.mp), nb = win_words(bb, p.n * i0 + bb.mp);
 #pragma unroll 1
   for (int i = i0; i < i1; i++) {
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_su
   extern __shared__ __align__(128) unsigned char smem[];
   float* s_res = reinterpret_cast<float*>(smem);  // [MN][128] per-lane result (private column, no barrier)
   const WinBase wb = win_base(p, (long)blockIdx.x * blockDim.x + threadIdx.x);
-  const int i0 = p.i_base + blockIdx.y * kL1Steps, i1 = min(i0 + kL1Steps, p.i_end);
+  const int i0 = p.i_base + blockIdx.y * p.i_steps, i1 = min(i0 + p.i_steps, p.i_end);
   Win3 nw = win_words(wb, p.n * i0 + wb.mp);
 #pragma unroll 1
   for (int i = i0; i < i1; i++) {
