@@ -388,3 +388,29 @@ def test_bench_batch_sampled_parity(name, frames, picks):
     assert (st == 0).all()
     np.testing.assert_allclose(L.sum(2), 1.0, atol=1e-5)
     assert_parity(L, st, run_oracle(cfg, b, picks), picks)
+
+
+def test_decode_captures_into_cuda_graph():
+    """decode_batch is stream-ordered and allocation-free once its workspace exists, so a caller
+    can capture it in a CUDA graph and replay it (launch-bound small batches: C1 latency); the
+    replayed result equals the eager one bit for bit."""
+    cfg = small_cfg("C1")
+    b = bsidgen.make_batch(cfg, 3, 4)
+    Decoder = _dec()
+    d = Decoder.from_config(cfg, b.C, device=0)
+    rx, off, rho, pri = to_dev(b)
+    L = torch.empty((4, cfg.N, cfg.q), dtype=torch.float32, device="cuda")
+    st = torch.empty((4,), dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        d.decode_batch(rx, off, rho, pri, L, st, s)   # warm-up: workspace, smem opt-ins
+    torch.cuda.synchronize()
+    L_eager = L.clone()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        d.decode_batch(rx, off, rho, pri, L, st, s)
+    L.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(L, L_eager)
+    assert (st == 0).all()
