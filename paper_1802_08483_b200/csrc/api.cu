@@ -19,6 +19,7 @@
 #include "k_local_x2.cuh"
 #include "k_lattice_x4.cuh"
 #include "k_alphabeta_cta.cuh"
+#include "k_local_cta.cuh"
 
 namespace bsidmap {
 __global__ void k_frame_init(const DecodeParams p);
@@ -124,7 +125,8 @@ struct Layout {
 // Storage schedules.  kSchedLocal is the paper's local storage: gamma computed in
 // the alpha pass and again in the beta + L pass, only alpha rows kept.  kSchedGammaSum keeps
 // Gamma = sum_D gamma between two parallel lattice passes.  kSchedStored keeps every gamma.
-enum Sched { kSchedStored = 1, kSchedLocal = 2, kSchedGammaSum = 3 };
+// kSchedLocalCta is the same schedule with one CTA per frame (M_tau > 64).
+enum Sched { kSchedStored = 1, kSchedLocal = 2, kSchedGammaSum = 3, kSchedLocalCta = 4 };
 
 int resolve_sched(const bsidmap_decoder* d, int mode) {
   if (mode == BSIDMAP_MODE_STORED) return kSchedStored;
@@ -132,16 +134,24 @@ int resolve_sched(const bsidmap_decoder* d, int mode) {
   // 148.4 ms for the fused local schedule per 65536 frames, profiles/r01_*)
   if (mode == BSIDMAP_MODE_GAMMASUM || mode == BSIDMAP_MODE_AUTO) return kSchedGammaSum;
   // RECOMPUTE: the paper's local schedule where a frame fits one warp tile, else Gamma-sum
-  return (d->kern.local_fwd && d->Mt <= kTileSlots) ? kSchedLocal : kSchedGammaSum;
+  if (d->kern.local_fwd && d->Mt <= kTileSlots) return kSchedLocal;
+  if (d->kern.local_cta_bwd[0] && d->Mt <= 4 * kLocalCtaThreads &&
+      local_cta_fwd_smem(d->Mn, (d->Mt + 3) & ~3) <= 227u * 1024 &&
+      local_cta_bwd_smem(d->Mn, (d->Mt + 3) & ~3, d->q) <= 227u * 1024)
+    return kSchedLocalCta;
+  return kSchedGammaSum;
 }
 
 const char* sched_name(int s) {
-  return s == kSchedStored ? "stored" : s == kSchedLocal ? "recompute-local" : "recompute-gammasum";
+  return s == kSchedStored ? "stored"
+         : s == kSchedLocal ? "recompute-local"
+         : s == kSchedLocalCta ? "recompute-local-cta"
+                               : "recompute-gammasum";
 }
 
 Layout layout(const bsidmap_decoder* d, long F, int sched) {
   Layout l{};
-  const bool local = sched == kSchedLocal;
+  const bool local = sched == kSchedLocal || sched == kSchedLocalCta;
   l.gsum = local ? 0 : align_up((size_t)F * d->N * d->Mn * ((d->Mt + 3) & ~3) * sizeof(float));
   l.gamma = sched == kSchedStored ? align_up((size_t)F * d->N * d->q * d->Mn * d->Mt * sizeof(float)) : 0;
   l.alpha = align_up((size_t)F * (d->N + 1) * d->Mt * sizeof(double));
@@ -208,7 +218,7 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
     const size_t blk = (size_t)d->Mn * Mtp * 4;
     P->ab_stages = (int)std::max<size_t>(1, std::min<size_t>(4, (200u * 1024 - 2 * (size_t)Mtp * 8 - 600) / blk));
     P->ab_smem = ab_cta_smem(d->Mn, Mtp, P->ab_stages);
-    if (mode != kSchedLocal && P->ab_smem > 227u * 1024)
+    if (mode != kSchedLocal && mode != kSchedLocalCta && P->ab_smem > 227u * 1024)
       return fail(d, BSIDMAP_EPLAN, "M_n x M_tau too large for the shared-memory Gamma ring of the alpha/beta kernel");
   }
   P->ab_warp = nullptr;
@@ -227,9 +237,13 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   if (mode != kSchedStored && d->kern.W == 2)
     P->app_smem = d->kern.app_W == 2 ? app_x2_smem(d->q, d->Mn) : app_x1_smem(d->q);
   // tiled APP with one warp tile per frame writes L directly (no accumulators / finalize)
-  P->direct_L = mode == kSchedLocal ||
+  P->direct_L = mode == kSchedLocal || mode == kSchedLocalCta ||
                 (mode == kSchedGammaSum && d->kern.W == 2 && tiles_per_frame_w(d->Mt, d->kern.app_W) == 1);
   P->local_smem = (size_t)kLocalWarps * local_warp_smem(d->Mn, d->q);
+  if (mode == kSchedLocalCta) {  // CTA local schedule: the larger of the two passes' smem
+    const int Mtp = (d->Mt + 3) & ~3;
+    P->local_smem = std::max(local_cta_fwd_smem(d->Mn, Mtp), local_cta_bwd_smem(d->Mn, Mtp, d->q));
+  }
   // pass 1: hoist the last K lattice rows out of the symbol loop (K = 3 for q > 24, else 2)
   P->l1_kernel = (d->q > 24 && d->kern.gamma_sum_k3) ? d->kern.gamma_sum_k3 : d->kern.gamma_sum;
   // pass 2: share lattice rows 1..KP between symbols with equal first KP codeword bits
@@ -437,6 +451,21 @@ int run_chunk(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s,
     if (first_chunk) record(d, 2, s);
     if (first_chunk) record(d, 3, s);
     d->kern.local_bwd<<<gl, kLocalWarps * 32, P.local_smem, s>>>(p);
+    if (first_chunk) record(d, 4, s);
+    k_zero_failed<<<p.F, 256, 0, s>>>(p);
+    d->launches += 3;
+    if (last_chunk) record(d, 5, s);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(d, e, "kernel launch");
+    return BSIDMAP_OK;
+  }
+  if (P.mode == kSchedLocalCta) {  // the same schedule, one CTA per frame (M_tau > 64)
+    const int kk = d->q > 24 ? 1 : 0, pr = p.priors ? 1 : 0;
+    if (first_chunk) record(d, 1, s);
+    d->kern.local_cta_fwd[kk][pr]<<<p.F, kLocalCtaThreads, P.local_smem, s>>>(p);
+    if (first_chunk) record(d, 2, s);
+    if (first_chunk) record(d, 3, s);
+    d->kern.local_cta_bwd[pr]<<<p.F, kLocalCtaThreads, P.local_smem, s>>>(p);
     if (first_chunk) record(d, 4, s);
     k_zero_failed<<<p.F, 256, 0, s>>>(p);
     d->launches += 3;
@@ -663,6 +692,12 @@ int bsidmap_decode_batch_opts(bsidmap_decoder* d, int F, const uint32_t* rx, con
   if (P.mode == kSchedLocal) {
     if ((rc = set_smem(d, (const void*)d->kern.local_fwd, P.local_smem))) return rc;
     if ((rc = set_smem(d, (const void*)d->kern.local_bwd, P.local_smem))) return rc;
+  } else if (P.mode == kSchedLocalCta) {
+    for (int a = 0; a < 2; a++) {
+      for (int b = 0; b < 2; b++)
+        if ((rc = set_smem(d, (const void*)d->kern.local_cta_fwd[a][b], P.local_smem))) return rc;
+      if ((rc = set_smem(d, (const void*)d->kern.local_cta_bwd[a], P.local_smem))) return rc;
+    }
   } else if ((rc = set_smem(d, (const void*)P.app_kernel, P.app_smem))) {
     return rc;
   }
@@ -904,7 +939,8 @@ int bsidmap_debug_states(bsidmap_decoder* d, int F, double* alpha_out, double* b
     return fail(d, BSIDMAP_EINVAL, "last decode was chunked or of a different size");
   cudaSetDevice(d->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (d->last_sched == kSchedLocal) return fail(d, BSIDMAP_EINVAL, "the local schedule keeps no beta rows");
+  if (d->last_sched == kSchedLocal || d->last_sched == kSchedLocalCta)
+    return fail(d, BSIDMAP_EINVAL, "the local schedule keeps no beta rows");
   const Layout l = layout(d, d->last_chunk, d->last_sched);
   DecodeParams p;
   bind_ws(d, l, &p);

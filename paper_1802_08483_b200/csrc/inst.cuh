@@ -4,6 +4,7 @@
 #include "k_local_x2.cuh"
 #include "k_lattice_x4.cuh"
 #include "k_alphabeta_cta.cuh"
+#include "k_local_cta.cuh"
 
 // register-heavy shapes (pair core at 2 CTAs/SM) with M_n up to this use the scalar core
 #ifndef BSIDMAP_SCALAR_MN_MAX
@@ -17,6 +18,7 @@
     *out = make_core_kernels_x2<SpecCoreX2<NN, LO, MN>>(SpecCoreX2<NN, LO, MN>::nodes()); \
     out->app_x4 = app_x4_kernel<NN, LO, MN>();                                            \
     out->ab_cta = k_alpha_beta_cta<MN>;                                                   \
+    local_cta_kernels<SpecCore<NN, LO, MN>>(out);                                          \
     if (SpecCoreX2<NN, LO, MN>::kMinBlocks <= 2 && MN <= BSIDMAP_SCALAR_MN_MAX) { /* measured: scalar pass 1 wins (C3, C5) */ \
       out->gamma_sum = k_gamma_sum_cls<SpecCore<NN, LO, MN>, 2, false>;                 \
       out->gamma_sum_k3 = k_gamma_sum_cls<SpecCore<NN, LO, MN>, 3, false>;              \

@@ -317,6 +317,8 @@ struct CoreKernels {
   void (*ab_warp[3])(const DecodeParams);  // warp-per-task alpha/beta for M_tau <= 32, 64, 128 (spec only)
   void (*ab_cta)(const DecodeParams, int);  // CTA-per-task alpha/beta with compile-time M_n (spec only)
   void (*local_fwd)(const DecodeParams);   // fused local schedule, M_tau <= 64 (spec only)
+  void (*local_cta_fwd[2][2])(const DecodeParams);  // CTA-per-frame local schedule [K - 2][priors] (spec only)
+  void (*local_cta_bwd[2])(const DecodeParams);     // [priors]
   void (*local_bwd)(const DecodeParams);
 };
 
@@ -343,6 +345,8 @@ CoreKernels make_core_kernels(long nodes) {
   k.local_fwd = k.local_bwd = nullptr;
   k.ab_cta = nullptr;
   k.l1_steps = false;
+  k.local_cta_fwd[0][0] = k.local_cta_fwd[0][1] = k.local_cta_fwd[1][0] = k.local_cta_fwd[1][1] = nullptr;
+  k.local_cta_bwd[0] = k.local_cta_bwd[1] = nullptr;
   return k;
 }
 

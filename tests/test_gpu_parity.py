@@ -350,7 +350,8 @@ def test_full_c5_frame_properties():
         pytest.skip("large test disabled")
     cfg = small_cfg("C5")
     b = bsidgen.make_batch(cfg, 0, 2)
-    _, L, st = run_gpu(cfg, b, 2)
+    d, L, st = run_gpu(cfg, b, 0)
+    assert d.plan(2)["mode"] == "recompute-gammasum"
     assert (st == 0).all()
     np.testing.assert_allclose(L.sum(2), 1.0, atol=1e-5)
     conf = L.max(2) > 1 - 1e-3
@@ -363,9 +364,16 @@ def test_full_c5_frame_properties():
     for f in range(2):
         bits = 1 - b.bits(f)
         b2.rx[f] = bsidgen.pack_bits(bits, b.rx.shape[1])
-    _, L2, st2 = run_gpu(cfg, b2, 2)
+    _, L2, st2 = run_gpu(cfg, b2, 0)
     assert (st2 == 0).all()
     np.testing.assert_allclose(L2, L, rtol=1e-5, atol=1e-30)
+    # the paper's local schedule (one CTA per frame, gamma recomputed in the alpha pass and in the
+    # combined beta + L pass) on the same full-size frames agrees with the Gamma-sum one
+    d3, L3, st3 = run_gpu(cfg, b, 2)
+    assert d3.plan(2)["mode"] == "recompute-local-cta"
+    np.testing.assert_array_equal(st3, st)
+    big = L > 1e-20
+    np.testing.assert_allclose(L3[big], L[big], rtol=2e-4)
 
 
 # ----------------------------------------------- bench launch configuration, full sizes

@@ -12,6 +12,8 @@ from paper_1802_08483_b200 import Decoder  # noqa: E402
 
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 iters = int(sys.argv[sys.argv.index("--iters") + 1]) if "--iters" in sys.argv else 7
+mode = int(sys.argv[sys.argv.index("--mode") + 1]) if "--mode" in sys.argv else 0
+args = [a for a in args if not (a.isdigit() and ("--iters" in sys.argv or "--mode" in sys.argv))]
 tag = os.environ.get("KTAG", "")
 dev = torch.device("cuda", 0)
 for spec in args:
@@ -19,7 +21,7 @@ for spec in args:
     F = int(F)
     cfg = bsidgen.configs()[name]
     b = bsidgen.make_batch(cfg, 0, F)
-    d = Decoder.from_config(cfg, b.C, mode=0, device=0)
+    d = Decoder.from_config(cfg, b.C, mode=mode, device=0)
     rx = torch.from_numpy(b.rx.ravel().copy()).to(dev)
     off = torch.from_numpy(b.offsets).to(dev)
     rho = torch.from_numpy(b.rho).to(dev)
@@ -33,6 +35,6 @@ for spec in args:
     ph = np.median(np.array(ph), 0)
     flops = d.valid_lattices(b.rho) * (5 * d.lattice_nodes() - cfg.Mn)
     tot = float(sum(ph[:5]))
-    print(f"{tag} {name} F={F} total {tot:8.3f} ms  {F / tot * 1e3:10.4g} frames/s  pass1 {ph[1]:8.3f} ms "
+    print(f"{tag} {name} {d.plan(F)['mode']} F={F} total {tot:8.3f} ms  {F / tot * 1e3:10.4g} frames/s  pass1 {ph[1]:8.3f} ms "
           f"{flops / ph[1] / 1e9:6.2f} TF/s  ab {ph[2]:7.3f}  pass2 {ph[3]:8.3f} ms {flops / ph[3] / 1e9:6.2f} TF/s",
           flush=True)

@@ -110,7 +110,7 @@ def main():
     steps = int(sys.argv[sys.argv.index("--steps") + 1]) if "--steps" in sys.argv else 3
     res = []
     for name in ("C1", "C2", "C3", "C4", "C5"):
-        for mode in ((0, 2, 1) if name in ("C1", "C2") else (0,)):
+        for mode in ((0, 2, 1) if name in ("C1", "C2") else (0, 2)):
             t = time.time()
             try:
                 r = run(name, mode, steps)
