@@ -21,6 +21,11 @@
 namespace bsidmap {
 
 constexpr int kLocalCtaThreads = 256;
+// frames (CTAs) per SM: 2 (128 registers per thread) measured faster for M_n <= 20 (C3: 268 vs
+// 399 ms per 2048 frames), 1 for wider corridors (C4: 321 vs 339 ms) -- tools/exp_lcta.sh
+#ifndef BSIDMAP_LOCAL_CTA_MINB
+#define BSIDMAP_LOCAL_CTA_MINB (Core::Mn <= 20 ? 2 : 1)
+#endif
 constexpr int kLocalCtaWarps = kLocalCtaThreads / 32;
 
 // fwd smem: s_res[M_n][256] floats | s_G[M_n][Mtp] floats | row[M_n + Mtp + M_n] doubles | part[32] doubles
@@ -48,7 +53,7 @@ __device__ __forceinline__ double block_sum(double v, double* part) {
 }
 
 template <class Core, int K, bool kPri>
-__global__ void __launch_bounds__(kLocalCtaThreads, 1) k_local_cta_fwd(const DecodeParams p) {
+__global__ void __launch_bounds__(kLocalCtaThreads, BSIDMAP_LOCAL_CTA_MINB) k_local_cta_fwd(const DecodeParams p) {
   constexpr int MN = Core::Mn;
   constexpr int NC = 1 << K;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -160,7 +165,7 @@ __global__ void __launch_bounds__(kLocalCtaThreads, 1) k_local_cta_fwd(const Dec
 }
 
 template <class Core, bool kPri>
-__global__ void __launch_bounds__(kLocalCtaThreads, 1) k_local_cta_bwd(const DecodeParams p) {
+__global__ void __launch_bounds__(kLocalCtaThreads, BSIDMAP_LOCAL_CTA_MINB) k_local_cta_bwd(const DecodeParams p) {
   constexpr int MN = Core::Mn;
   extern __shared__ __align__(128) unsigned char smem[];
   const int Mt = p.Mt, Mtp = p.Mtp, N = p.N, lo = p.mn_lo;
