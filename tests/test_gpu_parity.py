@@ -317,10 +317,13 @@ def test_modes_agree_and_plan():
     # memory estimate: stored gamma > Gamma-sum > local (alpha rows only)
     assert d.workspace_bytes(16, 1) > d.workspace_bytes(16, 3) > d.workspace_bytes(16, 2)
     assert d.workspace_bytes(16, 2) == 16 * (cfg.N + 1) * cfg.Mt * 8 or d.workspace_bytes(16, 2) < 16 * (cfg.N + 1) * cfg.Mt * 8 + 512
-    # M_tau > 64: the local schedule is not available, RECOMPUTE runs the Gamma-sum schedule
+    # M_tau > 64: RECOMPUTE runs the local schedule with one CTA per frame (alpha rows only);
+    # AUTO the Gamma-sum schedule
     c3 = small_cfg("C3")
     d3 = _dec().from_config(c3, bsidgen.codebook(c3), mode=2, device=0)
-    assert d3.plan(8)["mode"] == "recompute-gammasum"
+    assert d3.plan(8)["mode"] == "recompute-local-cta"
+    assert d3.workspace_bytes(8, 2) < 8 * (c3.N + 1) * c3.Mt * 8 + 512
+    assert _dec().from_config(c3, bsidgen.codebook(c3), mode=0, device=0).plan(8)["mode"] == "recompute-gammasum"
 
 
 def test_alpha_beta_states_vs_oracle():
