@@ -1,0 +1,51 @@
+"""GPU parity on the boundaries of the method's parameter space (readings R3-R5,
+R13, R14): the widest lattice window the ABI allows (n + m_n^+ = 63 bits, M_n = 32), a complete
+codebook (q = 2^n), no deletions (Pd = 0: the non-rescaled lattice), a maximally noisy
+substitution channel, single-symbol frames, and an empty batch -- each in all three storage
+schedules against the FP64 oracle at the north-star tolerance."""
+import numpy as np
+import pytest
+import torch
+
+import bsidgen
+from .test_gpu_parity import assert_parity, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+EDGES = {
+    # n = 32, corridor [0, 31]: 32 diagonals, window n + m_n^+ = 63 bits (kMaxWindow 64, kMaxMn 32)
+    "max_window": dict(q=3, n=32, N=3, Pi=0.02, Pd=0.02, Ps=0.01, mn=(0, 31), mt=(-3, 40)),
+    # every n-bit word is a codeword (q = 2^n)
+    "full_codebook": dict(q=16, n=4, N=20, Pi=0.05, Pd=0.05, Ps=0.02),
+    # no deletions: Pd = 0 (the G = F / Pd^r rescaling is not available, generic core)
+    "no_deletions": dict(q=8, n=6, N=15, Pi=0.03, Pd=0.0, Ps=0.01),
+    # substitutions only at Ps = 0.5: the received bits carry no information, L = priors
+    "uninformative": dict(q=8, n=5, N=10, Pi=0.0, Pd=0.0, Ps=0.5),
+    # one symbol per frame (N = 1): L_0(D) = P(D) R(Y | C_0(D)) / sum
+    "single_symbol": dict(q=32, n=8, N=1, Pi=0.05, Pd=0.05, Ps=0.0),
+}
+
+
+@pytest.mark.parametrize("name", sorted(EDGES))
+def test_edge_configuration(name):
+    kw = dict(EDGES[name])
+    cfg = bsidgen.Config(name, frames=0, seed=777, priors=(name == "single_symbol"), **kw)
+    b = bsidgen.make_batch(cfg, 0, 7)
+    res = run_oracle(cfg, b)
+    for mode in (1, 2, 3):
+        _, L, st = run_gpu(cfg, b, mode)
+        assert_parity(L, st, res)
+    if name == "uninformative":  # Ps = 1/2 and no insertions/deletions: the APPs are the (uniform) priors
+        _, L, _ = run_gpu(cfg, b, 3)
+        np.testing.assert_allclose(L, 1.0 / cfg.q, rtol=1e-5)
+
+
+def test_empty_batch():
+    from paper_1802_08483_b200 import Decoder
+    cfg = bsidgen.configs()["C1"]
+    d = Decoder.from_config(cfg, bsidgen.codebook(cfg), device=0)
+    e = torch.empty(0, dtype=torch.int32, device="cuda")
+    L, st = d.decode(torch.zeros(1, dtype=torch.int32, device="cuda"), torch.empty(0, dtype=torch.int64, device="cuda"), e)
+    torch.cuda.synchronize()
+    assert L.shape == (0, cfg.N, cfg.q) and st.shape == (0,)
+    assert d.last_launch_count() == 0
