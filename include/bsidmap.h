@@ -55,8 +55,9 @@ typedef struct bsidmap_decoder bsidmap_decoder; /* opaque; owns the device codeb
 #define BSIDMAP_MODE_STORED 1    /* paper's global storage: every gamma stored in HBM, read back for L */
 #define BSIDMAP_MODE_RECOMPUTE 2 /* paper's memory-reduced (local storage) schedule: gamma computed in
                                     the alpha pass and again in the combined beta + L pass, only alpha rows kept
-                                    (fused per-frame passes; available for M_tau <= 64 with a specialised core,
-                                    otherwise the GAMMASUM schedule runs) */
+                                    (fused per-frame passes with a specialised lattice core: one warp per frame
+                                    for M_tau <= 64, one CTA per frame for 64 < M_tau <= 1024; otherwise the
+                                    GAMMASUM schedule runs) */
 #define BSIDMAP_MODE_GAMMASUM 3  /* memory-reduced variant with parallel passes: Gamma = sum_D gamma, alpha and
                                     beta kept; gamma recomputed once for L */
 
