@@ -32,6 +32,16 @@
 
 namespace bsidmap {
 
+// rows per dispatch group of the scalar core (2: row pairs in one 4-way branch); measured: single
+// rows in the pass-1 class loop (C3 pass 1 72.3 -> 67.7 ms, C5 236 -> 228), pairs in the APP pass
+// (C3 85.6 vs 87.9 ms, C5 110 vs 122) -- tools/exp_sgroup.sh
+#ifndef BSIDMAP_SCALAR_GROUP
+#define BSIDMAP_SCALAR_GROUP 2
+#endif
+#ifndef BSIDMAP_SCALAR_L1_GROUP
+#define BSIDMAP_SCALAR_L1_GROUP 1
+#endif
+
 template <int NN, int LO, int MN>
 struct SpecCore {
   static constexpr int Mn = MN;
@@ -85,21 +95,22 @@ struct SpecCore {
   // Rows are issued in pairs: a 4-way branch on (x_R, x_{R+1}) puts rows R and R+1
   // in one basic block, so the scheduler interleaves their two insertion chains
   // (row R+1 node e only needs row R nodes e, e+1) -- ILP 2 without extra registers.
-  template <int R, int RLAST = NN>
+  template <int R, int RLAST = NN, int G = BSIDMAP_SCALAR_GROUP>
   __device__ __forceinline__ static void rows(float (&f)[MN], uint32_t x, const Lane& L, const LatticeConst& lc) {
-    if constexpr (R + 1 <= RLAST) {
+    if constexpr (G >= 2 && R + 1 <= RLAST) {
       switch ((x >> (R - 1)) & 3u) {
         case 0u: row<R, true>(f, L.q0, lc); row<R + 1, true>(f, L.q0, lc); break;
         case 1u: row<R, true>(f, L.q1, lc); row<R + 1, true>(f, L.q0, lc); break;
         case 2u: row<R, true>(f, L.q0, lc); row<R + 1, true>(f, L.q1, lc); break;
         default: row<R, true>(f, L.q1, lc); row<R + 1, true>(f, L.q1, lc); break;
       }
-      rows<R + 2, RLAST>(f, x, L, lc);
-    } else if constexpr (R == RLAST) {
+      rows<R + 2, RLAST, G>(f, x, L, lc);
+    } else if constexpr (R <= RLAST) {
       if ((x >> (R - 1)) & 1u)
         row<R, true>(f, L.q1, lc);
       else
         row<R, true>(f, L.q0, lc);
+      rows<R + 1, RLAST, G>(f, x, L, lc);
     }
   }
 
@@ -108,12 +119,12 @@ struct SpecCore {
   __device__ __forceinline__ static void run_prefix(const Lane& L, uint32_t x, const DecodeParams& p, float (&f)[MN]) {
 #pragma unroll
     for (int e = 0; e < MN; e++) f[e] = p.lc.row0[e];
-    if constexpr (NN - K >= 1) rows<1, NN - K>(f, x, L, p.lc);
+    if constexpr (NN - K >= 1) rows<1, NN - K, BSIDMAP_SCALAR_L1_GROUP>(f, x, L, p.lc);
   }
   template <int K>
   __device__ __forceinline__ static void apply_last_rows(const Lane& L, uint32_t cls, const DecodeParams& p,
                                                          float (&f)[MN]) {
-    rows<NN - K + 1, NN>(f, cls << (NN - K), L, p.lc);
+    rows<NN - K + 1, NN, BSIDMAP_SCALAR_L1_GROUP>(f, cls << (NN - K), L, p.lc);
   }
 
   // Rows 1..KP (shared by symbols with the same first KP codeword bits) and rows KP+1..n-1
