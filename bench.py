@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--frames", type=int, default=None, help="frames per GPU (default: the config's batch)")
+    ap.add_argument("--total-frames", type=int, default=None,
+                    help="strong scaling: this many frames for the whole job, split over the ranks")
     ap.add_argument("--mode", default="auto", choices=["auto", "stored", "recompute"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -192,7 +194,8 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_1802_08483_b200 import Decoder, MODE_AUTO, MODE_RECOMPUTE, MODE_STORED
-    from paper_1802_08483_b200.sharding import barrier, dist_env, frame_range, max_over_ranks, sum_over_ranks
+    from paper_1802_08483_b200.sharding import (barrier, dist_env, frame_range, frame_range_strong, max_over_ranks,
+                                                sum_over_ranks)
 
     rank, world, local = dist_env()
     if world != args.gpus and rank == 0:
@@ -210,7 +213,8 @@ def main():
             dist.init_process_group(backend)
 
     frames = args.frames or cfg.frames
-    first, count = frame_range(rank, world, frames)
+    strong = args.total_frames is not None
+    first, count = frame_range_strong(rank, world, args.total_frames) if strong else frame_range(rank, world, frames)
     b = bsidgen.make_batch(cfg, first, count)
     mode = {"auto": MODE_AUTO, "stored": MODE_STORED, "recompute": MODE_RECOMPUTE}[args.mode]
     d = Decoder.from_config(cfg, b.C, mode=mode, device=local)
@@ -315,10 +319,11 @@ def main():
         line = {
             "metric": "frames/s", "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32",
             "dtype_detail": "FP32 lattice (receiver metric, P:272-275); FP64 alpha/beta and APP accumulation",
             "data": "synthetic",
-            "config": {"workload": describe(cfg), "frames_per_gpu": count, "mode": plan["mode"],
+            "config": {"workload": describe(cfg), "frames_per_gpu": count,
+                       "total_frames": int(total_frames // args.steps), "mode": plan["mode"],
                        "core": plan["core"], "chunks": plan["chunks"], "parallelism": f"frames sharded x{world}",
                        "l2": "flushed (256 MiB write) between timed steps; per-step working set > L2"},
             "symbols_per_s": value * cfg.N,

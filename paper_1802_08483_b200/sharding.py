@@ -28,6 +28,15 @@ def frame_range(rank: int, world: int, frames_per_rank: int):
     return first, frames_per_rank
 
 
+def frame_range_strong(rank: int, world: int, total_frames: int):
+    """Strong scaling: the job's total_frames split into contiguous slices whose sizes differ by
+    at most one frame (the first total % world ranks take one more)."""
+    assert 0 <= rank < world and total_frames >= 0
+    base, extra = divmod(total_frames, world)
+    first = rank * base + min(rank, extra)
+    return first, base + (1 if rank < extra else 0)
+
+
 def _red_device(device):
     # NCCL reduces device tensors; gloo (CPU tests, functional multi-rank runs) host tensors
     return device if dist.get_backend() == "nccl" else None

@@ -68,3 +68,14 @@ def test_single_process_reductions_are_identity():
     assert sharding.max_over_ranks(3.5) == 3.5
     assert sharding.sum_over_ranks(7) == 7.0
     assert sharding.frame_range(0, 1, 10) == (0, 10)
+
+
+def test_strong_scaling_partition():
+    """bench.py --total-frames: contiguous, disjoint, covering, sizes within one frame."""
+    for total in (0, 1, 7, 256, 1001):
+        for world in (1, 2, 3, 8):
+            parts = [sharding.frame_range_strong(r, world, total) for r in range(world)]
+            assert sum(c for _, c in parts) == total
+            assert all(parts[r][0] + parts[r][1] == parts[r + 1][0] for r in range(world - 1))
+            assert parts[0][0] == 0
+            assert max(c for _, c in parts) - min(c for _, c in parts) <= 1
