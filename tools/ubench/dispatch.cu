@@ -20,15 +20,28 @@ __device__ __forceinline__ float lo(u64 v) { return __uint_as_float((unsigned)v)
 #define NR 9
 #define JJ (NR + MN + 2)
 #define NLAT 256
+// u = (x_r ? q1 : q0) * f + g as two predicated FFMA2 (no branch, no select)
+__device__ __forceinline__ u64 f2fma_pred(uint32_t bit, u64 q1, u64 q0, u64 b, u64 c) {
+  u64 d;
+  asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+      "@p fma.rn.f32x2 %0, %2, %4, %5;\n\t@!p fma.rn.f32x2 %0, %3, %4, %5;\n\t}"
+      : "=l"(d) : "r"(bit), "l"(q1), "l"(q0), "l"(b), "l"(c));
+  return d;
+}
 template <int MODE>
 __device__ __forceinline__ void lrow(u64 (&f)[MN], const u64 (&q1)[JJ], const u64 (&q0)[JJ], int r, uint32_t x, u64 a2, bool b) {
   u64 prev = 0ull;
 #pragma unroll
   for (int e = 0; e < MN; e++) {
-    u64 Q;
-    if (MODE == 3) Q = ((x >> r) & 1u) ? q1[r + e] : q0[r + e];
-    else Q = b ? q1[r + e] : q0[r + e];
-    const u64 u = (e + 1 < MN) ? f2fma(Q, f[e], f[e + 1]) : f2fma(Q, f[e], 0ull);
+    u64 u;
+    if (MODE == 4) {
+      u = f2fma_pred((x >> r) & 1u, q1[r + e], q0[r + e], f[e], (e + 1 < MN) ? f[e + 1] : 0ull);
+    } else {
+      u64 Q;
+      if (MODE == 3) Q = ((x >> r) & 1u) ? q1[r + e] : q0[r + e];
+      else Q = b ? q1[r + e] : q0[r + e];
+      u = (e + 1 < MN) ? f2fma(Q, f[e], f[e + 1]) : f2fma(Q, f[e], 0ull);
+    }
     const u64 v = e > 0 ? f2fma(a2, prev, u) : u;
     f[e] = v; prev = v;
   }
@@ -47,7 +60,7 @@ __global__ void k_lat(float* out, const uint32_t* xs, float s, float a) {
     const uint32_t x = sx[l];
     u64 f[MN];
 #pragma unroll
-    for (int e = 0; e < MN; e++) f[e] = pack(1.f + e, 1.f);
+    for (int e = 0; e < MN; e++) f[e] = pack(1.f + e, __uint_as_float(x & 0x3fffffffu) * 1e-30f + 1.f);  // depends on x: not hoistable
     if (MODE == 0) {
 #pragma unroll
       for (int r = 0; r < NR; r++) lrow<0>(f, q1, q0, r, x, a2, true);
@@ -71,9 +84,26 @@ __global__ void k_lat(float* out, const uint32_t* xs, float s, float a) {
         if ((x >> (NR - 1)) & 1u) lrow<2>(f, q1, q0, NR - 1, x, a2, true);
         else lrow<2>(f, q1, q0, NR - 1, x, a2, false);
       }
-    } else {
+    } else if (MODE == 5) {  // 8-way switch per row triple
+#pragma unroll
+      for (int r = 0; r + 2 < NR; r += 3) {
+        switch ((x >> r) & 7u) {
+          case 0: lrow<2>(f, q1, q0, r, x, a2, false); lrow<2>(f, q1, q0, r + 1, x, a2, false); lrow<2>(f, q1, q0, r + 2, x, a2, false); break;
+          case 1: lrow<2>(f, q1, q0, r, x, a2, true); lrow<2>(f, q1, q0, r + 1, x, a2, false); lrow<2>(f, q1, q0, r + 2, x, a2, false); break;
+          case 2: lrow<2>(f, q1, q0, r, x, a2, false); lrow<2>(f, q1, q0, r + 1, x, a2, true); lrow<2>(f, q1, q0, r + 2, x, a2, false); break;
+          case 3: lrow<2>(f, q1, q0, r, x, a2, true); lrow<2>(f, q1, q0, r + 1, x, a2, true); lrow<2>(f, q1, q0, r + 2, x, a2, false); break;
+          case 4: lrow<2>(f, q1, q0, r, x, a2, false); lrow<2>(f, q1, q0, r + 1, x, a2, false); lrow<2>(f, q1, q0, r + 2, x, a2, true); break;
+          case 5: lrow<2>(f, q1, q0, r, x, a2, true); lrow<2>(f, q1, q0, r + 1, x, a2, false); lrow<2>(f, q1, q0, r + 2, x, a2, true); break;
+          case 6: lrow<2>(f, q1, q0, r, x, a2, false); lrow<2>(f, q1, q0, r + 1, x, a2, true); lrow<2>(f, q1, q0, r + 2, x, a2, true); break;
+          default: lrow<2>(f, q1, q0, r, x, a2, true); lrow<2>(f, q1, q0, r + 1, x, a2, true); lrow<2>(f, q1, q0, r + 2, x, a2, true); break;
+        }
+      }
+    } else if (MODE == 3) {
 #pragma unroll
       for (int r = 0; r < NR; r++) lrow<3>(f, q1, q0, r, x, a2, true);
+    } else {
+#pragma unroll
+      for (int r = 0; r < NR; r++) lrow<4>(f, q1, q0, r, x, a2, true);
     }
 #pragma unroll
     for (int e = 0; e < MN; e++) acc[e] = f2fma(f[e], q1[e], acc[e]);
@@ -104,6 +134,7 @@ int main() {
     run("disp1", [&] { k_lat<1><<<grid, block>>>(out, xs, 1.0f, 0.005f); });
     run("disp2", [&] { k_lat<2><<<grid, block>>>(out, xs, 1.0f, 0.005f); });
     run("select", [&] { k_lat<3><<<grid, block>>>(out, xs, 1.0f, 0.005f); });
+    run("disp3", [&] { k_lat<5><<<grid, block>>>(out, xs, 1.0f, 0.005f); });
   }
   return 0;
 }
