@@ -11,7 +11,7 @@ OBJS    := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(CU))
 HDRS    := $(wildcard $(CSRC)/*.cuh) include/bsidmap.h
 LIB     := paper_1802_08483_b200/libbsidmap.so
 
-all: $(LIB) oracle/libbsid_oracle.so bsidgen/libbsidgen.so
+all: $(LIB) oracle/libbsid_oracle.so bsidgen/libbsidgen.so examples/decode_host
 
 $(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
@@ -26,10 +26,14 @@ oracle/libbsid_oracle.so: oracle/bsid_oracle.c
 bsidgen/libbsidgen.so: bsidgen/bsidgen.c
 	gcc -O2 -std=c11 -fPIC -shared -o $@ $< -lm
 
+# the C ABI used from plain C (no Python): host-buffer decode of a small batch
+examples/decode_host: examples/decode_host.c include/bsidmap.h $(LIB)
+	gcc -O2 -std=c11 -Iinclude -o $@ $< -Lpaper_1802_08483_b200 -lbsidmap -Wl,-rpath,'$$ORIGIN/../paper_1802_08483_b200'
+
 ptxas:
 	@for f in $(CU); do $(NVCC) $(NVFLAGS) -Xptxas -v -c $$f -o /dev/null 2>&1 | grep -E "Compiling|registers|spill" ; done
 
 clean:
-	rm -rf build $(LIB) oracle/libbsid_oracle.so bsidgen/libbsidgen.so
+	rm -rf build $(LIB) oracle/libbsid_oracle.so bsidgen/libbsidgen.so examples/decode_host
 
 .PHONY: all clean ptxas

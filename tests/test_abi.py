@@ -5,6 +5,7 @@ import ctypes
 import glob
 import os
 import re
+import subprocess
 
 import numpy as np
 import pytest
@@ -82,3 +83,13 @@ def test_null_decoder_calls_fail_cleanly():
     assert lib.bsidmap_decode_batch(None, 1, None, None, None, None, None, None, None) == _lib.BSIDMAP_EINVAL
     assert lib.bsidmap_workspace_bytes(None, 10, 0) == 0
     lib.bsidmap_destroy(None)
+
+
+def test_c_example_builds_and_links():
+    """The C ABI is usable from plain C: examples/decode_host.c compiles against include/bsidmap.h
+    and links against the library (run on the GPU box by test_gpu_edges.test_c_example_runs)."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "examples", "decode_host")
+    r = subprocess.run(["make", "-C", root, "examples/decode_host"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert os.path.exists(exe)

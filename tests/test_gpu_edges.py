@@ -49,3 +49,17 @@ def test_empty_batch():
     torch.cuda.synchronize()
     assert L.shape == (0, cfg.N, cfg.q) and st.shape == (0,)
     assert d.last_launch_count() == 0
+
+
+def test_c_example_runs():
+    """examples/decode_host (plain C, host buffers through bsidmap_decode_batch_host) decodes its
+    256 C1-shaped frames with every frame OK and a small symbol error rate."""
+    import os
+    import re
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run(["make", "-C", root, "examples/decode_host"], check=True, capture_output=True)
+    r = subprocess.run([os.path.join(root, "examples", "decode_host")], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    ser = float(re.search(r"symbol error rate ([0-9.]+)", r.stdout).group(1))
+    assert ser < 0.05, r.stdout
