@@ -46,9 +46,14 @@ for d in kernels:
     name = d["kernel"]
     key = "lattice_pass1" if "gamma_sum" in name else "lattice_pass2" if "k_app" in name else "alpha_beta"
     rd, wr = gb(d.get("dram__bytes_read.sum", ("", ""))), gb(d.get("dram__bytes_write.sum", ("", "")))
+    fp = d.get("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", ("", ""))[0]
+    try:
+        fp = float(fp) / 100.0
+    except ValueError:
+        fp = None
     entry[key] = {"kernel": name, "dram_bytes_per_launch": (rd + wr) if rd is not None and wr is not None else None,
                   "time_ms": float(d["gpu__time_duration.sum"][0]) if "gpu__time_duration.sum" in d else None,
-                  "round": tag}
+                  "fma_pipe_active": fp, "round": tag}
     lines.append(f"## {name}")
     for m in METRICS:
         if m in d:
