@@ -1,4 +1,7 @@
 // Microbenchmark: cost of the per-row warp-uniform table dispatch in the lattice (B200).
+// Build: python tools/ubench/gen_brx.py && nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o dispatch dispatch.cu
+// Measured (warps/SM 12-20, fraction of the FMA pipe): nodisp 0.75, disp2 0.55, disp1 0.51, select 0.50,
+// disp3 0.49, pred 0.25, brx.idx jump tables 0.36-0.46.
 // A "lattice" = NR rows of MN nodes on two windows (FFMA2); row r uses table q1 or q0 by bit r
 // of a per-lattice codeword x that is warp-uniform (read from shared memory per lattice).
 //   k_nodisp : rows always use q1 (no branch) -- the ceiling
@@ -20,6 +23,7 @@ __device__ __forceinline__ float lo(u64 v) { return __uint_as_float((unsigned)v)
 #define NR 9
 #define JJ (NR + MN + 2)
 #define NLAT 256
+#include "brx_rows.cuh"
 // u = (x_r ? q1 : q0) * f + g as two predicated FFMA2 (no branch, no select)
 __device__ __forceinline__ u64 f2fma_pred(uint32_t bit, u64 q1, u64 q0, u64 b, u64 c) {
   u64 d;
@@ -98,6 +102,12 @@ __global__ void k_lat(float* out, const uint32_t* xs, float s, float a) {
           default: lrow<2>(f, q1, q0, r, x, a2, true); lrow<2>(f, q1, q0, r + 1, x, a2, true); lrow<2>(f, q1, q0, r + 2, x, a2, true); break;
         }
       }
+    } else if (MODE >= 6 && MODE <= 8) {  // one indexed jump (brx.idx) per group of G = MODE - 5 rows
+      constexpr int G = MODE - 5;
+#pragma unroll
+      for (int r = 0; r + G <= NR; r += G) brx_rows<G>(f, q1, q0, r, (x >> r) & ((1u << G) - 1u), a2);
+#pragma unroll
+      for (int r = (NR / G) * G; r < NR; r++) brx_rows<1>(f, q1, q0, r, (x >> r) & 1u, a2);
     } else if (MODE == 3) {
 #pragma unroll
       for (int r = 0; r < NR; r++) lrow<3>(f, q1, q0, r, x, a2, true);
@@ -135,6 +145,9 @@ int main() {
     run("disp2", [&] { k_lat<2><<<grid, block>>>(out, xs, 1.0f, 0.005f); });
     run("select", [&] { k_lat<3><<<grid, block>>>(out, xs, 1.0f, 0.005f); });
     run("disp3", [&] { k_lat<5><<<grid, block>>>(out, xs, 1.0f, 0.005f); });
+    run("brx1", [&] { k_lat<6><<<grid, block>>>(out, xs, 1.0f, 0.005f); });
+    run("brx2", [&] { k_lat<7><<<grid, block>>>(out, xs, 1.0f, 0.005f); });
+    run("brx3", [&] { k_lat<8><<<grid, block>>>(out, xs, 1.0f, 0.005f); });
   }
   return 0;
 }
