@@ -63,3 +63,25 @@ def test_c_example_runs():
     assert r.returncode == 0, r.stdout + r.stderr
     ser = float(re.search(r"symbol error rate ([0-9.]+)", r.stdout).group(1))
     assert ser < 0.05, r.stdout
+
+
+@pytest.mark.parametrize("shape,seed", [(s, k) for s in ("C1", "C2", "C3", "C4", "C5") for k in range(2)])
+def test_spec_shapes_random_channels(shape, seed):
+    """Each specialised lattice shape (n, m_n^-, M_n) of C1-C5 with a random channel around its
+    own (Pi, Pd, Ps > 0 for every shape), random priors on or off and a short frame, in the
+    three storage schedules and the auto plan, against the oracle."""
+    rng = np.random.default_rng(100 + seed)
+    base = bsidgen.configs()[shape]
+    Pi = float(base.Pi * rng.uniform(0.5, 1.5))
+    Pd = float(base.Pd * rng.uniform(0.5, 1.5))
+    Ps = float(rng.choice([0.0, 0.003, 0.02]))
+    N = int(rng.integers(3, 9))
+    cfg = bsidgen.Config(f"{shape}r{seed}", q=base.q, n=base.n, N=N, Pi=Pi, Pd=Pd, Ps=Ps, frames=0,
+                         priors=bool(rng.random() < 0.5), mn=base.mn,
+                         mt=(min(base.mn[0], -3 * base.n), max(base.mn[1], 3 * base.n)), seed=500 + seed)
+    b = bsidgen.make_batch(cfg, 0, int(rng.integers(2, 7)))
+    res = run_oracle(cfg, b)
+    for mode in (0, 1, 2, 3):
+        d, L, st = run_gpu(cfg, b, mode)
+        assert d.plan(len(b.rho))["core"] == "spec"
+        assert_parity(L, st, res)
