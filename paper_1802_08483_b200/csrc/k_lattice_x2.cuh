@@ -138,14 +138,9 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_
 // Pass 1 with the last K lattice rows hoisted out of the symbol loop.  The rows are linear in
 // the row they read and rows n-K+1..n depend only on the codeword's last K bits, so
 //   Gamma_i(m', .) = sum_cls Last_cls( sum_{D : C_i(D) ends in cls} P(D) G_{n-K}(m', ., D) ):
-// the symbols are visited class by class (a per-CTA counting sort of C_i by its last K bits)
+// the symbols are visited class by class (C_i grouped by its last K bits once at create: Cs/Ds/Cst)
 // and the last K rows run once per class instead of once per symbol.  Exact algebra; the
 // node count of the algorithm is unchanged (the roofline still counts 5 flops per node).
-template <int K>
-__host__ __device__ __forceinline__ size_t cls_smem(int q, int Mn, int lanes_pairs) {
-  return (size_t)q * 4 + (size_t)((q * 2 + 15) / 16) * 16 + 64 + (size_t)Mn * lanes_pairs * 8;
-}
-
 // Symbol indices per CTA of the pass-1 kernels: the windows' frame geometry is loaded once and the
 // received words of step i + 1 are prefetched while step i computes.
 #ifndef BSIDMAP_L1_STEPS
@@ -462,9 +457,6 @@ __device__ __forceinline__ void app_weights_pair(const DecodeParams& p, const La
 #endif
 #ifndef BSIDMAP_APP_GROUP
 #define BSIDMAP_APP_GROUP (Core::kMinBlocks > 2 ? 2 : 1)
-#endif
-#ifndef BSIDMAP_APP_BT_SMEM
-#define BSIDMAP_APP_BT_SMEM 1
 #endif
 // per-warp staging of the per-lane contributions c(lane, D): [q][33] floats (odd stride), reduced
 // over the lanes once after the D loop instead of one shuffle chain per D
