@@ -12,6 +12,16 @@ from tests.test_gpu_parity import FLOOR, TOL, _dec, run_oracle, small_cfg, to_de
 pytestmark = pytest.mark.gpu
 
 
+def _cfg(name, **kw):
+    """C1/C2 as configured; "C3r", "C4r", "C5r": that config's code, channel, corridor and trellis
+    (M_tau 267 / 611 / 906: CTA alpha/beta, scalar or register-heavy APP kernels, the CTA local
+    schedule) with N cut to 24 so the oracle stays fast."""
+    if name.endswith("r"):
+        full = bsidgen.configs()[name[:-1]]
+        return small_cfg(name[:-1], N=24, mn=full.mn, mt=full.mt, **kw)
+    return small_cfg(name, **kw)
+
+
 def _soft_batch(cfg, F, seed):
     """Frames whose received sequence carries extra random bits before and after the
     frame, decoded with a start-drift prior and end-drift weights over the states."""
@@ -36,9 +46,10 @@ def _soft_batch(cfg, F, seed):
     return b, a0, bN
 
 
-@pytest.mark.parametrize("name,mode", [("C1", 1), ("C1", 2), ("C1", 3), ("C2", 2), ("C2", 3)])
+@pytest.mark.parametrize("name,mode", [("C1", 1), ("C1", 2), ("C1", 3), ("C2", 2), ("C2", 3), ("C3r", 0),
+                                       ("C3r", 2), ("C4r", 0), ("C4r", 2), ("C5r", 0), ("C5r", 2)])
 def test_soft_boundary_priors_parity(name, mode):
-    cfg = small_cfg(name)
+    cfg = _cfg(name)
     b, a0, bN = _soft_batch(cfg, 12, seed=hash(name) % 97)
     d = _dec().from_config(cfg, b.C, mode=mode, device=0)
     rx, off, rho, pri = to_dev(b)
@@ -48,7 +59,8 @@ def test_soft_boundary_priors_parity(name, mode):
     prob = oracle.Problem(cfg.q, cfg.n, cfg.N, b.C, cfg.Pi, cfg.Pd, cfg.Ps, cfg.mn, cfg.mt)
     worst = 0.0
     for f in range(12):
-        r = oracle.decode(prob, b.bits(f), alpha0=a0[f], betaN=bN[f])
+        pf = b.priors[f].astype(np.float64) if b.priors is not None else None
+        r = oracle.decode(prob, b.bits(f), pf, alpha0=a0[f], betaN=bN[f])
         assert st[f] == r["status"]
         if r["status"] != oracle.OK:
             continue
@@ -73,9 +85,10 @@ def test_soft_boundary_generic_core():
             assert (np.abs(L[f] - r["L"]) / np.maximum(r["L"], FLOOR)).max() <= TOL
 
 
-@pytest.mark.parametrize("name,mode", [("C1", 3), ("C2", 2), ("C2", 3)])
+@pytest.mark.parametrize("name,mode", [("C1", 3), ("C2", 2), ("C2", 3), ("C3r", 0), ("C4r", 0), ("C5r", 0),
+                                       ("C5r", 2)])
 def test_extrinsic_parity(name, mode):
-    cfg = small_cfg(name, priors=True)
+    cfg = _cfg(name, priors=True)
     b = bsidgen.make_batch(cfg, 0, 10)
     b.priors[1, 2, :] = 0.0
     b.priors[1, 2, 0] = 1.0
