@@ -114,6 +114,31 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- oracle leg
 
+ORACLE_FRAME_SECONDS = 4.0  # target single-core oracle time of one sampled frame
+
+
+def oracle_workload(cfg):
+    """(config the oracle is timed on, frames/s scale to the full config).  A full C4/C5 frame takes
+    the FP64 oracle minutes to an hour on one core, so long frames are timed as frames of the same
+    code, channel, corridor and trellis with fewer symbol positions N_s (every oracle step costs the
+    same: ~2 passes x M_tau q lattices x corridor cells), and the rate is scaled by N_s / N."""
+    cells = cfg.n * cfg.Mn - cfg.mn[0] * (cfg.mn[0] - 1) // 2
+    per_symbol = 2 * cfg.Mt * cfg.q * cells * 12e-9  # ~12 ns per FP64 cell on one core (SURVEY 8(d))
+    ns = int(max(10, min(cfg.N, ORACLE_FRAME_SECONDS / per_symbol)))
+    if ns >= cfg.N:
+        return cfg, 1.0, ""
+
+    def windows(N):  # lattice windows the oracle evaluates: 0 <= n i + m' <= rho (~ n N), reading R5
+        t = cfg.n * N
+        return sum(max(0, min(cfg.mt[1], t - cfg.n * i) - max(cfg.mt[0], -cfg.n * i) + 1) for i in range(N))
+
+    import dataclasses
+    sc = dataclasses.replace(cfg, N=ns, name=f"{cfg.name}@N{ns}")
+    scale = windows(ns) / windows(cfg.N)
+    return sc, scale, (f"; timed on frames of {cfg.name}'s code/channel/trellis with N = {ns}, rate scaled by "
+                       f"the ratio of lattice windows {scale:.3g}")
+
+
 def oracle_sample(cfg, target_seconds, first=10_000_000, max_frames=4096):
     """Time the FP64 oracle (as it stands) on host cores over a bounded sample of the workload."""
     import oracle
@@ -143,11 +168,12 @@ def run_oracle_frames(cfg, prob, first, count, threads):
 
 
 def cpu_baseline(cfg, target_seconds):
-    prob, count, _, threads = oracle_sample(cfg, target_seconds)
-    dt = run_oracle_frames(cfg, prob, 20_000_000, count, threads)
-    return {"value": count / dt, "unit": "frames/s", "cores": threads, "kind": "oracle",
-            "sample": f"{count} frames of {cfg.name} (global frame indices 20000000..), FP64 C oracle, "
-                      f"{threads} host threads over frames, {dt:.1f} s"}
+    ocfg, scale, note = oracle_workload(cfg)
+    prob, count, _, threads = oracle_sample(ocfg, target_seconds)
+    dt = run_oracle_frames(ocfg, prob, 20_000_000, count, threads)
+    return {"value": count / dt * scale, "unit": "frames/s", "cores": threads, "kind": "oracle",
+            "sample": f"{count} frames of {ocfg.name} (global frame indices 20000000..), FP64 C oracle, "
+                      f"{threads} host threads over frames, {dt:.1f} s{note}"}
 
 
 def reference_arm(args, cfg):
@@ -156,21 +182,22 @@ def reference_arm(args, cfg):
     if rank != 0:
         return
     per_step = max(2.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
-    prob, count, _, threads = oracle_sample(cfg, per_step)
+    ocfg, scale, note = oracle_workload(cfg)
+    prob, count, _, threads = oracle_sample(ocfg, per_step)
     for w in range(args.warmup):
-        run_oracle_frames(cfg, prob, 30_000_000 + w * count, count, threads)
-    times = [run_oracle_frames(cfg, prob, 40_000_000 + s * count, count, threads) for s in range(args.steps)]
+        run_oracle_frames(ocfg, prob, 30_000_000 + w * count, count, threads)
+    times = [run_oracle_frames(ocfg, prob, 40_000_000 + s * count, count, threads) for s in range(args.steps)]
     total = sum(times)
-    value = count * args.steps / total
+    value = count * args.steps / total * scale  # frames/s of the full configuration
     line = {
         "impl": "reference", "metric": "frames/s", "value": value, "unit": "frames/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": describe(cfg), "frames_per_step": count, "sample": "bounded oracle sample"},
+        "config": {"workload": describe(cfg), "frames_per_step": count, "sample": "bounded oracle sample" + note},
         "symbols_per_s": value * cfg.N,
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "oracle",
-                         "sample": f"{count} frames x {args.steps} steps of {cfg.name}, FP64 C oracle on "
-                                   f"{threads} host threads"},
+                         "sample": f"{count} frames x {args.steps} steps of {ocfg.name}, FP64 C oracle on "
+                                   f"{threads} host threads{note}"},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
