@@ -261,7 +261,9 @@ def main():
     torch.cuda.synchronize(dev)
 
     nodes = d.lattice_nodes()
-    lattices = d.valid_lattices(b.rho)          # windows with 0 <= n i + m' <= rho, per lattice pass
+    # windows with 0 <= n i + m' <= rho, per lattice pass, of the frames the phase events time: the
+    # library's phase events bracket the FIRST chunk's kernels when the batch is chunked
+    lattices = d.valid_lattices(b.rho[:plan["chunk"]])
     flops_per_lattice = 5 * nodes - cfg.Mn       # P:857 node count; 3 mul + 2 add per node, last row 3 flops
     flops_pass = lattices * flops_per_lattice
 
@@ -362,6 +364,7 @@ def main():
                          "peak_basis": f"{sms} SMs x 128 FP32 lanes x 2 flop x 1965 MHz (max SM clock); "
                                        "derived, MEASURED_PEAKS.json has no FP32 entry",
                          "flops_per_launch": flops_pass, "launch_ms": float(mean_ph[dominant]),
+                         "frames_per_launch": int(min(plan["chunk"], count)),
                          "fma_pipe_active_ncu": pipe,
                          "note": "achieved counts the paper's 5 flops per lattice node (P:857); the kernel "
                                  "executes 2 FFMA per node after exact re-associations, so the executed FMA-pipe "

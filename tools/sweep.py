@@ -45,10 +45,11 @@ def run(name, mode, steps):
         tot.append(e0.elapsed_time(e1))
     ms = float(np.median(tot))
     phm = np.median(np.array(ph), 0)
-    flops = d.valid_lattices(b.rho) * (5 * d.lattice_nodes() - cfg.Mn)
+    plan = d.plan(F)
+    # phases 1-3 time the first chunk's kernels: the flops of that chunk
+    flops = d.valid_lattices(b.rho[:plan["chunk"]]) * (5 * d.lattice_nodes() - cfg.Mn)
     p1 = flops / (phm[1] / 1e3) / 1e12
     p2 = flops / (phm[3] / 1e3) / 1e12
-    plan = d.plan(F)
     ser = float((np.argmax(L.cpu().numpy(), 2) != b.msg).mean())
     extra = {}
     if plan["mode"] == "stored":
