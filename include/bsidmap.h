@@ -72,8 +72,17 @@ typedef struct bsidmap_decoder bsidmap_decoder; /* opaque; owns the device codeb
  *                    mn_lo <= 0 <= mn_hi, n + mn_hi <= 64.
  *   mt_lo, mt_hi   : trellis drift limits m_tau^-, m_tau^+ (M_tau states), mt_lo <= mn_lo, mt_hi >= mn_hi.
  *   mode           : BSIDMAP_MODE_* (0..3).
- * On success *out receives the decoder.  Allocates only the codebook (N*q*4 bytes);
+ * On success *out receives the decoder.  Allocates the codebook and its symbol visiting orders
+ * (about 3 N q * 6 bytes: lexicographic and last-2/3-bit class orders used by the lattice passes);
  * the workspace is allocated lazily by the first decode of a given size.
+ *
+ * Kernel-variant overrides, read from the environment at create (measurement and testing only;
+ * the defaults are the measured-fastest choices):
+ *   BSIDMAP_AB_SUB=k   alpha/beta side-stream sub-batches (1 = off; default: 2 when 2F <= #SMs)
+ *   BSIDMAP_APP_KP=k   APP prefix-sharing length (0 = off; default ~log2(q) - 1)
+ *   BSIDMAP_APP_KS=k   lattice rows folded into the APP weights (1 or 2; default 2 for register-heavy shapes)
+ *   BSIDMAP_APP_X4=1   four-window APP kernel (small corridors; default off)
+ *   BSIDMAP_L1_PRE=1   pass 1 with prefix sharing + shared-memory class sums (default off)
  */
 int bsidmap_create(bsidmap_decoder **out, int q, int n, int N, const uint32_t *codebook_host,
                    double Pi, double Pd, double Ps, int mn_lo, int mn_hi, int mt_lo, int mt_hi,
