@@ -663,7 +663,9 @@ int bsidmap_create(bsidmap_decoder** out, int q, int n, int N, const uint32_t* c
     const int j = mn_lo + e;
     d->lc.row0[e] = (e < Mn && j >= 0) ? (float)std::ldexp(std::pow(0.5 * Pi, j), seed) : 0.f;
   }
-  d->spec = rescaled && find_spec_kernels(n, mn_lo, Mn, &d->kern);
+  // the specialised APP kernels stage one float per (symbol, lane) in shared memory (~544 q bytes
+  // per CTA): very large alphabets use the generic core, whose APP pass stages symbols in chunks
+  d->spec = rescaled && (size_t)q * 544 + 64 * 1024 <= 227u * 1024 && find_spec_kernels(n, mn_lo, Mn, &d->kern);
   if (!d->spec && !find_generic_kernels(Mn, &d->kern)) {
     delete d;
     return fail(nullptr, BSIDMAP_EPLAN, "no lattice core for M_n = " + std::to_string(Mn));

@@ -85,3 +85,16 @@ def test_spec_shapes_random_channels(shape, seed):
         d, L, st = run_gpu(cfg, b, mode)
         assert d.plan(len(b.rho))["core"] == "spec"
         assert_parity(L, st, res)
+
+
+def test_large_alphabet_uses_generic_core():
+    """q = 512 on C2's lattice shape: the specialised APP kernels would need more shared memory than
+    a CTA has, so the decoder takes the generic core; parity against the oracle in all schedules."""
+    cfg = bsidgen.Config("bigq", q=512, n=10, N=3, Pi=0.01, Pd=0.01, Ps=0.001, frames=0, seed=31,
+                         mn=(-6, 7), mt=(-12, 12))
+    b = bsidgen.make_batch(cfg, 0, 3)
+    res = run_oracle(cfg, b)
+    for mode in (0, 1, 2, 3):
+        d, L, st = run_gpu(cfg, b, mode)
+        assert d.plan(3)["core"] == "generic"
+        assert_parity(L, st, res)
