@@ -27,7 +27,8 @@ constexpr int kLocalWarps = 4;  // frames per CTA
 //                s_row[64] doubles | s_C[q] words
 __host__ __device__ __forceinline__ int local_g_floats(int Mn, int q) { return Mn * 64 > q ? Mn * 64 : q; }
 __host__ __device__ __forceinline__ size_t local_warp_smem(int Mn, int q) {
-  return (size_t)local_g_floats(Mn, q) * 4 + 64 * 8 + (size_t)q * 4;
+  // rounded to 16 bytes: the next warp's FP64 row must stay 8-byte aligned for odd q
+  return ((size_t)local_g_floats(Mn, q) * 4 + 64 * 8 + (size_t)q * 4 + 15) & ~size_t(15);
 }
 
 template <class Core>

@@ -98,3 +98,18 @@ def test_large_alphabet_uses_generic_core():
         d, L, st = run_gpu(cfg, b, mode)
         assert d.plan(3)["core"] == "generic"
         assert_parity(L, st, res)
+
+
+@pytest.mark.parametrize("shape,q", [("C5", 25), ("C2", 7), ("C3", 31)])
+def test_odd_alphabet_local_schedule(shape, q):
+    """Odd q on a specialised shape with M_tau <= 64 (the warp-per-frame local schedule): the per-warp
+    shared-memory slices must keep the FP64 rows 8-byte aligned (found by tools/stress.py)."""
+    base = bsidgen.configs()[shape]
+    cfg = bsidgen.Config(f"odd{shape}", q=q, n=base.n, N=5, Pi=0.02, Pd=0.02, Ps=0.01, frames=0, seed=63,
+                         mn=base.mn, mt=(base.mn[0] - 6, base.mn[1] + 7))
+    b = bsidgen.make_batch(cfg, 0, 24)
+    res = run_oracle(cfg, b)
+    for mode in (2, 3):
+        d, L, st = run_gpu(cfg, b, mode)
+        assert_parity(L, st, res)
+    assert d.plan(24)["core"] == "spec"
