@@ -91,7 +91,6 @@ struct bsidmap_decoder {
   int app_kp = -1;                      // pass-2 prefix length override (-1 = automatic)
   int app_x4 = -1;                      // four-window APP kernel (-1 = automatic, 0 = off)
   int app_ks = -1;                      // rows folded into the APP weights (-1 = automatic; BSIDMAP_APP_KS)
-  int l1_pre = -1;                      // pass-1 prefix sharing (-1 = automatic; BSIDMAP_L1_PRE)
   cudaStream_t s_ab = nullptr;
   cudaEvent_t ev_p1[kMaxAbSub] = {}, ev_ab[kMaxAbSub] = {};
   cudaEvent_t ev_abt[2] = {};           // alpha/beta stream busy time (timed decodes)
@@ -179,7 +178,6 @@ struct Plan {
   int app_kp;                              // its prefix length (0 = none)
   int app_w4;                              // 1: app_kernel is the four-window k_app_x4 (half-warp tiles)
   int app_ks;                              // lattice rows folded into the APP weights (1 or 2)
-  int l1_pre;                              // pass 1 with prefix sharing (prefix length; 0 = class kernel)
 };
 
 size_t budget(const bsidmap_decoder* d) {
@@ -248,17 +246,6 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   }
   // pass 1: hoist the last K lattice rows out of the symbol loop (K = 3 for q > 24, else 2)
   P->l1_kernel = (d->q > 24 && d->kern.gamma_sum_k3) ? d->kern.gamma_sum_k3 : d->kern.gamma_sum;
-  // pass 1 with prefix sharing + suffix classes in shared memory (pair core)
-  P->l1_pre = 0;
-  {
-    const int kp = app_prefix_bits(d->q, d->n);
-    const int want = d->l1_pre >= 0 ? d->l1_pre : 0;
-    if (mode != kSchedStored && want && kp >= 2 && d->kern.l1_W == 2 && d->kern.gamma_sum_pre[kp - 2][0] &&
-        kp + 1 <= d->n - 2) {
-      P->l1_pre = kp;
-      P->l1_smem = pre_smem(d->Mn);
-    }
-  }
   // pass 2: share lattice rows 1..KP between symbols with equal first KP codeword bits
   P->app_kp = (mode == kSchedStored) ? 0 : app_prefix_bits(d->q, d->n);
   if (d->app_kp >= 0) P->app_kp = (d->app_kp == 0 || d->app_kp > d->n - 2) ? 0 : std::min(4, std::max(2, d->app_kp));
@@ -299,7 +286,6 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   P->l1_smem = (d->kern.gamma_sum_k3 && mode != kSchedStored)
                    ? (size_t)d->Mn * kLatticeThreads * 8 + (size_t)d->q * 6 + 64 + 16
                    : (size_t)d->q * 4;
-  if (P->l1_pre) P->l1_smem = pre_smem(d->Mn);
   return BSIDMAP_OK;
 }
 
@@ -410,8 +396,7 @@ void launch_pass1(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_
   const long lanes = (long)p.F * d->Mt;
   const unsigned gx_flat = (unsigned)((lanes + kLatticeThreads - 1) / kLatticeThreads);
   auto l1 = P.mode == kSchedStored ? d->kern.gamma_store : P.l1_kernel;
-  if (P.l1_pre) l1 = d->kern.gamma_sum_pre[P.l1_pre - 2][p.priors ? 1 : 0];
-  else if (P.mode != kSchedStored && p.priors) {  // the non-uniform-prior instance of the pass-1 kernel
+  if (P.mode != kSchedStored && p.priors) {  // the non-uniform-prior instance of the pass-1 kernel
     if (l1 == d->kern.gamma_sum && d->kern.gamma_sum_pri) l1 = d->kern.gamma_sum_pri;
     if (l1 == d->kern.gamma_sum_k3 && d->kern.gamma_sum_k3_pri) l1 = d->kern.gamma_sum_k3_pri;
   }
@@ -644,7 +629,6 @@ int bsidmap_create(bsidmap_decoder** out, int q, int n, int N, const uint32_t* c
   if (const char* v = std::getenv("BSIDMAP_APP_KP")) d->app_kp = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("BSIDMAP_APP_X4")) d->app_x4 = std::atoi(v);
   if (const char* v = std::getenv("BSIDMAP_APP_KS")) d->app_ks = std::atoi(v) == 2 ? 2 : 1;
-  if (const char* v = std::getenv("BSIDMAP_L1_PRE")) d->l1_pre = std::atoi(v) ? 1 : 0;
   // lattice constants (eqn:F, Q-dot); row 0 = insertions only, F_{0,j} = 2^s (Pi/2)^j
   const double Pt = 1.0 - Pi - Pd;
   // G = F / Pd^r grows by at most Pd^-n over the lattice: keep 2^s Pd^-n q M_n below FLT_MAX / 2^10
@@ -707,9 +691,6 @@ int bsidmap_decode_batch_opts(bsidmap_decoder* d, int F, const uint32_t* rx, con
   if ((rc = ensure_ws(d, l.total))) return rc;
   if ((rc = set_smem(d, P.ab_warp ? (const void*)P.ab_warp : (const void*)P.ab_cta, P.ab_smem))) return rc;
   if ((rc = set_smem(d, (const void*)P.l1_kernel, P.l1_smem))) return rc;
-  if (P.l1_pre)
-    for (int b = 0; b < 2; b++)
-      if ((rc = set_smem(d, (const void*)d->kern.gamma_sum_pre[P.l1_pre - 2][b], P.l1_smem))) return rc;
   if (P.mode == kSchedLocal) {
     if ((rc = set_smem(d, (const void*)d->kern.local_fwd, P.local_smem))) return rc;
     if ((rc = set_smem(d, (const void*)d->kern.local_bwd, P.local_smem))) return rc;

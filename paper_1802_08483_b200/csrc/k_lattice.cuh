@@ -298,7 +298,6 @@ __global__ void __launch_bounds__(kLatticeThreads) k_gamma_dump(const DecodePara
 struct CoreKernels {
   void (*gamma_sum)(const DecodeParams);
   void (*gamma_sum_k3)(const DecodeParams);  // pass 1 with 3 hoisted rows (large q); nullptr = none
-  void (*gamma_sum_pre[3][2])(const DecodeParams);  // pass 1 with prefix sharing + 2 suffix rows [KP-2][priors]
   void (*gamma_sum_pri)(const DecodeParams);     // the same two with non-uniform priors (nullptr: the
   void (*gamma_sum_k3_pri)(const DecodeParams);  // plain kernels read priors themselves)
   void (*gamma_store)(const DecodeParams);
@@ -329,7 +328,6 @@ CoreKernels make_core_kernels(long nodes) {
   k.gamma_sum = k_gamma_sum<Core, false>;
   k.gamma_sum_k3 = nullptr;
   k.gamma_sum_pri = k.gamma_sum_k3_pri = nullptr;
-  for (int a = 0; a < 3; a++) k.gamma_sum_pre[a][0] = k.gamma_sum_pre[a][1] = nullptr;
   k.gamma_store = k_gamma_sum<Core, true>;
   k.app = k_app<Core>;
   k.app_pre[0] = k.app_pre[1] = k.app_pre[2] = nullptr;

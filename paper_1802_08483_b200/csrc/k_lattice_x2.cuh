@@ -241,98 +241,6 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_
   }
 }
 
-// Pass 1 with BOTH re-associations: symbols in lexicographic codeword order (Cp/Dp) share lattice
-// rows 1..KP per distinct prefix (as the APP pass), and each symbol's row n-2 output is added, with
-// its prior, into the shared-memory accumulator of its suffix class (last two codeword bits); the
-// last two rows then run once per class on the class sums:
-//   Gamma_i(m', .) = sum_cls Last2_cls( sum_{D in cls} P(D) G_{n-2}(m', ., D) ).
-// The accumulators live in shared memory ([4][M_n][128 lanes] pairs, per-lane columns: no barrier),
-// so the prefix row takes the registers the class accumulator held before.
-__host__ __device__ __forceinline__ size_t pre_smem(int Mn) { return (size_t)4 * Mn * kLatticeThreads * 8; }
-
-template <class Core, int KP, bool kPri>
-__global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_x2_pre(const DecodeParams p) {
-  constexpr int MN = Core::Mn;
-  constexpr int RL = Core::NNr - 2;  // rows run per symbol (after the shared head)
-  extern __shared__ __align__(128) unsigned char smem[];
-  f32x2* s_acc = reinterpret_cast<f32x2*>(smem) + threadIdx.x;  // [4][MN][128], this lane's column
-  const long ga = (long)blockIdx.x * (2 * blockDim.x) + threadIdx.x;
-  const WinBase ba = win_base(p, ga), bb = win_base(p, ga + blockDim.x);
-  const int i0 = p.i_base + blockIdx.y * p.i_steps, i1 = min(i0 + p.i_steps, p.i_end);
-  Win3 na = win_words(ba, p.n * i0 + ba.mp), nb = win_words(bb, p.n * i0 + bb.mp);
-  const int sh = p.n - 2;
-#pragma unroll 1
-  for (int i = i0; i < i1; i++) {
-    const LaneGeom A = geom_step(p, ba, i), B = geom_step(p, bb, i);
-    const Win3 wa = na, wb = nb;
-    if (i + 1 < i1) {  // prefetch the next step's received words
-      na = win_words(ba, A.s + p.n);
-      nb = win_words(bb, B.s + p.n);
-    }
-    const uint32_t* Ci = p.Cp + (size_t)i * p.q;  // lexicographic codeword order
-    const uint16_t* Di = p.Dp + (size_t)i * p.q;
-    f32x2 acc[MN];
-#pragma unroll
-    for (int e = 0; e < MN; e++) acc[e] = 0ull;
-    if (__any_sync(0xffffffffu, A.active || B.active)) {
-      typename Core::Lane lane;
-      Core::init(lane, A.active ? win_bits(wa, A.s) : 0ull, B.active ? win_bits(wb, B.s) : 0ull, p);
-      const float* pa = kPri ? p.priors + ((size_t)A.f * p.N + i) * p.q : nullptr;
-      const float* pb = kPri ? p.priors + ((size_t)B.f * p.N + i) * p.q : nullptr;
-#pragma unroll
-      for (int c = 0; c < 4 * MN; c++) s_acc[c * kLatticeThreads] = 0ull;
-      unsigned used = 0u;
-      f32x2 fh[MN];  // rows 1..KP of the current prefix
-      XPrefetch xs(Ci, 0, p.q);
-      uint32_t xprev = 0u;
-      for (int k = 0; k < p.q; k++) {
-        const uint32_t x = xs.take(k);
-        if (k == 0 || ((x ^ xprev) & ((1u << KP) - 1u)) != 0u)
-          Core::template run_head<KP, BSIDMAP_L1_GROUP>(lane, x, p, fh);
-        xprev = x;
-        f32x2 fo[MN];
-#pragma unroll
-        for (int e = 0; e < MN; e++) fo[e] = fh[e];
-        Core::template run_tail_to<KP, RL, BSIDMAP_L1_GROUP>(lane, x, p, fo);
-        const uint32_t c = (x >> sh) & 3u;
-        used |= 1u << c;
-        f32x2* a = s_acc + (size_t)c * MN * kLatticeThreads;
-        if constexpr (kPri) {  // P(D_i = D) of the two windows' frames
-          const int D = Di[k];
-          const f32x2 P = pk(__ldg(pa + D), __ldg(pb + D));
-#pragma unroll
-          for (int e = 0; e < MN; e++) a[e * kLatticeThreads] = ffma2(P, fo[e], a[e * kLatticeThreads]);
-        } else {  // uniform priors: the common factor 1/q is applied at the store
-#pragma unroll
-          for (int e = 0; e < MN; e++) a[e * kLatticeThreads] = fadd2(fo[e], a[e * kLatticeThreads]);
-        }
-      }
-#pragma unroll 1
-      for (int c = 0; c < 4; c++) {  // the last two rows once per class, on the class sums
-        if (!((used >> c) & 1u)) continue;
-        f32x2 f[MN];
-        const f32x2* a = s_acc + (size_t)c * MN * kLatticeThreads;
-#pragma unroll
-        for (int e = 0; e < MN; e++) f[e] = a[e * kLatticeThreads];
-        Core::template apply_last_rows<2>(lane, (uint32_t)c, p, f);
-#pragma unroll
-        for (int e = 0; e < MN; e++) acc[e] = fadd2(acc[e], f[e]);
-      }
-    }
-    const float sc = kPri ? 1.f : 1.f / p.q;
-    if (A.in) {
-      float* out = p.Gsum + ((size_t)A.f * p.N + i) * MN * p.Mtp + A.mi;
-#pragma unroll
-      for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, A, e) ? sc * lo_of(acc[e]) : 0.f;
-    }
-    if (B.in) {
-      float* out = p.Gsum + ((size_t)B.f * p.N + i) * MN * p.Mtp + B.mi;
-#pragma unroll
-      for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, B, e) ? sc * hi_of(acc[e]) : 0.f;
-    }
-  }
-}
-
 // Scalar-core version (one window per lane, flat geometry) for the register-heavy shapes.
 template <class Core, int K, bool kPri = true>
 __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_sum_cls(const DecodeParams p) {
@@ -792,12 +700,6 @@ template <class Core>
 CoreKernels make_core_kernels_x2_base(long nodes) {
   CoreKernels k{};
   k.gamma_sum = k_gamma_sum_x2_cls<Core, 2, false>;
-  k.gamma_sum_pre[0][0] = k_gamma_sum_x2_pre<Core, 2, false>;
-  k.gamma_sum_pre[0][1] = k_gamma_sum_x2_pre<Core, 2, true>;
-  k.gamma_sum_pre[1][0] = k_gamma_sum_x2_pre<Core, 3, false>;
-  k.gamma_sum_pre[1][1] = k_gamma_sum_x2_pre<Core, 3, true>;
-  k.gamma_sum_pre[2][0] = k_gamma_sum_x2_pre<Core, 4, false>;
-  k.gamma_sum_pre[2][1] = k_gamma_sum_x2_pre<Core, 4, true>;
   k.gamma_sum_k3 = k_gamma_sum_x2_cls<Core, 3, false>;
   k.gamma_sum_pri = k_gamma_sum_x2_cls<Core, 2, true>;
   k.gamma_sum_k3_pri = k_gamma_sum_x2_cls<Core, 3, true>;

@@ -302,21 +302,6 @@ def test_app_two_folded_rows(name, frames, monkeypatch):
     assert_parity(L2, st2, run_oracle(cfg, b))
 
 
-@pytest.mark.parametrize("name,frames,pri", [("C1", 9, False), ("C2", 7, False), ("C2", 5, True), ("C4", 2, False)])
-def test_pass1_prefix_sharing(name, frames, pri, monkeypatch):
-    """Pass 1 with prefix sharing and shared-memory suffix-class accumulators
-    (k_gamma_sum_x2_pre, BSIDMAP_L1_PRE) against the oracle and the class kernel."""
-    cfg = small_cfg(name, priors=pri)
-    b = bsidgen.make_batch(cfg, 8, frames)
-    monkeypatch.setenv("BSIDMAP_L1_PRE", "1")
-    _, L1, st1 = run_gpu(cfg, b, 3)
-    monkeypatch.setenv("BSIDMAP_L1_PRE", "0")
-    _, L0, st0 = run_gpu(cfg, b, 3)
-    np.testing.assert_array_equal(st1, st0)
-    np.testing.assert_allclose(L1, L0, rtol=2e-5, atol=1e-30)
-    assert_parity(L1, st1, run_oracle(cfg, b))
-
-
 def test_modes_agree_and_plan():
     cfg = small_cfg("C2")
     b = bsidgen.make_batch(cfg, 0, 16)

@@ -23,13 +23,20 @@ for t in range(count):
         n = int(rng.integers(2, 13))
         q = int(rng.integers(2, min(64, 2 ** n) + 1))
         mn = None
-    N = int(rng.integers(1, 12))
+    N = int(rng.integers(1, 40))
     p = float(rng.choice([0.005, 0.02, 0.06]))
     cfg = bsidgen.Config(f"S{t}", q=q, n=n, N=N, Pi=p * float(rng.uniform(0.3, 1.7)), Pd=p * float(rng.uniform(0.3, 1.7)),
                          Ps=float(rng.choice([0.0, 0.01, 0.05])), frames=0, priors=bool(rng.random() < 0.4), mn=mn,
                          seed=7000 + t)
     if mn is not None:
         cfg.mt = (min(cfg.mn[0], cfg.mt[0]), max(cfg.mn[1], cfg.mt[1]))
+    if rng.random() < 0.4:  # wide trellis: multi-tile APP, CTA alpha/beta, CTA local schedule
+        w = int(rng.choice([40, 90, 200, 400]))
+        cfg.mt = (min(cfg.mn[0], -w), max(cfg.mn[1], w + int(rng.integers(0, 9))))
+    if rng.random() < 0.1:
+        cfg.Pd = 0.0  # no deletions: the non-rescaled generic lattice
+    if rng.random() < 0.1:
+        cfg.Pi = 0.0
     F = int(rng.integers(1, 70))
     b = bsidgen.make_batch(cfg, int(rng.integers(0, 1000)), F)
     res = run_oracle(cfg, b)
