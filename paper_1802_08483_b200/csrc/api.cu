@@ -209,6 +209,10 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   if (chunk < 1) return fail(d, BSIDMAP_ENOMEM, "workspace for one frame (" + std::to_string(per) +
                                                     " B) exceeds the budget (" + std::to_string(bud) + " B)");
   chunk = std::min<long>(chunk, F);
+  {  // equal chunks (a short tail chunk would leave the GPU half idle)
+    const long nch = (F + chunk - 1) / chunk;
+    chunk = (F + nch - 1) / nch;
+  }
   P->mode = mode;
   P->chunk = (int)chunk;
   P->nchunks = (int)((F + chunk - 1) / chunk);
