@@ -113,3 +113,20 @@ def test_odd_alphabet_local_schedule(shape, q):
         d, L, st = run_gpu(cfg, b, mode)
         assert_parity(L, st, res)
     assert d.plan(24)["core"] == "spec"
+
+
+def test_chunked_overlapped_c5_shape_bit_identical():
+    """C5's shape (scalar core, CTA alpha/beta, priors) decoded in one call and in chunks of two frames
+    (each chunk's alpha/beta on the side stream, two sub-batches of one frame): identical L."""
+    full = bsidgen.configs()["C5"]
+    cfg = bsidgen.Config("C5c", q=full.q, n=full.n, N=150, Pi=full.Pi, Pd=full.Pd, Ps=full.Ps, frames=0,
+                         priors=True, mn=full.mn, mt=full.mt, seed=full.seed)
+    b = bsidgen.make_batch(cfg, 0, 6)
+    d1, L1, st1 = run_gpu(cfg, b, 0)
+    assert d1.plan(6)["alpha_beta_overlap_subbatches"] == 2
+    per = d1.workspace_bytes(1, 0)
+    d2, L2, st2 = run_gpu(cfg, b, 0, ws_limit=2 * per + 1024)
+    assert d2.plan(6)["chunks"] == 3
+    np.testing.assert_array_equal(st2, st1)
+    np.testing.assert_array_equal(L2, L1)
+    assert (st1 == 0).all()
