@@ -42,7 +42,13 @@ for t in range(count):
     res = run_oracle(cfg, b)
     for mode in (0, 1, 2, 3):
         try:
-            d, L, st = run_gpu(cfg, b, mode)
+            ws = None
+            if rng.random() < 0.3 and F > 2:  # force chunking of the batch
+                from paper_1802_08483_b200 import Decoder
+                probe = Decoder.from_config(cfg, b.C, mode=mode, device=0)
+                ws = probe.workspace_bytes(1, mode) * int(rng.integers(1, F)) + 4096
+                del probe
+            d, L, st = run_gpu(cfg, b, mode, ws_limit=ws)
             assert_parity(L, st, res)
         except Exception as e:  # report and continue
             fails += 1
