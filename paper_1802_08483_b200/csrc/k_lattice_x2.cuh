@@ -66,6 +66,11 @@ __device__ __forceinline__ int exp2_of(double x) {  // floor(log2 x) for normal 
 #ifndef BSIDMAP_L1_MINB
 #define BSIDMAP_L1_MINB Core::kMinBlocks
 #endif
+// the class-ordered pass 1 at one more CTA/SM where 3 fit (128 registers, ~140 B of spills outside
+// the row loop; tools/exp_minb.sh: C2 pass 1 52.98 -> 50.79 ms, C1 shape 0.205 -> 0.192 ms)
+#ifndef BSIDMAP_L1C_MINB
+#define BSIDMAP_L1C_MINB (Core::kMinBlocks > 2 ? 4 : Core::kMinBlocks)
+#endif
 // row pairs (ILP) in pass 1 only where the register budget allows 3 CTAs/SM
 #ifndef BSIDMAP_L1_GROUP
 #define BSIDMAP_L1_GROUP (Core::kMinBlocks > 2 ? 2 : 1)
@@ -162,7 +167,7 @@ __device__ __forceinline__ LaneGeom geom_step(const DecodeParams& p, const WinBa
 }
 
 template <class Core, int K, bool kPri = true>
-__global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_x2_cls(const DecodeParams p) {
+__global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1C_MINB) k_gamma_sum_x2_cls(const DecodeParams p) {
   constexpr int MN = Core::Mn;
   constexpr int NC = 1 << K;
   extern __shared__ __align__(128) unsigned char smem[];
