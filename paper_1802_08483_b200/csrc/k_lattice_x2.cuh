@@ -394,6 +394,11 @@ __host__ __device__ __forceinline__ int app_prefix_bits(int q, int n) {
 // KS = lattice rows folded into the APP weights: 1 = the last row (two tables, by x_n); 2 = the
 // last two rows (four tables, by (x_{n-1}, x_n); row n-1 transposed by SpecCoreX2::row_transpose),
 // so each symbol runs rows 1..n-2 only.  Exact re-association (the rows are linear maps).
+// the weight dot inside the basic block of the last lattice row (rows_then), so it interleaves
+// with the row's insertion chain instead of running as a dependent tail after the branch merge
+#ifndef BSIDMAP_APP_FUSED_DOT
+#define BSIDMAP_APP_FUSED_DOT 1
+#endif
 #ifndef BSIDMAP_APP_MINB_KS2
 #define BSIDMAP_APP_MINB_KS2 (Core::kMinBlocks > 2 ? 3 : 2)
 #endif
@@ -478,24 +483,36 @@ __global__ void __launch_bounds__(kLatticeThreads, KS == 2 ? BSIDMAP_APP_MINB_KS
     for (int k = 0; k < p.q; k++) {
       const uint32_t x = xs.take(k);
       f32x2 fo[MN];
+      // t(m', D) = sum_k G_n(m', k, D) bt(m', k) = sum_e G_{n-KS}[e] w[e]  (two chains)
+      const f32x2* W = KS == 1 ? wt + (((x >> nb) & 1u) ? 0 : MN * 32)
+                               : wt + (size_t)((((x >> nb) & 1u) ? 0 : 2) + (((x >> (nb - 1)) & 1u) ? 0 : 1)) * MN * 32;
+      f32x2 t0 = 0ull, t1 = 0ull;
+      auto dot = [&](const f32x2 (&g)[MN]) {
+#pragma unroll
+        for (int e = 0; e < MN; e += 2) {
+          t0 = ffma2(g[e], W[e * 32], t0);
+          if (e + 1 < MN) t1 = ffma2(g[e + 1], W[(e + 1) * 32], t1);
+        }
+      };
       if constexpr (KP > 0) {
         if (k == 0 || ((x ^ xprev) & ((1u << KP) - 1u)) != 0u)
           Core::template run_head<KP, BSIDMAP_APP_GROUP>(lane_t, x, p, fh);
         xprev = x;
 #pragma unroll
         for (int e = 0; e < MN; e++) fo[e] = fh[e];
+#if BSIDMAP_APP_FUSED_DOT
+        Core::template run_tail_to_then<KP, RL, BSIDMAP_APP_GROUP>(lane_t, x, p, fo, dot);
+#else
         Core::template run_tail_to<KP, RL, BSIDMAP_APP_GROUP>(lane_t, x, p, fo);
+        dot(fo);
+#endif
       } else {
+#if BSIDMAP_APP_FUSED_DOT
+        Core::template run_to_then<RL, BSIDMAP_APP_GROUP>(lane_t, x, p, fo, dot);
+#else
         Core::template run_to<RL, BSIDMAP_APP_GROUP>(lane_t, x, p, fo);
-      }
-      // t(m', D) = sum_k G_n(m', k, D) bt(m', k) = sum_e G_{n-KS}[e] w[e]  (two chains)
-      const f32x2* W = KS == 1 ? wt + (((x >> nb) & 1u) ? 0 : MN * 32)
-                               : wt + (size_t)((((x >> nb) & 1u) ? 0 : 2) + (((x >> (nb - 1)) & 1u) ? 0 : 1)) * MN * 32;
-      f32x2 t0 = 0ull, t1 = 0ull;
-#pragma unroll
-      for (int e = 0; e < MN; e += 2) {
-        t0 = ffma2(fo[e], W[e * 32], t0);
-        if (e + 1 < MN) t1 = ffma2(fo[e + 1], W[(e + 1) * 32], t1);
+        dot(fo);
+#endif
       }
       const int D = KP > 0 ? (int)Di[k] : k;
       stg[D * 33 + lane] = fmaf(wa, lo_of(t0) + lo_of(t1), wb * (hi_of(t0) + hi_of(t1)));
@@ -603,23 +620,31 @@ __global__ void __launch_bounds__(kLatticeThreads, (KP > 0 || KS == 2) ? BSIDMAP
       const uint32_t x = xs.take(k);
       const int D = KP > 0 ? (int)Di[k] : k;
       float fo[MN];
+      float t0 = 0.f, t1 = 0.f;
+      // KS = 2: the table dot fused into the last row's basic block (rows_then); KS = 1: after it
+      const float* W = s_w + (size_t)((((x >> nb) & 1u) ? 0 : 2) + (((x >> (nb - 1)) & 1u) ? 0 : 1)) * MN * kLatticeThreads;
+      auto dot = [&](const float (&g)[MN]) {
+        if constexpr (KS == 2) {
+#pragma unroll
+          for (int e = 0; e < MN; e += 2) {
+            t0 = fmaf(g[e], W[e * kLatticeThreads], t0);
+            if (e + 1 < MN) t1 = fmaf(g[e + 1], W[(e + 1) * kLatticeThreads], t1);
+          }
+        }
+      };
       if constexpr (KP > 0) {
         if (k == 0 || ((x ^ xprev) & ((1u << KP) - 1u)) != 0u) Core::template run_head<KP>(lane_t, x, p, fh);
         xprev = x;
 #pragma unroll
         for (int e = 0; e < MN; e++) fo[e] = fh[e];
-        Core::template run_tail_to<KP, RL>(lane_t, x, p, fo);
+        if constexpr (KS == 2 && BSIDMAP_APP_FUSED_DOT) Core::template run_tail_to_then<KP, RL>(lane_t, x, p, fo, dot);
+        else Core::template run_tail_to<KP, RL>(lane_t, x, p, fo);
       } else {
-        Core::template run_to<RL>(lane_t, x, p, fo);
+        if constexpr (KS == 2 && BSIDMAP_APP_FUSED_DOT) Core::template run_to_then<RL>(lane_t, x, p, fo, dot);
+        else Core::template run_to<RL>(lane_t, x, p, fo);
       }
-      float t0 = 0.f, t1 = 0.f;
       if constexpr (KS == 2) {
-        const float* W = s_w + (size_t)((((x >> nb) & 1u) ? 0 : 2) + (((x >> (nb - 1)) & 1u) ? 0 : 1)) * MN * kLatticeThreads;
-#pragma unroll
-        for (int e = 0; e < MN; e += 2) {
-          t0 = fmaf(fo[e], W[e * kLatticeThreads], t0);
-          if (e + 1 < MN) t1 = fmaf(fo[e + 1], W[(e + 1) * kLatticeThreads], t1);
-        }
+        if constexpr (!BSIDMAP_APP_FUSED_DOT) dot(fo);
       } else if ((x >> nb) & 1u) {
 #pragma unroll
         for (int e = 0; e < MN; e += 2) {

@@ -114,6 +114,34 @@ struct SpecCore {
     }
   }
 
+  // rows<R, RLAST> then tail(f) inside the basic block of the last row (SpecCoreX2::rows_then)
+  template <int R, int RLAST, class Tail, int G = BSIDMAP_SCALAR_GROUP>
+  __device__ __forceinline__ static void rows_then(float (&f)[MN], uint32_t x, const Lane& L, const LatticeConst& lc,
+                                                   Tail& tail) {
+    if constexpr (R > RLAST) {
+      tail(f);
+    } else if constexpr (G >= 2 && R + 1 <= RLAST) {
+      constexpr bool kEnd = (R + 1 == RLAST);
+      switch ((x >> (R - 1)) & 3u) {
+        case 0u: row<R, true>(f, L.q0, lc); row<R + 1, true>(f, L.q0, lc); if constexpr (kEnd) tail(f); break;
+        case 1u: row<R, true>(f, L.q1, lc); row<R + 1, true>(f, L.q0, lc); if constexpr (kEnd) tail(f); break;
+        case 2u: row<R, true>(f, L.q0, lc); row<R + 1, true>(f, L.q1, lc); if constexpr (kEnd) tail(f); break;
+        default: row<R, true>(f, L.q1, lc); row<R + 1, true>(f, L.q1, lc); if constexpr (kEnd) tail(f); break;
+      }
+      if constexpr (!kEnd) rows_then<R + 2, RLAST, Tail, G>(f, x, L, lc, tail);
+    } else {
+      constexpr bool kEnd = (R == RLAST);
+      if ((x >> (R - 1)) & 1u) {
+        row<R, true>(f, L.q1, lc);
+        if constexpr (kEnd) tail(f);
+      } else {
+        row<R, true>(f, L.q0, lc);
+        if constexpr (kEnd) tail(f);
+      }
+      if constexpr (!kEnd) rows_then<R + 1, RLAST, Tail, G>(f, x, L, lc, tail);
+    }
+  }
+
   // Rows 1..n-K and the last K rows for a class (see SpecCoreX2::run_prefix / apply_last_rows).
   template <int K>
   __device__ __forceinline__ static void run_prefix(const Lane& L, uint32_t x, const DecodeParams& p, float (&f)[MN]) {
@@ -150,6 +178,18 @@ struct SpecCore {
   template <int KP, int RL>
   __device__ __forceinline__ static void run_tail_to(const Lane& L, uint32_t x, const DecodeParams& p, float (&f)[MN]) {
     if constexpr (KP + 1 <= RL) rows<KP + 1, RL>(f, x, L, p.lc);
+  }
+  template <int RL, class Tail>
+  __device__ __forceinline__ static void run_to_then(const Lane& L, uint32_t x, const DecodeParams& p, float (&f)[MN],
+                                                     Tail& tail) {
+#pragma unroll
+    for (int e = 0; e < MN; e++) f[e] = p.lc.row0[e];
+    rows_then<1, RL>(f, x, L, p.lc, tail);
+  }
+  template <int KP, int RL, class Tail>
+  __device__ __forceinline__ static void run_tail_to_then(const Lane& L, uint32_t x, const DecodeParams& p,
+                                                          float (&f)[MN], Tail& tail) {
+    rows_then<KP + 1, RL>(f, x, L, p.lc, tail);
   }
   // Transpose of lattice row R < n (SpecCoreX2::row_transpose): weights on G_R -> weights on G_{R-1}.
   template <int R>

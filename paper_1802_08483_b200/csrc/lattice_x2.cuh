@@ -158,8 +158,37 @@ struct SpecCoreX2 {
     rows<NN - K + 1, false, NN>(f, cls << (NN - K), L, pk(p.lc.a, p.lc.a));
   }
 
+  // rows<R, G, RLAST> followed by tail(f), with the tail placed inside each branch of the group
+  // that ends at row RLAST: the consumer of the last row (the APP's weight dot) shares that basic
+  // block with the row's insertion chain, so the two interleave (G <= 2).
+  template <int R, int G, int RLAST, class Tail>
+  __device__ __forceinline__ static void rows_then(f32x2 (&f)[MN], uint32_t x, const Lane& L, f32x2 a2, Tail& tail) {
+    if constexpr (R > RLAST) {
+      tail(f);
+    } else if constexpr (G >= 2 && R + 1 <= RLAST) {
+      constexpr bool kEnd = (R + 1 == RLAST);
+      switch ((x >> (R - 1)) & 3u) {
+        case 0u: row<R>(f, L.q0, a2); row<R + 1>(f, L.q0, a2); if constexpr (kEnd) tail(f); break;
+        case 1u: row<R>(f, L.q1, a2); row<R + 1>(f, L.q0, a2); if constexpr (kEnd) tail(f); break;
+        case 2u: row<R>(f, L.q0, a2); row<R + 1>(f, L.q1, a2); if constexpr (kEnd) tail(f); break;
+        default: row<R>(f, L.q1, a2); row<R + 1>(f, L.q1, a2); if constexpr (kEnd) tail(f); break;
+      }
+      if constexpr (!kEnd) rows_then<R + 2, G, RLAST>(f, x, L, a2, tail);
+    } else {
+      constexpr bool kEnd = (R == RLAST);
+      if ((x >> (R - 1)) & 1u) {
+        row<R>(f, L.q1, a2);
+        if constexpr (kEnd) tail(f);
+      } else {
+        row<R>(f, L.q0, a2);
+        if constexpr (kEnd) tail(f);
+      }
+      if constexpr (!kEnd) rows_then<R + 1, G, RLAST>(f, x, L, a2, tail);
+    }
+  }
+
   // Rows 1..RL, and rows KP+1..RL after a shared head (the APP pass with the last n - RL rows
-  // folded into its weights).
+  // folded into its weights); the *_then forms end with tail(f) (rows_then).
   template <int RL, int G = 1>
   __device__ __forceinline__ static void run_to(const Lane& L, uint32_t x, const DecodeParams& p, f32x2 (&f)[MN]) {
 #pragma unroll
@@ -170,6 +199,18 @@ struct SpecCoreX2 {
   __device__ __forceinline__ static void run_tail_to(const Lane& L, uint32_t x, const DecodeParams& p,
                                                      f32x2 (&f)[MN]) {
     rows<KP + 1, G, RL>(f, x, L, pk(p.lc.a, p.lc.a));
+  }
+  template <int RL, int G, class Tail>
+  __device__ __forceinline__ static void run_to_then(const Lane& L, uint32_t x, const DecodeParams& p, f32x2 (&f)[MN],
+                                                     Tail& tail) {
+#pragma unroll
+    for (int e = 0; e < MN; e++) f[e] = pk(p.lc.row0[e], p.lc.row0[e]);
+    rows_then<1, G, RL>(f, x, L, pk(p.lc.a, p.lc.a), tail);
+  }
+  template <int KP, int RL, int G, class Tail>
+  __device__ __forceinline__ static void run_tail_to_then(const Lane& L, uint32_t x, const DecodeParams& p,
+                                                          f32x2 (&f)[MN], Tail& tail) {
+    rows_then<KP + 1, G, RL>(f, x, L, pk(p.lc.a, p.lc.a), tail);
   }
 
   // Transpose of lattice row R (R < n) with Q-dot table Q: weights w on the row's outputs G_R ->
