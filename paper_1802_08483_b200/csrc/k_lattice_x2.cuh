@@ -68,6 +68,9 @@ __device__ __forceinline__ int exp2_of(double x) {  // floor(log2 x) for normal 
 #endif
 // the class-ordered pass 1 at one more CTA/SM where 3 fit (128 registers, ~140 B of spills outside
 // the row loop; tools/exp_minb.sh: C2 pass 1 52.98 -> 50.79 ms, C1 shape 0.205 -> 0.192 ms)
+#ifndef BSIDMAP_L1_FUSED_ADD
+#define BSIDMAP_L1_FUSED_ADD 1
+#endif
 #ifndef BSIDMAP_L1C_MINB
 #define BSIDMAP_L1C_MINB (Core::kMinBlocks > 2 ? 4 : Core::kMinBlocks)
 #endif
@@ -215,16 +218,21 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1C_MINB) k_gamma_sum
           cur = c;
         }
         f32x2 fo[MN];
-        Core::template run_prefix<K, BSIDMAP_L1_GROUP>(lane, x, p, fo);
+        f32x2 P = 0ull;
         if constexpr (kPri) {  // P(D_i = D) of the two windows' frames
           const int D = Di[k];
-          const f32x2 P = pk(__ldg(pa + D), __ldg(pb + D));
-#pragma unroll
-          for (int e = 0; e < MN; e++) acc[e] = ffma2(P, fo[e], acc[e]);
-        } else {  // uniform priors: the common factor 1/q is applied at the store
-#pragma unroll
-          for (int e = 0; e < MN; e++) acc[e] = fadd2(fo[e], acc[e]);
+          P = pk(__ldg(pa + D), __ldg(pb + D));
         }
+        auto add = [&](const f32x2 (&g)[MN]) {
+#pragma unroll
+          for (int e = 0; e < MN; e++) acc[e] = kPri ? ffma2(P, g[e], acc[e]) : fadd2(g[e], acc[e]);
+        };
+#if BSIDMAP_L1_FUSED_ADD  // the class-sum update inside the last row group's basic block (rows_then)
+        Core::template run_prefix_then<K, BSIDMAP_L1_GROUP>(lane, x, p, fo, add);
+#else
+        Core::template run_prefix<K, BSIDMAP_L1_GROUP>(lane, x, p, fo);
+        add(fo);  // uniform priors: the common factor 1/q is applied at the store
+#endif
       }
       Core::template apply_last_rows<K>(lane, cur, p, acc);
       if (!first) {

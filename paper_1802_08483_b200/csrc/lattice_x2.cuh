@@ -152,6 +152,13 @@ struct SpecCoreX2 {
     for (int e = 0; e < MN; e++) f[e] = pk(p.lc.row0[e], p.lc.row0[e]);
     rows<1, G, NN - K>(f, x, L, pk(p.lc.a, p.lc.a));
   }
+  template <int K, int G, class Tail>
+  __device__ __forceinline__ static void run_prefix_then(const Lane& L, uint32_t x, const DecodeParams& p,
+                                                         f32x2 (&f)[MN], Tail& tail) {
+#pragma unroll
+    for (int e = 0; e < MN; e++) f[e] = pk(p.lc.row0[e], p.lc.row0[e]);
+    rows_then<1, G, NN - K>(f, x, L, pk(p.lc.a, p.lc.a), tail);
+  }
   template <int K>
   __device__ __forceinline__ static void apply_last_rows(const Lane& L, uint32_t cls, const DecodeParams& p,
                                                          f32x2 (&f)[MN]) {
