@@ -82,6 +82,8 @@ typedef struct bsidmap_decoder bsidmap_decoder; /* opaque; owns the device codeb
  *   BSIDMAP_APP_KP=k   APP prefix-sharing length (0 = off; default ~log2(q) - 1)
  *   BSIDMAP_APP_KS=k   lattice rows folded into the APP weights (1 or 2; default 2 for register-heavy shapes)
  *   BSIDMAP_APP_X4=1   four-window APP kernel (small corridors; default off)
+ *   BSIDMAP_PASS_SMEM_MIN=b  floor (bytes) on the lattice passes' dynamic shared memory, i.e. an
+ *                      occupancy cap leaving room for co-resident alpha/beta blocks (default 0)
  */
 int bsidmap_create(bsidmap_decoder **out, int q, int n, int N, const uint32_t *codebook_host,
                    double Pi, double Pd, double Ps, int mn_lo, int mn_hi, int mt_lo, int mt_hi,

@@ -87,6 +87,7 @@ struct bsidmap_decoder {
   // alpha/beta overlap: sub-batch k's alpha/beta recursions run on a high-priority side
   // stream while the lattice passes of the other sub-batches run on the decode stream
   int ab_sub = 0;                       // sub-batches per chunk (0 = automatic, 1 = no overlap)
+  size_t pass_smem_min = 0;             // floor on the lattice passes' dynamic smem (occupancy cap)
   int num_sms = 148;
   int app_kp = -1;                      // pass-2 prefix length override (-1 = automatic)
   int app_x4 = -1;                      // four-window APP kernel (-1 = automatic, 0 = off)
@@ -290,6 +291,10 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   P->l1_smem = (d->kern.gamma_sum_k3 && mode != kSchedStored)
                    ? (size_t)d->Mn * kLatticeThreads * 8 + (size_t)d->q * 6 + 64 + 16
                    : (size_t)d->q * 4;
+  if (d->pass_smem_min) {  // leave room for co-resident alpha/beta blocks (experiment)
+    P->l1_smem = std::max(P->l1_smem, d->pass_smem_min);
+    P->app_smem = std::max(P->app_smem, d->pass_smem_min);
+  }
   return BSIDMAP_OK;
 }
 
@@ -630,6 +635,7 @@ int bsidmap_create(bsidmap_decoder** out, int q, int n, int N, const uint32_t* c
   d->Pi = Pi; d->Pd = Pd; d->Ps = Ps;
   d->mode = mode;
   if (const char* v = std::getenv("BSIDMAP_AB_SUB")) d->ab_sub = std::max(1, std::atoi(v));
+  if (const char* v = std::getenv("BSIDMAP_PASS_SMEM_MIN")) d->pass_smem_min = (size_t)std::max(0, std::atoi(v));
   if (const char* v = std::getenv("BSIDMAP_APP_KP")) d->app_kp = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("BSIDMAP_APP_X4")) d->app_x4 = std::atoi(v);
   if (const char* v = std::getenv("BSIDMAP_APP_KS")) d->app_ks = std::atoi(v) == 2 ? 2 : 1;

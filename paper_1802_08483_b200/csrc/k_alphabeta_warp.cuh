@@ -17,12 +17,21 @@
 
 namespace bsidmap {
 
-constexpr int kAbWarpThreads = 128;  // 4 (frame, direction) tasks per CTA
-constexpr int kAbStages = 4;
+#ifndef BSIDMAP_AB_WARP_THREADS
+#define BSIDMAP_AB_WARP_THREADS 64
+#endif
+// 2 (frame, direction) tasks per CTA: finer-grained residency than 4 (C2: 9.38 -> 8.80 ms;
+// 1 per CTA 15.8 ms; tools/exp_abw.sh)
+constexpr int kAbWarpThreads = BSIDMAP_AB_WARP_THREADS;
+#ifndef BSIDMAP_AB_STAGES
+#define BSIDMAP_AB_STAGES 4
+#endif
+constexpr int kAbStages = BSIDMAP_AB_STAGES;
 
 // shared memory per warp: row[SPT*32] doubles | ring[kStages][MN][Mtp] floats | bars[kStages]
 __host__ __device__ __forceinline__ size_t ab_warp_smem(int SPT, int MN, int Mtp) {
-  return (size_t)SPT * 32 * 8 + (size_t)kAbStages * MN * Mtp * 4 + kAbStages * 8;
+  // rounded to 16 bytes: the next warp's TMA ring must stay 16-byte aligned
+  return ((size_t)SPT * 32 * 8 + (size_t)kAbStages * MN * Mtp * 4 + kAbStages * 8 + 15) & ~(size_t)15;
 }
 
 template <int SPT, int MN>
