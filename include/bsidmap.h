@@ -82,6 +82,8 @@ typedef struct bsidmap_decoder bsidmap_decoder; /* opaque; owns the device codeb
  *   BSIDMAP_APP_KP=k   APP prefix-sharing length (0 = off; default ~log2(q) - 1)
  *   BSIDMAP_APP_KS=k   lattice rows folded into the APP weights (1 or 2; default 2 for register-heavy shapes)
  *   BSIDMAP_APP_X4=1   four-window APP kernel (small corridors; default off)
+ *   BSIDMAP_AB_CTA_STAGES=k, BSIDMAP_AB_CTA_THREADS=t  ring depth / block size of the CTA alpha/beta
+ *                      kernel (M_tau > 128; defaults: 1 stage when 2F >= 4 #SMs, ~M_tau/2 threads)
  *   BSIDMAP_PASS_SMEM_MIN=b  floor (bytes) on the lattice passes' dynamic shared memory, i.e. an
  *                      occupancy cap leaving room for co-resident alpha/beta blocks (default 0)
  */

@@ -88,6 +88,7 @@ struct bsidmap_decoder {
   // stream while the lattice passes of the other sub-batches run on the decode stream
   int ab_sub = 0;                       // sub-batches per chunk (0 = automatic, 1 = no overlap)
   size_t pass_smem_min = 0;             // floor on the lattice passes' dynamic smem (occupancy cap)
+  int ab_stages = 0, ab_threads = 0;    // CTA alpha/beta ring depth and block size (0 = automatic)
   int num_sms = 148;
   int app_kp = -1;                      // pass-2 prefix length override (-1 = automatic)
   int app_x4 = -1;                      // four-window APP kernel (-1 = automatic, 0 = off)
@@ -217,11 +218,18 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   P->mode = mode;
   P->chunk = (int)chunk;
   P->nchunks = (int)((F + chunk - 1) / chunk);
-  P->ab_threads = std::min(1024, ((d->Mt + 31) / 32) * 32);
+  // CTA alpha/beta: ~2 states per thread (smaller blocks, more of them resident per SM), and a
+  // single-stage Gamma ring when the grid has several CTAs per SM -- the other resident CTAs hide
+  // each one's copy latency (C3: 11.7 -> 7.7 ms, C4: 14.6 -> 11.9 ms; tools/exp_abcta*.sh).  The
+  // block size depends on M_tau only, so chunking does not change the arithmetic.
+  P->ab_threads = std::min(1024, std::max(64, ((d->Mt + 1) / 2 + 31) / 32 * 32));
   {  // TMA ring depth: up to 4 stages of Gamma_i blocks within ~200 KB of shared memory
     const int Mtp = (d->Mt + 3) & ~3;
     const size_t blk = (size_t)d->Mn * Mtp * 4;
     P->ab_stages = (int)std::max<size_t>(1, std::min<size_t>(4, (200u * 1024 - 2 * (size_t)Mtp * 8 - 600) / blk));
+    if (2L * chunk >= 4L * d->num_sms) P->ab_stages = 1;
+    if (d->ab_stages > 0) P->ab_stages = d->ab_stages;
+    if (d->ab_threads > 0) P->ab_threads = std::min(1024, d->ab_threads);
     P->ab_smem = ab_cta_smem(d->Mn, Mtp, P->ab_stages);
     if (mode != kSchedLocal && mode != kSchedLocalCta && P->ab_smem > 227u * 1024)
       return fail(d, BSIDMAP_EPLAN, "M_n x M_tau too large for the shared-memory Gamma ring of the alpha/beta kernel");
@@ -635,6 +643,8 @@ int bsidmap_create(bsidmap_decoder** out, int q, int n, int N, const uint32_t* c
   d->Pi = Pi; d->Pd = Pd; d->Ps = Ps;
   d->mode = mode;
   if (const char* v = std::getenv("BSIDMAP_AB_SUB")) d->ab_sub = std::max(1, std::atoi(v));
+  if (const char* v = std::getenv("BSIDMAP_AB_CTA_STAGES")) d->ab_stages = std::max(0, std::atoi(v));
+  if (const char* v = std::getenv("BSIDMAP_AB_CTA_THREADS")) d->ab_threads = std::max(0, std::atoi(v)) & ~31;
   if (const char* v = std::getenv("BSIDMAP_PASS_SMEM_MIN")) d->pass_smem_min = (size_t)std::max(0, std::atoi(v));
   if (const char* v = std::getenv("BSIDMAP_APP_KP")) d->app_kp = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("BSIDMAP_APP_X4")) d->app_x4 = std::atoi(v);
