@@ -23,8 +23,9 @@ namespace bsidmap {
 // 2 (frame, direction) tasks per CTA: finer-grained residency than 4 (C2: 9.38 -> 8.80 ms;
 // 1 per CTA 15.8 ms; tools/exp_abw.sh)
 constexpr int kAbWarpThreads = BSIDMAP_AB_WARP_THREADS;
+// TMA ring depth per warp (C2: 2 stages 8.48 ms, 3: 8.35, 4: 8.80, 5: 8.87, 8: 14.1; tools/exp_abw2.sh)
 #ifndef BSIDMAP_AB_STAGES
-#define BSIDMAP_AB_STAGES 4
+#define BSIDMAP_AB_STAGES 3
 #endif
 constexpr int kAbStages = BSIDMAP_AB_STAGES;
 
