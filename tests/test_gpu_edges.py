@@ -130,3 +130,23 @@ def test_chunked_overlapped_c5_shape_bit_identical():
     np.testing.assert_array_equal(st2, st1)
     np.testing.assert_array_equal(L2, L1)
     assert (st1 == 0).all()
+
+
+def test_cta_alpha_beta_ring_depth_bit_identical():
+    """C4's shape (M_tau = 611: the CTA alpha/beta kernel, ~M_tau/2 threads): 640 frames in one call
+    (grid of 1280 CTAs >= 4 per SM: single-stage Gamma ring) and in chunks of 64 frames (deep ring)
+    give identical L; the first frames match the oracle."""
+    full = bsidgen.configs()["C4"]
+    cfg = bsidgen.Config("C4r", q=full.q, n=full.n, N=12, Pi=full.Pi, Pd=full.Pd, Ps=full.Ps, frames=0,
+                         mn=full.mn, mt=full.mt, seed=full.seed)
+    F = 640
+    b = bsidgen.make_batch(cfg, 0, F)
+    d1, L1, st1 = run_gpu(cfg, b, 0)
+    plan = d1.plan(F)
+    assert plan["chunks"] == 1 and plan["alpha_beta_block"] == 320
+    per = d1.workspace_bytes(1, 0)
+    d2, L2, st2 = run_gpu(cfg, b, 0, ws_limit=64 * per + 1024)
+    assert d2.plan(F)["chunks"] == 10
+    np.testing.assert_array_equal(st2, st1)
+    np.testing.assert_array_equal(L2, L1)
+    assert_parity(L1, st1, run_oracle(cfg, b, frames=[0, 1]), frames=[0, 1])
