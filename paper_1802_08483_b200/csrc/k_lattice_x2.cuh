@@ -71,8 +71,18 @@ __device__ __forceinline__ int exp2_of(double x) {  // floor(log2 x) for normal 
 #ifndef BSIDMAP_L1_FUSED_ADD
 #define BSIDMAP_L1_FUSED_ADD 1
 #endif
+// and at 3 (168 registers, ~100 B of spills) for the 2-CTA shapes with M_n <= BSIDMAP_SCALAR_MN_MAX
+// (whose APP runs on the scalar core): C3 pass 1 67.7 -> 62.2 ms, C5 226.1 -> 199.7 ms against the
+// scalar class kernel; C4 (M_n = 26) stays at 2 (71.9 vs 76.9 ms at 3) -- tools/exp_p1x2*.sh
+#ifndef BSIDMAP_SCALAR_MN_MAX
+#define BSIDMAP_SCALAR_MN_MAX 20
+#endif
+#ifndef BSIDMAP_L1C_MINB_LOW
+#define BSIDMAP_L1C_MINB_LOW 3
+#endif
 #ifndef BSIDMAP_L1C_MINB
-#define BSIDMAP_L1C_MINB (Core::kMinBlocks > 2 ? 4 : Core::kMinBlocks)
+#define BSIDMAP_L1C_MINB \
+  (Core::kMinBlocks > 2 ? 4 : (Core::Mn <= BSIDMAP_SCALAR_MN_MAX ? BSIDMAP_L1C_MINB_LOW : Core::kMinBlocks))
 #endif
 // row pairs (ILP) in pass 1 only where the register budget allows 3 CTAs/SM
 #ifndef BSIDMAP_L1_GROUP
