@@ -21,7 +21,7 @@ $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
 
 oracle/libbsid_oracle.so: oracle/bsid_oracle.c
-	gcc -O2 -std=c11 -fPIC -shared -fno-fast-math -ffp-contract=off -o $@ $< -lm
+	gcc -O2 -std=c11 -fPIC -shared -fno-fast-math -ffp-contract=off -fopenmp -o $@ $< -lm
 
 bsidgen/libbsidgen.so: bsidgen/bsidgen.c
 	gcc -O2 -std=c11 -fPIC -shared -o $@ $< -lm

@@ -48,7 +48,20 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the oracle sample")
+    ap.add_argument("--N", type=int, default=None,
+                    help="symbols per frame (default: the config's); keeps the config's code, channel and "
+                         "drift limits -- a reduced-length test workload, not a bench line")
+    ap.add_argument("--ws-limit-gb", type=float, default=None, help="cap the decoder workspace (chunking)")
+    ap.add_argument("--dump", default=None, help="directory: each rank writes its L/status/frame range")
     return ap.parse_args()
+
+
+def workload(args):
+    import dataclasses
+    cfg = bsidgen.configs()[args.config]
+    if args.N is not None and args.N != cfg.N:
+        cfg = dataclasses.replace(cfg, N=args.N, name=f"{cfg.name}@N{args.N}")
+    return cfg
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -114,66 +127,68 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- oracle leg
 
-ORACLE_FRAME_SECONDS = 4.0  # target single-core oracle time of one sampled frame
-
-
-def oracle_workload(cfg):
-    """(config the oracle is timed on, frames/s scale to the full config).  A full C4/C5 frame takes
-    the FP64 oracle minutes to an hour on one core, so long frames are timed as frames of the same
-    code, channel, corridor and trellis with fewer symbol positions N_s (every oracle step costs the
-    same: ~2 passes x M_tau q lattices x corridor cells), and the rate is scaled by N_s / N."""
+def oracle_frame_seconds(cfg):
+    """Rough single-core oracle time of one full frame: 2 lattice passes x N x M_tau x q lattices x
+    corridor cells, ~12 ns per FP64 cell; used only to size the sample."""
     cells = cfg.n * cfg.Mn - cfg.mn[0] * (cfg.mn[0] - 1) // 2
-    per_symbol = 2 * cfg.Mt * cfg.q * cells * 12e-9  # ~12 ns per FP64 cell on one core (SURVEY 8(d))
-    ns = int(max(10, min(cfg.N, ORACLE_FRAME_SECONDS / per_symbol)))
-    if ns >= cfg.N:
-        return cfg, 1.0, ""
-
-    def windows(N):  # lattice windows the oracle evaluates: 0 <= n i + m' <= rho (~ n N), reading R5
-        t = cfg.n * N
-        return sum(max(0, min(cfg.mt[1], t - cfg.n * i) - max(cfg.mt[0], -cfg.n * i) + 1) for i in range(N))
-
-    import dataclasses
-    sc = dataclasses.replace(cfg, N=ns, name=f"{cfg.name}@N{ns}")
-    scale = windows(ns) / windows(cfg.N)
-    return sc, scale, (f"; timed on frames of {cfg.name}'s code/channel/trellis with N = {ns}, rate scaled by "
-                       f"the ratio of lattice windows {scale:.3g}")
+    return 2 * cfg.N * cfg.Mt * cfg.q * cells * 12e-9
 
 
-def oracle_sample(cfg, target_seconds, first=10_000_000, max_frames=4096):
-    """Time the FP64 oracle (as it stands) on host cores over a bounded sample of the workload."""
-    import oracle
-    threads = os.cpu_count() or 1
-    prob = oracle.Problem(cfg.q, cfg.n, cfg.N, bsidgen.codebook(cfg), cfg.Pi, cfg.Pd, cfg.Ps, cfg.mn, cfg.mt)
-    probe = min(threads, max_frames)
-    b = bsidgen.make_batch(cfg, first, probe, C=prob.C)
-    t0 = time.perf_counter()
-    oracle.decode_many(prob, [b.bits(f) for f in range(probe)],
-                       [b.priors[f].astype(np.float64) if b.priors is not None else None for f in range(probe)],
-                       threads)
-    dt = time.perf_counter() - t0
-    per_wall = dt / probe
-    count = int(max(probe, min(max_frames, target_seconds / max(per_wall, 1e-9))))
-    count = max(threads, (count // threads) * threads)
-    return prob, count, per_wall, threads
+class OracleSampler:
+    """Times the FP64 oracle, as it stands, on the host cores over whole frames of the workload.
+    Short frames: one frame per host thread (frames in parallel).  Long frames (single-core estimate
+    above the target, C4/C5): one frame at a time with the oracle's in-frame threads on every core
+    (its m' loops; bit-identical to the serial oracle) -- at least one FULL frame is always timed,
+    so C5's baseline is a full N = 10^4 frame (minutes), never an extrapolation."""
 
+    def __init__(self, cfg, target_seconds):
+        import oracle
+        self.cfg = cfg
+        self.threads = os.cpu_count() or 1
+        self.prob = oracle.Problem(cfg.q, cfg.n, cfg.N, bsidgen.codebook(cfg), cfg.Pi, cfg.Pd, cfg.Ps, cfg.mn, cfg.mt)
+        est = oracle_frame_seconds(cfg)
+        self.in_frame = est > target_seconds
+        if self.in_frame:
+            self.count = 1
+            self.how = f"one frame at a time, {self.threads} oracle threads inside the frame"
+            dt = self.run(10_000_000, 1)
+            self.count = int(max(1, min(64, target_seconds / dt)))
+        else:
+            probe = self.threads
+            dt = self.run(10_000_000, probe)
+            self.count = max(self.threads, int(target_seconds / max(dt / probe, 1e-9)) // self.threads * self.threads)
+            self.count = min(self.count, 4096)
+            self.how = f"{self.threads} host threads over frames"
+        self.probe_s = dt
 
-def run_oracle_frames(cfg, prob, first, count, threads):
-    import oracle
-    b = bsidgen.make_batch(cfg, first, count, C=prob.C)
-    ys = [b.bits(f) for f in range(count)]
-    pl = [b.priors[f].astype(np.float64) if b.priors is not None else None for f in range(count)]
-    t0 = time.perf_counter()
-    oracle.decode_many(prob, ys, pl, threads)
-    return time.perf_counter() - t0
+    def run(self, first, count):
+        import oracle
+        b = bsidgen.make_batch(self.cfg, first, count, C=self.prob.C)
+        ys = [b.bits(f) for f in range(count)]
+        pl = [b.priors[f].astype(np.float64) if b.priors is not None else None for f in range(count)]
+        t0 = time.perf_counter()
+        if self.in_frame:
+            oracle.set_threads(self.threads)
+            try:
+                for y, pr in zip(ys, pl):
+                    oracle.decode(self.prob, y, pr)
+            finally:
+                oracle.set_threads(1)
+        else:
+            oracle.decode_many(self.prob, ys, pl, self.threads)
+        return time.perf_counter() - t0
 
 
 def cpu_baseline(cfg, target_seconds):
-    ocfg, scale, note = oracle_workload(cfg)
-    prob, count, _, threads = oracle_sample(ocfg, target_seconds)
-    dt = run_oracle_frames(ocfg, prob, 20_000_000, count, threads)
-    return {"value": count / dt * scale, "unit": "frames/s", "cores": threads, "kind": "oracle",
-            "sample": f"{count} frames of {ocfg.name} (global frame indices 20000000..), FP64 C oracle, "
-                      f"{threads} host threads over frames, {dt:.1f} s{note}"}
+    o = OracleSampler(cfg, target_seconds)
+    if o.in_frame and o.count == 1:
+        dt, count = o.probe_s, 1   # the probe already timed one full frame
+    else:
+        count = o.count
+        dt = o.run(20_000_000, count)
+    return {"value": count / dt, "unit": "frames/s", "cores": o.threads, "kind": "oracle",
+            "sample": f"{count} full frames of {cfg.name} (global frame indices 10000000.. / 20000000..), "
+                      f"FP64 C oracle, {o.how}, {dt:.1f} s"}
 
 
 def reference_arm(args, cfg):
@@ -182,22 +197,21 @@ def reference_arm(args, cfg):
     if rank != 0:
         return
     per_step = max(2.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
-    ocfg, scale, note = oracle_workload(cfg)
-    prob, count, _, threads = oracle_sample(ocfg, per_step)
+    o = OracleSampler(cfg, per_step)
+    count = o.count
     for w in range(args.warmup):
-        run_oracle_frames(ocfg, prob, 30_000_000 + w * count, count, threads)
-    times = [run_oracle_frames(ocfg, prob, 40_000_000 + s * count, count, threads) for s in range(args.steps)]
+        o.run(30_000_000 + w * count, count)
+    times = [o.run(40_000_000 + s * count, count) for s in range(args.steps)]
     total = sum(times)
-    value = count * args.steps / total * scale  # frames/s of the full configuration
+    value = count * args.steps / total  # frames/s of the configuration, whole frames timed
     line = {
         "impl": "reference", "metric": "frames/s", "value": value, "unit": "frames/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": describe(cfg), "frames_per_step": count, "sample": "bounded oracle sample" + note},
+        "config": {"workload": describe(cfg), "frames_per_step": count, "sample": "bounded oracle sample of full frames"},
         "symbols_per_s": value * cfg.N,
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "oracle",
-                         "sample": f"{count} frames x {args.steps} steps of {ocfg.name}, FP64 C oracle on "
-                                   f"{threads} host threads{note}"},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": o.threads, "kind": "oracle",
+                         "sample": f"{count} full frames x {args.steps} steps of {cfg.name}, FP64 C oracle, {o.how}"},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -214,7 +228,7 @@ def describe(cfg):
 
 def main():
     args = parse()
-    cfg = bsidgen.configs()[args.config]
+    cfg = workload(args)
     if args.impl == "reference":
         return reference_arm(args, cfg)
 
@@ -245,6 +259,8 @@ def main():
     b = bsidgen.make_batch(cfg, first, count)
     mode = {"auto": MODE_AUTO, "stored": MODE_STORED, "recompute": MODE_RECOMPUTE}[args.mode]
     d = Decoder.from_config(cfg, b.C, mode=mode, device=local)
+    if args.ws_limit_gb:
+        d.set_workspace_limit(int(args.ws_limit_gb * 2**30))
     rx = torch.from_numpy(b.rx.ravel().copy()).to(dev)
     off = torch.from_numpy(b.offsets).to(dev)
     rho = torch.from_numpy(b.rho).to(dev)
@@ -342,7 +358,15 @@ def main():
             print(f"warning: only {ok:.4f} of frames decoded OK in e2e", file=sys.stderr)
 
     st_h = st.cpu().numpy()
-    ser = float((np.argmax(L.cpu().numpy(), 2) != b.msg).mean())
+    L_h = L.cpu().numpy()
+    if args.dump:
+        os.makedirs(args.dump, exist_ok=True)
+        np.savez(os.path.join(args.dump, f"rank{rank}.npz"), L=L_h, status=st_h, first=first, count=count)
+    # job-wide symbol errors and decoded frames: summed over ranks (each rank holds its own shard)
+    sym_err = sum_over_ranks(int((np.argmax(L_h, 2) != b.msg).sum()), dev)
+    frames_ok = sum_over_ranks(int((st_h == 0).sum()), dev)
+    job_frames = sum_over_ranks(count, dev)
+    ser = sym_err / max(1.0, job_frames * cfg.N)
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
@@ -377,7 +401,7 @@ def main():
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk,
-            "frames_ok": float((st_h == 0).mean()),
+            "frames_ok": frames_ok / max(1.0, job_frames),
             "symbol_error_rate": ser,
         }
         print(json.dumps(line), flush=True)

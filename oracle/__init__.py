@@ -35,7 +35,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
         tmp = _LIB_PATH + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fno-fast-math",
-                               "-ffp-contract=off", "-o", tmp, _SRC, "-lm"])
+                               "-ffp-contract=off", "-fopenmp", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB_PATH)
     return _LIB_PATH
 
@@ -56,6 +56,8 @@ def _load():
             lib.oracle_decode.argtypes = [i, i, i, p, d, d, d, i, i, i, i, p, i, p, p, p, p, p, p, p, p, p]
             lib.oracle_extrinsic.restype = i
             lib.oracle_extrinsic.argtypes = [i, i, p, p, p]
+            lib.oracle_set_threads.restype = i
+            lib.oracle_set_threads.argtypes = [i]
             lib.oracle_gamma_at.restype = i
             lib.oracle_gamma_at.argtypes = [i, i, i, p, d, d, d, i, i, i, i, p, i, p, i, p]
             _lib = lib
@@ -123,11 +125,18 @@ def gamma(prob: Problem, y, i: int, priors=None):
     return g
 
 
+def set_threads(t: int) -> int:
+    """Host threads used inside ONE frame decode (gamma's m' loop, L's D loop, beta's m' loop).
+    The result is bit-identical for every thread count (the loops split keep the serial order of
+    every sum); the default 1 leaves frame-level threading (decode_many) to the caller."""
+    return _load().oracle_set_threads(int(t))
+
+
 def decode(prob: Problem, y, priors=None, want_states=False, alpha0=None, betaN=None, extrinsic=False):
     """Decode one frame.  Returns dict(status, L[N][q], log_lambda[, alpha, beta, logA, logB][, E]).
 
     alpha0 / betaN: optional frame-boundary priors over the M_tau states (P:152-154);
-    default point masses delta(0), delta(rho - tau)."""
+    default point masses delta(0), delta(rho - tau).  Threads inside the frame: set_threads()."""
     y = np.ascontiguousarray(y, dtype=np.uint8)
     pr = None if priors is None else np.ascontiguousarray(priors, dtype=np.float64).reshape(prob.N, prob.q)
     a0 = None if alpha0 is None else np.ascontiguousarray(alpha0, dtype=np.float64).reshape(prob.Mt)

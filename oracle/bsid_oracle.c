@@ -37,6 +37,7 @@
  * lambda-constancy), bit-complement symmetry.
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -45,6 +46,24 @@
 #define ORACLE_DRIFT_OUT_OF_RANGE 1
 #define ORACLE_UNDERFLOW 2
 #define ORACLE_EINVAL (-1)
+
+/*
+ * Host threads used INSIDE one frame (default 1).  Only loops whose iterations
+ * are independent and each keep the serial summation order are split across
+ * threads -- the m' loop of gamma (one lattice per (m', D)), the D
+ * loop of L_i(D) and the m' loop of beta_i(m') -- so the result is
+ * bit-identical to the single-threaded oracle for every thread count
+ * (tests/test_oracle_pins.py::test_threaded_oracle_bit_identical).  The
+ * alpha scatter (eqn:alpha) stays serial.  This is a speed knob for decoding a
+ * full-length frame (C5: N = 10^4), not a change of the arithmetic.
+ */
+static int oracle_threads = 1;
+
+int oracle_set_threads(int t)
+{
+    oracle_threads = t < 1 ? 1 : t;
+    return oracle_threads;
+}
 
 /* Q(y|x) = Pt*Ps if y != x, Pt*(1-Ps) if y == x, Pt = 1-Pi-Pd. */
 double oracle_qdot(int y, int x, double Pi, double Pd, double Ps)
@@ -146,38 +165,43 @@ static int check_problem(const oracle_problem *p)
 int oracle_gamma(const oracle_problem *p, int i, double *g)
 {
     const int Mt = p->mt_hi - p->mt_lo + 1, Mn = p->mn_hi - p->mn_lo + 1, n = p->n;
-    int mp, D, k, r;
-    uint8_t x[32];
-    double *F = (double *)malloc(sizeof(double) * (size_t)(n + 1) * (size_t)(n + p->mn_hi + 1));
-    if (F == NULL)
-        return ORACLE_EINVAL;
+    int mp, failed = 0;
     memset(g, 0, sizeof(double) * (size_t)Mt * Mn * p->q);
-    for (mp = p->mt_lo; mp <= p->mt_hi; mp++) {
-        const int s = n * i + mp; /* Y[n i + m' ...] (eqn:gamma) */
-        int W;
-        if (s < 0 || s > p->rho)
-            continue; /* R5: window outside the received sequence */
-        W = n + p->mn_hi;
-        if (p->rho - s < W)
-            W = p->rho - s;
-        for (D = 0; D < p->q; D++) {
-            const uint32_t word = p->C[(size_t)i * p->q + D];
-            const double prior = p->priors ? p->priors[(size_t)i * p->q + D] : 1.0 / p->q;
-            for (r = 0; r < n; r++)
-                x[r] = (uint8_t)((word >> r) & 1u);
-            oracle_lattice(n, x, W, p->y + s, p->Pi, p->Pd, p->Ps, 1, p->mn_lo, p->mn_hi, F);
-            for (k = p->mn_lo; k <= p->mn_hi; k++) {
-                const int m = mp + k, j = n + k;
-                if (j < 0 || j > W || m < p->mt_lo || m > p->mt_hi)
-                    continue;
-                /* gamma = P(D_i = D) R(Y[ni+m' .. n(i+1)+m) | C_i(D)) = prior * F_{n, n+k} */
-                g[((size_t)(mp - p->mt_lo) * Mn + (k - p->mn_lo)) * p->q + D] =
-                    prior * F[(size_t)n * (W + 1) + j];
+#pragma omp parallel num_threads(oracle_threads) reduction(| : failed)
+    {
+        int D, k, r;
+        uint8_t x[32];
+        double *F = (double *)malloc(sizeof(double) * (size_t)(n + 1) * (size_t)(n + p->mn_hi + 1));
+        if (F == NULL)
+            failed = 1;
+#pragma omp for schedule(dynamic, 4)
+        for (mp = p->mt_lo; mp <= p->mt_hi; mp++) {
+            const int s = n * i + mp; /* Y[n i + m' ...] (eqn:gamma) */
+            int W;
+            if (F == NULL || s < 0 || s > p->rho)
+                continue; /* R5: window outside the received sequence */
+            W = n + p->mn_hi;
+            if (p->rho - s < W)
+                W = p->rho - s;
+            for (D = 0; D < p->q; D++) {
+                const uint32_t word = p->C[(size_t)i * p->q + D];
+                const double prior = p->priors ? p->priors[(size_t)i * p->q + D] : 1.0 / p->q;
+                for (r = 0; r < n; r++)
+                    x[r] = (uint8_t)((word >> r) & 1u);
+                oracle_lattice(n, x, W, p->y + s, p->Pi, p->Pd, p->Ps, 1, p->mn_lo, p->mn_hi, F);
+                for (k = p->mn_lo; k <= p->mn_hi; k++) {
+                    const int m = mp + k, j = n + k;
+                    if (j < 0 || j > W || m < p->mt_lo || m > p->mt_hi)
+                        continue;
+                    /* gamma = P(D_i = D) R(Y[ni+m' .. n(i+1)+m) | C_i(D)) = prior * F_{n, n+k} */
+                    g[((size_t)(mp - p->mt_lo) * Mn + (k - p->mn_lo)) * p->q + D] =
+                        prior * F[(size_t)n * (W + 1) + j];
+                }
             }
         }
+        free(F);
     }
-    free(F);
-    return ORACLE_OK;
+    return failed ? ORACLE_EINVAL : ORACLE_OK;
 }
 
 /*
@@ -252,7 +276,10 @@ int oracle_decode(int q, int n, int N, const uint32_t *C,
     for (i = 1; i <= N && status == ORACLE_OK; i++) {
         double c = 0.0;
         double *An = A + (size_t)i * Mt, *Ap = A + (size_t)(i - 1) * Mt;
-        oracle_gamma(&p, i - 1, g);
+        if (oracle_gamma(&p, i - 1, g) != ORACLE_OK) {
+            status = ORACLE_EINVAL;
+            break;
+        }
         for (mp = 0; mp < Mt; mp++)
             for (k = 0; k < Mn; k++)
                 for (D = 0; D < q; D++) {
@@ -306,8 +333,12 @@ int oracle_decode(int q, int n, int N, const uint32_t *C,
         for (i = N - 1; i >= 0; i--) {
             double c = 0.0;
             double *Bi = B + (size_t)i * Mt, *Bn = B + (size_t)(i + 1) * Mt, *Ai = A + (size_t)i * Mt;
-            oracle_gamma(&p, i, g);
+            if (oracle_gamma(&p, i, g) != ORACLE_OK) {
+                status = ORACLE_EINVAL;
+                break;
+            }
             /* L_i(D) = (1/lambda_N) sum_{m',m} alpha_i(m') gamma_i(m',m,D) beta_{i+1}(m) */
+#pragma omp parallel for num_threads(oracle_threads) private(mp, k, m) schedule(static)
             for (D = 0; D < q; D++) {
                 double s = 0.0;
                 for (mp = 0; mp < Mt; mp++)
@@ -320,6 +351,7 @@ int oracle_decode(int q, int n, int N, const uint32_t *C,
                 L[(size_t)i * q + D] = s * exp(lA[i] + lB[i + 1] - lnlam);
             }
             /* beta_i(m') = sum_{m,D} beta_{i+1}(m) gamma_i(m',m,D) (eqn:beta) */
+#pragma omp parallel for num_threads(oracle_threads) private(k, D, m) schedule(static)
             for (mp = 0; mp < Mt; mp++)
                 for (k = 0; k < Mn; k++)
                     for (D = 0; D < q; D++) {

@@ -395,3 +395,34 @@ def test_extrinsic_equals_posterior_without_own_prior():
     np.testing.assert_allclose(res["E"].sum(1), 1.0, atol=1e-12)
     res_u = oracle.decode(prob, b.bits(0), extrinsic=True)
     np.testing.assert_allclose(res_u["E"], res_u["L"] / res_u["L"].sum(1, keepdims=True), rtol=1e-13)
+
+
+@pytest.mark.parametrize("threads", [2, 5, 8])
+def test_threaded_oracle_bit_identical(threads):
+    """oracle.set_threads(t) splits only loops whose iterations are independent (gamma's m' loop,
+    L's D loop, beta's m' loop) and keeps every sum's serial order, so the threaded decode must
+    equal the single-threaded one bit for bit -- including the states, the log scales, soft
+    frame boundaries and non-uniform priors -- and therefore inherits every pin above."""
+    import dataclasses
+    cfg = dataclasses.replace(bsidgen.configs()["C2"], N=30, priors=True)
+    b = bsidgen.make_batch(cfg, 77, 2)
+    prob = oracle.Problem(cfg.q, cfg.n, cfg.N, b.C, cfg.Pi, cfg.Pd, cfg.Ps, cfg.mn, cfg.mt)
+    rng = np.random.default_rng(threads)
+    kw = dict(want_states=True, extrinsic=True)
+    for f in range(2):
+        args = (prob, b.bits(f), b.priors[f].astype(np.float64))
+        extra = {} if f == 0 else dict(alpha0=rng.random(prob.Mt), betaN=rng.random(prob.Mt))
+        try:
+            oracle.set_threads(1)
+            r1 = oracle.decode(*args, **kw, **extra)
+            g1 = oracle.gamma(prob, b.bits(f), 17, b.priors[f])
+            oracle.set_threads(threads)
+            rt = oracle.decode(*args, **kw, **extra)
+            gt = oracle.gamma(prob, b.bits(f), 17, b.priors[f])
+        finally:
+            oracle.set_threads(1)
+        assert r1["status"] == rt["status"] == oracle.OK
+        assert r1["log_lambda"] == rt["log_lambda"]
+        for k in ("L", "E", "alpha", "beta", "logA", "logB"):
+            np.testing.assert_array_equal(rt[k], r1[k])
+        np.testing.assert_array_equal(gt, g1)
