@@ -224,6 +224,47 @@ def describe(cfg):
             f"priors={'non-uniform' if cfg.priors else 'uniform'}")
 
 
+# ------------------------------------------------------------------------- roofline inputs
+
+def fp32_peak(sms):
+    """FP32 peak of the ALU roofline: the measured FFMA2 throughput of this B200 pool
+    (profiles/fp32_peak.json, tools/ubench/fp32_peak.cu: independent FFMA2 chains on every SM);
+    MEASURED_PEAKS.json has no FP32 entry.  Fallback: the guide's unit counts at the max SM clock."""
+    path = os.path.join(ROOT, "profiles", "fp32_peak.json")
+    nominal = sms * FP32_LANES_PER_SM * 2 * 1965e6 / 1e12
+    try:
+        m = json.load(open(path))
+        return float(m["ffma2_tflops"]), (f"measured: FFMA2 microbenchmark {m['ffma2_tflops']:.1f} TFLOP/s at "
+                                          f"{m.get('sm_mhz_nvidia_smi_under_load', '?')} MHz (profiles/fp32_peak.json; nominal "
+                                          f"{nominal:.1f} = {sms} SMs x 128 lanes x 2 flop x 1965 MHz)")
+    except (OSError, KeyError, ValueError):
+        return nominal, (f"nominal: {sms} SMs x 128 FP32 lanes x 2 flop x 1965 MHz (no profiles/fp32_peak.json; "
+                         "MEASURED_PEAKS.json has no FP32 entry)")
+
+
+def ncu_profile(cfg, key, frames, plan):
+    """DRAM traffic and executed FP32 flops of the dominant kernel from one `ncu --set full` capture
+    (profiles/ncu_summary.json, tools/ncu_summary.py) -- used only if it was captured at this source
+    digest, for this workload and batch (else null, with the reason)."""
+    from paper_1802_08483_b200._lib import source_digest
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    digest = source_digest()
+    try:
+        ent = json.load(open(path)).get(cfg.name, {}).get(key)
+    except (OSError, ValueError):
+        ent = None
+    if not ent:
+        return {"traffic": None, "ncu": f"no capture of {cfg.name}/{key} in profiles/ncu_summary.json"}
+    if ent.get("src_digest") != digest or ent.get("frames") != frames:
+        return {"traffic": None, "ncu": f"stale: capture {ent.get('round')} at source digest {ent.get('src_digest')}, "
+                                        f"{ent.get('frames')} frames; this run {digest}, {frames} frames"}
+    out = {"traffic": ent.get("dram_bytes_per_launch"), "ncu": f"{ent.get('round')} (source digest {digest})",
+           "fma_pipe_active_ncu": ent.get("fma_pipe_active")}
+    if ent.get("fp32_flops_executed"):
+        out["executed_flops_per_launch"] = ent["fp32_flops_executed"]
+    return out
+
+
 # ------------------------------------------------------------------------------ our arm
 
 def main():
@@ -310,19 +351,12 @@ def main():
     mean_ph = ph.mean(0)
     dominant = 1 if mean_ph[1] >= mean_ph[3] else 3
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    peak_tf = sms * FP32_LANES_PER_SM * 2 * 1965e6 / 1e12
+    peak_tf, peak_basis = fp32_peak(sms)
     achieved = flops_pass / (mean_ph[dominant] / 1e3) / 1e12
-    stored = plan["mode"] == "stored"
-    traffic = None
-    pipe = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(prof):
-        try:
-            ent = json.load(open(prof)).get(cfg.name, {}).get("lattice_pass1" if dominant == 1 else "lattice_pass2", {})
-            traffic = ent.get("dram_bytes_per_launch")
-            pipe = ent.get("fma_pipe_active")
-        except Exception:
-            traffic = None
+    prof = ncu_profile(cfg, "lattice_pass1" if dominant == 1 else "lattice_pass2", count, plan)
+    if "executed_flops_per_launch" in prof:  # executed work over the same live launch time
+        prof["executed_achieved"] = prof["executed_flops_per_launch"] / (mean_ph[dominant] / 1e3) / 1e12
+        prof["frac_executed"] = prof["executed_achieved"] / peak_tf
 
     # end-to-end through the host-buffer C-ABI entry (pinned buffers, copies inside the timed region)
     e2e = None
@@ -375,7 +409,9 @@ def main():
             "metric": "frames/s", "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32",
-            "dtype_detail": "FP32 lattice (receiver metric, P:272-275); FP64 alpha/beta and APP accumulation",
+"dtype_detail": "FP32: lattice / gamma / Gamma (receiver metric, P:272-275) and each window's APP term "
+                            "alpha*beta*gamma; FP64: alpha/beta recursions and normalisation, the APP sum over "
+                            "windows and symbols, and the L normalisation (output FP32)",
             "data": "synthetic",
             "config": {"workload": describe(cfg), "frames_per_gpu": count,
                        "total_frames": int(total_frames // args.steps), "mode": plan["mode"],
@@ -383,16 +419,18 @@ def main():
                        "l2": "flushed (256 MiB write) between timed steps; per-step working set > L2"},
             "symbols_per_s": value * cfg.N,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tf, "traffic": traffic,
+                         "frac": achieved / peak_tf, "traffic": prof.get("traffic"),
                          "kernel": "lattice pass 1 (k_gamma_sum)" if dominant == 1 else "lattice pass 2 (k_app)",
-                         "peak_basis": f"{sms} SMs x 128 FP32 lanes x 2 flop x 1965 MHz (max SM clock); "
-                                       "derived, MEASURED_PEAKS.json has no FP32 entry",
+                         "peak_basis": peak_basis,
                          "flops_per_launch": flops_pass, "launch_ms": float(mean_ph[dominant]),
                          "frames_per_launch": int(min(plan["chunk"], count)),
-                         "fma_pipe_active_ncu": pipe,
-                         "note": "achieved counts the paper's 5 flops per lattice node (P:857); the kernel "
-                                 "executes 2 FFMA per node after exact re-associations, so the executed FMA-pipe "
-                                 "utilisation (fma_pipe_active_ncu, from profiles/ncu_summary.json) is lower"},
+                         "note": "achieved/frac count the paper's algorithmic work, 5 flops per lattice node over "
+                                 "the P:857 node count of every valid lattice (algorithmic-equivalent); the kernel "
+                                 "executes fewer (2 FFMA per node after the exact G = F/Pd^r rescaling, suffix "
+                                 "classes, prefix sharing, folded rows, skipped all-zero tiles): executed_* are the "
+                                 "FP32 flops ncu counted for this kernel at this source digest over the same "
+                                 "live launch time",
+                         **{k: v for k, v in prof.items() if k != "traffic"}},
             "phase_ms": {"init": float(mean_ph[0]), "lattice_pass1": float(mean_ph[1]),
                          "alpha_beta": float(mean_ph[2]), "lattice_pass2": float(mean_ph[3]),
                          "finalize": float(mean_ph[4]),

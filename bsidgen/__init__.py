@@ -105,10 +105,38 @@ def _trim(p, off, floor):
     return p[nz[0]:nz[-1] + 1].copy(), off + int(nz[0])
 
 
-def drift_limits(T: int, Pi: float, Pd: float, Pr: float = 1e-10):
-    """(m_T^-, m_T^+): m^- = max{m : P(S_T < m) <= Pr/2}, m^+ = min{m : P(S_T > m) <= Pr/2},
-    clamped to -T <= m^- <= 0 <= m^+ (reading R8)."""
+def drift_limits(T: int, Pi: float, Pd: float, Pr: float = 1e-10, rule: str = "greedy"):
+    """(m_T^-, m_T^+) with exclusion probability Pr (reading R8).
+
+    rule "greedy" (default): grow [0, 0] one state at a time on the side with more
+    excluded mass (ties: the positive side) until P(S_T < m^-) + P(S_T > m^+) < Pr.
+    rule "tails" (round 1): m^- = max{m : P(S_T < m) <= Pr/2}, m^+ = min{m : P(S_T > m) <= Pr/2},
+    clamped to -T <= m^- <= 0 <= m^+.
+    """
     off, p = drift_pmf(T, Pi, Pd)
+    if rule == "greedy":
+        mass = float(p.sum())
+        if not (1.0 - mass < Pr):
+            raise ValueError("drift PMF truncation loss >= Pr")
+        left = np.concatenate([[0.0], np.cumsum(p)])              # left[j] = P(S < off + j)
+        right = np.concatenate([np.cumsum(p[::-1])[::-1][1:], [0.0]])  # right[j] = P(S > off + j)
+
+        def below(m):
+            j = m - off
+            return 0.0 if j <= 0 else mass if j >= len(p) else float(left[j])
+
+        def above(m):
+            j = m - off
+            return 0.0 if j >= len(p) else mass if j < 0 else float(right[j])
+
+        lo = hi = 0
+        while below(lo) + above(hi) >= Pr:
+            if above(hi) >= below(lo):
+                hi += 1
+            else:
+                lo -= 1
+        return int(lo), int(hi)
+    assert rule == "tails", rule
     cdf = np.cumsum(p)             # cdf[j] = P(S <= off + j)
     lo = 0
     for j in range(len(p)):        # P(S < off + j) = cdf[j-1]

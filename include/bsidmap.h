@@ -81,11 +81,8 @@ typedef struct bsidmap_decoder bsidmap_decoder; /* opaque; owns the device codeb
  *   BSIDMAP_AB_SUB=k   alpha/beta side-stream sub-batches (1 = off; default: 2 when 2F <= #SMs)
  *   BSIDMAP_APP_KP=k   APP prefix-sharing length (0 = off; default ~log2(q) - 1)
  *   BSIDMAP_APP_KS=k   lattice rows folded into the APP weights (1 or 2; default 2 for register-heavy shapes)
- *   BSIDMAP_APP_X4=1   four-window APP kernel (small corridors; default off)
  *   BSIDMAP_AB_CTA_STAGES=k, BSIDMAP_AB_CTA_THREADS=t  ring depth / block size of the CTA alpha/beta
  *                      kernel (M_tau > 128; defaults: 1 stage when 2F >= 4 #SMs, ~M_tau/2 threads)
- *   BSIDMAP_PASS_SMEM_MIN=b  floor (bytes) on the lattice passes' dynamic shared memory, i.e. an
- *                      occupancy cap leaving room for co-resident alpha/beta blocks (default 0)
  */
 int bsidmap_create(bsidmap_decoder **out, int q, int n, int N, const uint32_t *codebook_host,
                    double Pi, double Pd, double Ps, int mn_lo, int mn_hi, int mt_lo, int mt_hi,
@@ -218,9 +215,14 @@ int bsidmap_debug_states(bsidmap_decoder *d, int num_frames, double *alpha_out, 
 /* pmf[m - lo] = P(S_T = m) for m in [lo, hi] (FP64; mass outside the range is dropped). */
 int bsidmap_drift_pmf(int T, double Pi, double Pd, int lo, int hi, double *pmf);
 /* Limits with exclusion probability Pr (reading R8; the paper defers the rule to
- * bbw14joe): lo = max{m : P(S_T < m) <= Pr/2},
- * hi = min{m : P(S_T > m) <= Pr/2}, clamped to -T <= lo <= 0 <= hi. */
+ * bbw14joe, and names P_r at P:1747-1750): the smallest [lo, hi] containing 0 with
+ * P(S_T < lo) + P(S_T > hi) < Pr, grown from [0, 0] one state at a time on the side with more
+ * excluded mass, ties to the positive side.  BSIDMAP_EINVAL for bad arguments or
+ * when the PMF's own truncation loss (insertions per bit cut at Pi^k < 1e-17) is >= Pr. */
 int bsidmap_drift_limits(int T, double Pi, double Pd, double Pr, int *lo, int *hi);
+/* The per-tail rule (round 1's default): lo = max{m : P(S_T < m) <= Pr/2},
+ * hi = min{m : P(S_T > m) <= Pr/2}, clamped to -T <= lo <= 0 <= hi. */
+int bsidmap_drift_limits_tails(int T, double Pi, double Pd, double Pr, int *lo, int *hi);
 /* m_n^± from T = n and m_tau^± from T = n N, widened to contain m_n (bsidmap_create's rule). */
 int bsidmap_state_space(int n, int N, double Pi, double Pd, double Pr, int *mn_lo, int *mn_hi, int *mt_lo,
                         int *mt_hi);

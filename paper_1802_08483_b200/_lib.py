@@ -12,6 +12,21 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbsidmap.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "bsidmap.h")
 
+def source_digest() -> str:
+    """sha256 (first 16 hex digits) of the library's sources (csrc/*.cu, *.cuh and the header): ties
+    a stored profile (profiles/ncu_summary.json) to the kernels it measured; a stale one is refused."""
+    import hashlib
+    csrc = os.path.join(_HERE, "csrc")
+    h = hashlib.sha256()
+    for f in sorted(os.listdir(csrc)) + [HEADER_PATH]:
+        path = f if os.path.isabs(f) else os.path.join(csrc, f)
+        if path.endswith((".cu", ".cuh", ".h")):
+            h.update(os.path.basename(path).encode())
+            with open(path, "rb") as fh:
+                h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 BSIDMAP_OK = 0
 BSIDMAP_EINVAL = -1
 BSIDMAP_ENOTINJECTIVE = -2
@@ -50,6 +65,7 @@ SIGNATURES = {
     "bsidmap_debug_states": (_i, [_p, _i, _p, _p, _p]),
     "bsidmap_drift_pmf": (_i, [_i, _d, _d, _i, _i, _p]),
     "bsidmap_drift_limits": (_i, [_i, _d, _d, _d, _p, _p]),
+    "bsidmap_drift_limits_tails": (_i, [_i, _d, _d, _d, _p, _p]),
     "bsidmap_state_space": (_i, [_i, _i, _d, _d, _d, _p, _p, _p, _p]),
     "bsidmap_phi": (_i, [_i, _d, _d, _i, _i, _i, _p, _p]),
     "bsidmap_mc_generate": (_i, [_p, ctypes.c_uint64, ctypes.c_int64, _i, _i, _p, _p, _p, _p, _p]),

@@ -17,7 +17,6 @@
 
 #include "../../include/bsidmap.h"
 #include "k_local_x2.cuh"
-#include "k_lattice_x4.cuh"
 #include "k_alphabeta_cta.cuh"
 #include "k_local_cta.cuh"
 
@@ -87,11 +86,9 @@ struct bsidmap_decoder {
   // alpha/beta overlap: sub-batch k's alpha/beta recursions run on a high-priority side
   // stream while the lattice passes of the other sub-batches run on the decode stream
   int ab_sub = 0;                       // sub-batches per chunk (0 = automatic, 1 = no overlap)
-  size_t pass_smem_min = 0;             // floor on the lattice passes' dynamic smem (occupancy cap)
   int ab_stages = 0, ab_threads = 0;    // CTA alpha/beta ring depth and block size (0 = automatic)
   int num_sms = 148;
   int app_kp = -1;                      // pass-2 prefix length override (-1 = automatic)
-  int app_x4 = -1;                      // four-window APP kernel (-1 = automatic, 0 = off)
   int app_ks = -1;                      // rows folded into the APP weights (-1 = automatic; BSIDMAP_APP_KS)
   cudaStream_t s_ab = nullptr;
   cudaEvent_t ev_p1[kMaxAbSub] = {}, ev_ab[kMaxAbSub] = {};
@@ -178,7 +175,6 @@ struct Plan {
   int ab_sub;                              // sub-batches of the alpha/beta-overlapped pipeline
   void (*app_kernel)(const DecodeParams);  // pass-2 kernel (prefix-sharing instance where available)
   int app_kp;                              // its prefix length (0 = none)
-  int app_w4;                              // 1: app_kernel is the four-window k_app_x4 (half-warp tiles)
   int app_ks;                              // lattice rows folded into the APP weights (1 or 2)
 };
 
@@ -277,15 +273,6 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
     P->app_kernel = P->app_kp > 0 ? d->kern.app_pre_ks2[P->app_kp - 2] : d->kern.app_ks2;
     P->app_smem = d->kern.app_W == 2 ? app_x2_smem(d->q, d->Mn, 2) : app_x1_smem(d->q, d->Mn, 2);
   }
-  // four windows per lane (k_app_x4) only on request: measured slower on B200 (C2 pass 2 41.9 vs
-  // 61.5 TF/s: 3 CTAs/SM with spills against 5) -- tools/exp_x4.sh
-  P->app_w4 = 0;
-  if (mode == kSchedGammaSum && d->kern.app_x4 && d->app_x4 > 0) {
-    P->app_kernel = d->kern.app_x4;
-    P->app_kp = 0;
-    P->app_w4 = 1;
-    P->app_smem = app_x4_smem(d->q, d->Mn);
-  }
   // alpha/beta overlap (Gamma-sum only): measured on B200 it only pays where the alpha/beta grid
   // cannot fill the GPU (one CTA per frame and direction, 2F <= #SMs: C5 at 32 frames/GPU,
   // 401 vs 424 ms); with a full grid the recursions compete with the lattice passes for issue
@@ -299,10 +286,6 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   P->l1_smem = (d->kern.gamma_sum_k3 && mode != kSchedStored)
                    ? (size_t)d->Mn * kLatticeThreads * 8 + (size_t)d->q * 6 + 64 + 16
                    : (size_t)d->q * 4;
-  if (d->pass_smem_min) {  // leave room for co-resident alpha/beta blocks (experiment)
-    P->l1_smem = std::max(P->l1_smem, d->pass_smem_min);
-    P->app_smem = std::max(P->app_smem, d->pass_smem_min);
-  }
   return BSIDMAP_OK;
 }
 
@@ -409,14 +392,21 @@ int ensure_ab_stream(bsidmap_decoder* d) {
   return BSIDMAP_OK;
 }
 
-void launch_pass1(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s) {
-  const long lanes = (long)p.F * d->Mt;
-  const unsigned gx_flat = (unsigned)((lanes + kLatticeThreads - 1) / kLatticeThreads);
+// The pass-1 kernel a decode launches: the stored-gamma kernel, or the plan's class kernel in its
+// non-uniform-prior instance when priors are given (the smem opt-in is set on this same pointer).
+void (*pass1_kernel(const bsidmap_decoder* d, const Plan& P, bool priors))(const DecodeParams) {
   auto l1 = P.mode == kSchedStored ? d->kern.gamma_store : P.l1_kernel;
-  if (P.mode != kSchedStored && p.priors) {  // the non-uniform-prior instance of the pass-1 kernel
+  if (P.mode != kSchedStored && priors) {
     if (l1 == d->kern.gamma_sum && d->kern.gamma_sum_pri) l1 = d->kern.gamma_sum_pri;
     if (l1 == d->kern.gamma_sum_k3 && d->kern.gamma_sum_k3_pri) l1 = d->kern.gamma_sum_k3_pri;
   }
+  return l1;
+}
+
+void launch_pass1(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s) {
+  const long lanes = (long)p.F * d->Mt;
+  const unsigned gx_flat = (unsigned)((lanes + kLatticeThreads - 1) / kLatticeThreads);
+  auto l1 = pass1_kernel(d, P, p.priors != nullptr);
   // the class kernels walk up to kL1Steps symbol indices per CTA -- fewer where the grid would
   // not fill the GPU (small batches: single-frame latency)
   const bool multi = P.mode != kSchedStored && d->kern.l1_steps;
@@ -445,8 +435,7 @@ void launch_alpha_beta(bsidmap_decoder* d, const Plan& P, const DecodeParams& p,
 void launch_pass2(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s) {
   const long lanes = (long)p.F * d->Mt;
   const unsigned gx_tile =
-      P.app_w4 ? (unsigned)(((long)p.F * tiles_per_frame(d->Mt) + 2 * kX2Warps - 1) / (2 * kX2Warps))
-               : (unsigned)(((long)p.F * tiles_per_frame_w(d->Mt, d->kern.app_W) + kX2Warps - 1) / kX2Warps);
+      (unsigned)(((long)p.F * tiles_per_frame_w(d->Mt, d->kern.app_W) + kX2Warps - 1) / kX2Warps);
   const unsigned gx_flat = (unsigned)((lanes + kLatticeThreads - 1) / kLatticeThreads);
   const unsigned gx = d->kern.W == 2 ? gx_tile : gx_flat;
   auto l2 = P.app_kernel;
@@ -645,9 +634,7 @@ int bsidmap_create(bsidmap_decoder** out, int q, int n, int N, const uint32_t* c
   if (const char* v = std::getenv("BSIDMAP_AB_SUB")) d->ab_sub = std::max(1, std::atoi(v));
   if (const char* v = std::getenv("BSIDMAP_AB_CTA_STAGES")) d->ab_stages = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("BSIDMAP_AB_CTA_THREADS")) d->ab_threads = std::max(0, std::atoi(v)) & ~31;
-  if (const char* v = std::getenv("BSIDMAP_PASS_SMEM_MIN")) d->pass_smem_min = (size_t)std::max(0, std::atoi(v));
   if (const char* v = std::getenv("BSIDMAP_APP_KP")) d->app_kp = std::max(0, std::atoi(v));
-  if (const char* v = std::getenv("BSIDMAP_APP_X4")) d->app_x4 = std::atoi(v);
   if (const char* v = std::getenv("BSIDMAP_APP_KS")) d->app_ks = std::atoi(v) == 2 ? 2 : 1;
   // lattice constants (eqn:F, Q-dot); row 0 = insertions only, F_{0,j} = 2^s (Pi/2)^j
   const double Pt = 1.0 - Pi - Pd;
@@ -710,7 +697,7 @@ int bsidmap_decode_batch_opts(bsidmap_decoder* d, int F, const uint32_t* rx, con
   const Layout l = layout(d, P.chunk, P.mode);
   if ((rc = ensure_ws(d, l.total))) return rc;
   if ((rc = set_smem(d, P.ab_warp ? (const void*)P.ab_warp : (const void*)P.ab_cta, P.ab_smem))) return rc;
-  if ((rc = set_smem(d, (const void*)P.l1_kernel, P.l1_smem))) return rc;
+  if ((rc = set_smem(d, (const void*)pass1_kernel(d, P, priors != nullptr), P.l1_smem))) return rc;
   if (P.mode == kSchedLocal) {
     if ((rc = set_smem(d, (const void*)d->kern.local_fwd, P.local_smem))) return rc;
     if ((rc = set_smem(d, (const void*)d->kern.local_bwd, P.local_smem))) return rc;
@@ -907,7 +894,7 @@ int bsidmap_plan_info(bsidmap_decoder* d, int F, char* buf, size_t len) {
       d->kern.W == 2 ? ((long)P.chunk * tiles_per_frame(d->Mt) + kX2Warps - 1) / kX2Warps
                      : (lanes + kLatticeThreads - 1) / kLatticeThreads,
       d->N, kLatticeThreads, P.chunk, P.ab_warp ? kAbWarpThreads : P.ab_threads,
-      layout(d, P.chunk, P.mode).total, d->kern.W, d->q, d->n, d->N, d->Mn, d->Mt, std::min(P.ab_sub, P.chunk), P.app_kp, P.app_w4 ? 4 : d->kern.app_W, P.app_ks);
+      layout(d, P.chunk, P.mode).total, d->kern.W, d->q, d->n, d->N, d->Mn, d->Mt, std::min(P.ab_sub, P.chunk), P.app_kp, d->kern.app_W, P.app_ks);
   return nb;
 }
 

@@ -5,7 +5,10 @@
 // followed by a deletion (change k - 1, probability Pi^k Pd) or a transmission
 // (change k, probability Pi^k Pt).  Its PMF is the T-fold convolution, computed by
 // repeated squaring in FP64.  The limits follow DESIGN.md reading R8 (the paper
-// defers the rule to bbw14joe; exclusion probability P_r).
+// defers the rule to bbw14joe; exclusion probability P_r):
+// the smallest interval around 0 whose excluded mass is below P_r, grown one state at
+// a time on the side with more excluded mass; the older per-tail rule
+// (each tail <= P_r/2) stays available as bsidmap_drift_limits_tails.
 //
 // Phi_T (the paper names a "Compute Phi_T" kernel but never
 // defines it) is read as this drift PMF over T bits; k_phi writes it, restricted to a
@@ -100,8 +103,35 @@ int bsidmap_drift_pmf(int T, double Pi, double Pd, int lo, int hi, double* pmf) 
 int bsidmap_drift_limits(int T, double Pi, double Pd, double Pr, int* lo, int* hi) {
   if (T < 0 || !lo || !hi || !valid_channel(Pi, Pd) || !(Pr > 0 && Pr < 1)) return BSIDMAP_EINVAL;
   const Pmf d = drift_pmf(T, Pi, Pd);
+  const long W = (long)d.p.size();
+  // the excluded mass must be resolvable: the PMF's own truncation loss stays below Pr
+  double mass = 0.0;
+  for (long j = 0; j < W; j++) mass += d.p[j];
+  if (!(1.0 - mass < Pr)) return BSIDMAP_EINVAL;
+  // tail sums accumulated from the far ends (small terms first): left[j] = P(S < off + j),
+  // right[j] = P(S > off + j)
+  std::vector<double> left(W + 1, 0.0), right(W + 1, 0.0);
+  for (long j = 0; j < W; j++) left[j + 1] = left[j] + d.p[j];
+  for (long j = W - 1; j >= 0; j--) right[j] = (j + 1 < W ? right[j + 1] + d.p[j + 1] : 0.0);
+  auto below = [&](long m) { const long j = m - d.off; return j <= 0 ? 0.0 : j >= W ? mass : left[j]; };
+  auto above = [&](long m) { const long j = m - d.off; return j >= W ? 0.0 : j < 0 ? mass : right[j]; };
+  // grow [0, 0] one state at a time on the side with more excluded mass (ties: the positive
+  // side) until the excluded mass is below Pr (reading R8)
+  long mlo = 0, mhi = 0;
+  while (below(mlo) + above(mhi) >= Pr) {
+    if (above(mhi) >= below(mlo)) mhi++;
+    else mlo--;
+  }
+  *lo = (int)mlo;
+  *hi = (int)mhi;
+  return BSIDMAP_OK;
+}
+
+int bsidmap_drift_limits_tails(int T, double Pi, double Pd, double Pr, int* lo, int* hi) {
+  if (T < 0 || !lo || !hi || !valid_channel(Pi, Pd) || !(Pr > 0 && Pr < 1)) return BSIDMAP_EINVAL;
+  const Pmf d = drift_pmf(T, Pi, Pd);
   const size_t W = d.p.size();
-  // m^- = max{m : P(S < m) <= Pr/2},  m^+ = min{m : P(S > m) <= Pr/2}  (reading R8)
+  // m^- = max{m : P(S < m) <= Pr/2},  m^+ = min{m : P(S > m) <= Pr/2}  (the round-1 rule)
   long mlo = d.off, mhi = d.off + (long)W - 1;
   double below = 0.0;
   for (size_t j = 0; j < W; j++) {

@@ -2,7 +2,6 @@
 // nvcc compiles the unrolled lattice cores in parallel).
 #pragma once
 #include "k_local_x2.cuh"
-#include "k_lattice_x4.cuh"
 #include "k_alphabeta_cta.cuh"
 #include "k_local_cta.cuh"
 
@@ -11,30 +10,17 @@
 #define BSIDMAP_SCALAR_MN_MAX 20
 #endif
 
-// pass 1 of those shapes: the pair class kernel at 3 CTAs/SM (default, k_lattice_x2.cuh) or,
-// with -DBSIDMAP_SCALAR_L1=1, the scalar class kernel (measured slower: tools/exp_p1x2.sh)
-#if defined(BSIDMAP_SCALAR_L1) && BSIDMAP_SCALAR_L1
-#define BSIDMAP_SCALAR_PASS1(NN, LO, MN)                                   \
-  out->gamma_sum = k_gamma_sum_cls<SpecCore<NN, LO, MN>, 2, false>;       \
-  out->gamma_sum_k3 = k_gamma_sum_cls<SpecCore<NN, LO, MN>, 3, false>;    \
-  out->gamma_sum_pri = k_gamma_sum_cls<SpecCore<NN, LO, MN>, 2, true>;    \
-  out->gamma_sum_k3_pri = k_gamma_sum_cls<SpecCore<NN, LO, MN>, 3, true>; \
-  out->gamma_store = k_gamma_sum<SpecCore<NN, LO, MN>, true>;             \
-  out->l1_W = 1;
-#else
-#define BSIDMAP_SCALAR_PASS1(NN, LO, MN)
-#endif
+// pass 1 of those shapes stays on the pair class kernel at 3 CTAs/SM (k_lattice_x2.cuh; the scalar
+// class kernel measured slower: tools/exp_p1x2.sh)
 
 #define BSIDMAP_SPEC_UNIT(IDX, NN, LO, MN)                                               \
   namespace bsidmap {                                                                    \
   bool spec_unit_##IDX(int n, int lo, int Mn, CoreKernels* out) {                        \
     if (n != NN || lo != LO || Mn != MN) return false;                                   \
     *out = make_core_kernels_x2<SpecCoreX2<NN, LO, MN>>(SpecCoreX2<NN, LO, MN>::nodes()); \
-    out->app_x4 = app_x4_kernel<NN, LO, MN>();                                            \
     out->ab_cta = k_alpha_beta_cta<MN>;                                                   \
     local_cta_kernels<SpecCore<NN, LO, MN>>(out);                                          \
     if (SpecCoreX2<NN, LO, MN>::kMinBlocks <= 2 && MN <= BSIDMAP_SCALAR_MN_MAX) { /* measured: scalar APP wins (C3, C5) */ \
-      BSIDMAP_SCALAR_PASS1(NN, LO, MN)                                                  \
       out->app = k_app_x1<SpecCore<NN, LO, MN>, 0>;                                     \
       out->app_pre[0] = k_app_x1<SpecCore<NN, LO, MN>, 2>;                              \
       out->app_pre[1] = k_app_x1<SpecCore<NN, LO, MN>, 3>;                              \

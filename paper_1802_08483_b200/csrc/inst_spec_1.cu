@@ -1,3 +1,3 @@
-// Fully unrolled lattice core for (n, m_n^-, M_n) = (10,-6,14).
+// Fully unrolled lattice core for (n, m_n^-, M_n) = (10,-6,13).
 #include "inst.cuh"
-BSIDMAP_SPEC_UNIT(1, 10,-6,14)
+BSIDMAP_SPEC_UNIT(1, 10,-6,13)

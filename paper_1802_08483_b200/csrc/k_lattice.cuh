@@ -303,7 +303,6 @@ struct CoreKernels {
   void (*gamma_store)(const DecodeParams);
   void (*app)(const DecodeParams);
   void (*app_pre[3])(const DecodeParams);  // APP with prefix sharing, KP = 2, 3, 4 first codeword bits (spec only)
-  void (*app_x4)(const DecodeParams);      // APP on four windows per lane (SpecCoreX4; small corridors only)
   void (*app_ks2)(const DecodeParams);     // pair-core APP with the last two rows folded (KP = 0)
   void (*app_pre_ks2[3])(const DecodeParams);  // ... with prefix sharing KP = 2, 3, 4
   int app_ks_auto;                         // default folded rows of this core's APP kernel
@@ -331,7 +330,6 @@ CoreKernels make_core_kernels(long nodes) {
   k.gamma_store = k_gamma_sum<Core, true>;
   k.app = k_app<Core>;
   k.app_pre[0] = k.app_pre[1] = k.app_pre[2] = nullptr;
-  k.app_x4 = nullptr;
   k.app_ks2 = nullptr;
   k.app_ks_auto = 1;
   k.app_pre_ks2[0] = k.app_pre_ks2[1] = k.app_pre_ks2[2] = nullptr;

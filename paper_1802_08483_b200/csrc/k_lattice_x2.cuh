@@ -68,9 +68,6 @@ __device__ __forceinline__ int exp2_of(double x) {  // floor(log2 x) for normal 
 #endif
 // the class-ordered pass 1 at one more CTA/SM where 3 fit (128 registers, ~140 B of spills outside
 // the row loop; tools/exp_minb.sh: C2 pass 1 52.98 -> 50.79 ms, C1 shape 0.205 -> 0.192 ms)
-#ifndef BSIDMAP_L1_FUSED_ADD
-#define BSIDMAP_L1_FUSED_ADD 1
-#endif
 // and at 3 (168 registers, ~100 B of spills) for the 2-CTA shapes with M_n <= BSIDMAP_SCALAR_MN_MAX
 // (whose APP runs on the scalar core): C3 pass 1 67.7 -> 62.2 ms, C5 226.1 -> 199.7 ms against the
 // scalar class kernel; C4 (M_n = 26) stays at 2 (71.9 vs 76.9 ms at 3) -- tools/exp_p1x2*.sh
@@ -237,12 +234,9 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1C_MINB) k_gamma_sum
 #pragma unroll
           for (int e = 0; e < MN; e++) acc[e] = kPri ? ffma2(P, g[e], acc[e]) : fadd2(g[e], acc[e]);
         };
-#if BSIDMAP_L1_FUSED_ADD  // the class-sum update inside the last row group's basic block (rows_then)
+        // the class-sum update inside the last row group's basic block (rows_then); uniform priors:
+        // the common factor 1/q is applied at the store
         Core::template run_prefix_then<K, BSIDMAP_L1_GROUP>(lane, x, p, fo, add);
-#else
-        Core::template run_prefix<K, BSIDMAP_L1_GROUP>(lane, x, p, fo);
-        add(fo);  // uniform priors: the common factor 1/q is applied at the store
-#endif
       }
       Core::template apply_last_rows<K>(lane, cur, p, acc);
       if (!first) {
@@ -393,7 +387,7 @@ __device__ __forceinline__ void app_weights_pair(const DecodeParams& p, const La
 // over the lanes once after the D loop instead of one shuffle chain per D
 __host__ __device__ __forceinline__ size_t app_stage_floats(int q) { return (size_t)q * 33; }
 __host__ __device__ __forceinline__ size_t app_x2_smem(int q, int Mn, int ks = 1) {
-  return (size_t)kX2Warps * (2 << (ks - 1)) * Mn * 32 * 8 + (size_t)kX2Warps * (app_stage_floats(q) + q) * 4;
+  return (size_t)kX2Warps * (2 << (ks - 1)) * Mn * 32 * 8 + (size_t)kX2Warps * (app_stage_floats(q) * 4 + (size_t)q * 8);
 }
 // Symbols are visited in lexicographic codeword order (DecodeParams::Cp, prepared at create) so
 // that lattice rows 1..KP (run_head) are computed once per distinct prefix; KP = 0: natural order.
@@ -404,7 +398,7 @@ __host__ __device__ __forceinline__ int app_prefix_bits(int q, int n) {
 }
 // smem: s_w[kX2Warps][2][M_n][32] (f32x2: the scaled beta corridor of each lane's two windows with
 //       the last lattice row folded in, one table per value of x_n; smem, not registers) |
-//       s_S[kX2Warps][q] (float) | staging [kX2Warps][q][33]
+//       s_S[kX2Warps][q] (double) | staging [kX2Warps][q][33] (float)
 // prefix sharing keeps the head row live across the symbol loop (+2 M_n registers)
 #ifndef BSIDMAP_APP_MINB_PRE
 #define BSIDMAP_APP_MINB_PRE (Core::kMinBlocks > 2 ? 4 : 2)
@@ -414,9 +408,6 @@ __host__ __device__ __forceinline__ int app_prefix_bits(int q, int n) {
 // so each symbol runs rows 1..n-2 only.  Exact re-association (the rows are linear maps).
 // the weight dot inside the basic block of the last lattice row (rows_then), so it interleaves
 // with the row's insertion chain instead of running as a dependent tail after the branch merge
-#ifndef BSIDMAP_APP_FUSED_DOT
-#define BSIDMAP_APP_FUSED_DOT 1
-#endif
 #ifndef BSIDMAP_APP_MINB_KS2
 #define BSIDMAP_APP_MINB_KS2 (Core::kMinBlocks > 2 ? 3 : 2)
 #endif
@@ -429,8 +420,8 @@ __global__ void __launch_bounds__(kLatticeThreads, KS == 2 ? BSIDMAP_APP_MINB_KS
   constexpr int RL = Core::NNr - KS;  // last lattice row run per symbol
   extern __shared__ __align__(128) unsigned char smem[];
   f32x2* s_bt = reinterpret_cast<f32x2*>(smem);
-  float* s_S = reinterpret_cast<float*>(s_bt + kX2Warps * NT * MN * 32);
-  float* s_stage = s_S + kX2Warps * p.q;
+  double* s_S = reinterpret_cast<double*>(s_bt + kX2Warps * NT * MN * 32);
+  float* s_stage = reinterpret_cast<float*>(s_S + kX2Warps * p.q);
   const int i = blockIdx.y + p.i_base;
   // KP > 0: symbols in lexicographic codeword order (prefix groups contiguous); every smem array
   // below is per warp, so the kernel has no block barrier
@@ -466,7 +457,7 @@ __global__ void __launch_bounds__(kLatticeThreads, KS == 2 ? BSIDMAP_APP_MINB_KS
     wb = (float)(db * sc);
   }
   const bool live = __any_sync(0xffffffffu, wa > 0.f || wb > 0.f);
-  float* S = s_S + warp * p.q;
+  double* S = s_S + warp * p.q;
   float* stg = s_stage + (size_t)warp * app_stage_floats(p.q);
   if (live) {
     typename Core::Lane lane_t;
@@ -518,50 +509,40 @@ __global__ void __launch_bounds__(kLatticeThreads, KS == 2 ? BSIDMAP_APP_MINB_KS
         xprev = x;
 #pragma unroll
         for (int e = 0; e < MN; e++) fo[e] = fh[e];
-#if BSIDMAP_APP_FUSED_DOT
         Core::template run_tail_to_then<KP, RL, BSIDMAP_APP_GROUP>(lane_t, x, p, fo, dot);
-#else
-        Core::template run_tail_to<KP, RL, BSIDMAP_APP_GROUP>(lane_t, x, p, fo);
-        dot(fo);
-#endif
       } else {
-#if BSIDMAP_APP_FUSED_DOT
         Core::template run_to_then<RL, BSIDMAP_APP_GROUP>(lane_t, x, p, fo, dot);
-#else
-        Core::template run_to<RL, BSIDMAP_APP_GROUP>(lane_t, x, p, fo);
-        dot(fo);
-#endif
       }
       const int D = KP > 0 ? (int)Di[k] : k;
       stg[D * 33 + lane] = fmaf(wa, lo_of(t0) + lo_of(t1), wb * (hi_of(t0) + hi_of(t1)));
     }
     __syncwarp();
-    for (int D = lane; D < p.q; D += 32) {  // S(D) = P(D) sum over the warp's windows
-      float c = 0.f;
+    for (int D = lane; D < p.q; D += 32) {  // S(D) = P(D) sum over the warp's windows (FP64)
+      double c = 0.0;
 #pragma unroll 8
-      for (int l = 0; l < 32; l++) c += stg[D * 33 + l];
-      S[D] = pri ? c * __ldg(pri + D) : c;
+      for (int l = 0; l < 32; l++) c += (double)stg[D * 33 + l];
+      S[D] = pri ? c * (double)__ldg(pri + D) : c;
     }
   }
   __syncwarp();
   if (T == 1) {
     // the warp holds the whole sum over m': L_i(D) = S(D) / sum_D S(D)
-    float tot = 0.f;
+    double tot = 0.0;
     if (live)
       for (int D = lane; D < p.q; D += 32) tot += S[D];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    const bool ok = frame_ok && live && tot > 0.f;
-    const float inv = ok ? 1.f / tot : 0.f;
+    const bool ok = frame_ok && live && tot > 0.0;
+    const double inv = ok ? 1.0 / tot : 0.0;
     float* Lrow = p.L + ((size_t)f * p.N + i) * p.q;
-    for (int D = lane; D < p.q; D += 32) Lrow[D] = ok ? S[D] * inv : 0.f;
+    for (int D = lane; D < p.q; D += 32) Lrow[D] = ok ? (float)(S[D] * inv) : 0.f;
     if (frame_ok && !ok && lane == 0) p.status[f] = kFrameUnderflow;
   } else if (live) {
     const double sc = pow2d(Emax);
     double* acc = p.Lacc + ((size_t)f * p.N + i) * p.q;
     for (int D = lane; D < p.q; D += 32) {
-      const float v = S[D];
-      if (v > 0.f) atomicAdd(acc + D, (double)v * sc);
+      const double v = S[D];
+      if (v > 0.0) atomicAdd(acc + D, v * sc);
     }
   }
 }
@@ -570,7 +551,7 @@ __global__ void __launch_bounds__(kLatticeThreads, KS == 2 ? BSIDMAP_APP_MINB_KS
 // pair core is register-bound (C3, C5) -- also wastes fewer slots (C3: 9 x 32 vs 5 x 64 for 267).
 __host__ __device__ __forceinline__ int tiles_per_frame_w(int Mt, int W) { return (Mt + 32 * W - 1) / (32 * W); }
 __host__ __device__ __forceinline__ size_t app_x1_smem(int q, int Mn = 0, int ks = 1) {
-  return (size_t)kX2Warps * (app_stage_floats(q) + q) * 4 + (ks == 2 ? (size_t)4 * Mn * kLatticeThreads * 4 : 0);
+  return (size_t)kX2Warps * (app_stage_floats(q) * 4 + (size_t)q * 8) + (ks == 2 ? (size_t)4 * Mn * kLatticeThreads * 4 : 0);
 }
 
 #ifndef BSIDMAP_APP1_MINB_PRE
@@ -583,8 +564,8 @@ __global__ void __launch_bounds__(kLatticeThreads, (KP > 0 || KS == 2) ? BSIDMAP
   constexpr int MN = Core::Mn;
   constexpr int RL = Core::NNr - KS;  // last lattice row run per symbol
   extern __shared__ __align__(128) unsigned char smem[];
-  float* s_S = reinterpret_cast<float*>(smem);
-  float* s_stage = s_S + kX2Warps * p.q;
+  double* s_S = reinterpret_cast<double*>(smem);
+  float* s_stage = reinterpret_cast<float*>(s_S + kX2Warps * p.q);
   float* s_w = s_stage + (size_t)kX2Warps * app_stage_floats(p.q) + threadIdx.x;  // KS = 2: [4][MN][128]
   const int i = blockIdx.y + p.i_base;
   const uint32_t* Ci = (KP > 0 ? p.Cp : p.C) + (size_t)i * p.q;
@@ -607,7 +588,7 @@ __global__ void __launch_bounds__(kLatticeThreads, (KP > 0 || KS == 2) ? BSIDMAP
     wa = (float)(da * pow2d(-Emax));
   }
   const bool live = __any_sync(0xffffffffu, wa > 0.f);
-  float* S = s_S + warp * p.q;
+  double* S = s_S + warp * p.q;
   float* stg = s_stage + (size_t)warp * app_stage_floats(p.q);
   if (live) {
     typename Core::Lane lane_t;
@@ -655,14 +636,13 @@ __global__ void __launch_bounds__(kLatticeThreads, (KP > 0 || KS == 2) ? BSIDMAP
         xprev = x;
 #pragma unroll
         for (int e = 0; e < MN; e++) fo[e] = fh[e];
-        if constexpr (KS == 2 && BSIDMAP_APP_FUSED_DOT) Core::template run_tail_to_then<KP, RL>(lane_t, x, p, fo, dot);
+        if constexpr (KS == 2) Core::template run_tail_to_then<KP, RL>(lane_t, x, p, fo, dot);
         else Core::template run_tail_to<KP, RL>(lane_t, x, p, fo);
       } else {
-        if constexpr (KS == 2 && BSIDMAP_APP_FUSED_DOT) Core::template run_to_then<RL>(lane_t, x, p, fo, dot);
+        if constexpr (KS == 2) Core::template run_to_then<RL>(lane_t, x, p, fo, dot);
         else Core::template run_to<RL>(lane_t, x, p, fo);
       }
       if constexpr (KS == 2) {
-        if constexpr (!BSIDMAP_APP_FUSED_DOT) dot(fo);
       } else if ((x >> nb) & 1u) {
 #pragma unroll
         for (int e = 0; e < MN; e += 2) {
@@ -679,31 +659,31 @@ __global__ void __launch_bounds__(kLatticeThreads, (KP > 0 || KS == 2) ? BSIDMAP
       stg[D * 33 + lane] = wa * (t0 + t1);
     }
     __syncwarp();
-    for (int D = lane; D < p.q; D += 32) {
-      float c = 0.f;
+    for (int D = lane; D < p.q; D += 32) {  // FP64, as k_app_x2
+      double c = 0.0;
 #pragma unroll 8
-      for (int l = 0; l < 32; l++) c += stg[D * 33 + l];
-      S[D] = pri ? c * __ldg(pri + D) : c;
+      for (int l = 0; l < 32; l++) c += (double)stg[D * 33 + l];
+      S[D] = pri ? c * (double)__ldg(pri + D) : c;
     }
   }
   __syncwarp();
   if (T == 1) {
-    float tot = 0.f;
+    double tot = 0.0;
     if (live)
       for (int D = lane; D < p.q; D += 32) tot += S[D];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    const bool ok = frame_ok && live && tot > 0.f;
-    const float inv = ok ? 1.f / tot : 0.f;
+    const bool ok = frame_ok && live && tot > 0.0;
+    const double inv = ok ? 1.0 / tot : 0.0;
     float* Lrow = p.L + ((size_t)f * p.N + i) * p.q;
-    for (int D = lane; D < p.q; D += 32) Lrow[D] = ok ? S[D] * inv : 0.f;
+    for (int D = lane; D < p.q; D += 32) Lrow[D] = ok ? (float)(S[D] * inv) : 0.f;
     if (frame_ok && !ok && lane == 0) p.status[f] = kFrameUnderflow;
   } else if (live) {
     const double sc = pow2d(Emax);
     double* acc = p.Lacc + ((size_t)f * p.N + i) * p.q;
     for (int D = lane; D < p.q; D += 32) {
-      const float v = S[D];
-      if (v > 0.f) atomicAdd(acc + D, (double)v * sc);
+      const double v = S[D];
+      if (v > 0.0) atomicAdd(acc + D, v * sc);
     }
   }
 }
@@ -761,7 +741,6 @@ CoreKernels make_core_kernels_x2_base(long nodes) {
   k.app_pre_ks2[0] = k_app_x2<Core, 2, 2>;
   k.app_pre_ks2[1] = k_app_x2<Core, 3, 2>;
   k.app_pre_ks2[2] = k_app_x2<Core, 4, 2>;
-  k.app_x4 = nullptr;
   k.app_stored = k_app_stored<Core::Mn>;
   k.gamma_dump = k_gamma_dump_x2<Core>;
   k.nodes = nodes;

@@ -23,9 +23,9 @@ namespace bsidmap {
 
 constexpr int kLocalWarps = 4;  // frames per CTA
 
-// smem per warp: s_G[max(M_n * 64, q)] floats (fwd: Gamma_i [k][slot]; bwd: S(D)) |
+// smem per warp: s_G[max(M_n * 64, 2 q)] floats (fwd: Gamma_i [k][slot]; bwd: S(D) as doubles) |
 //                s_row[64] doubles | s_C[q] words
-__host__ __device__ __forceinline__ int local_g_floats(int Mn, int q) { return Mn * 64 > q ? Mn * 64 : q; }
+__host__ __device__ __forceinline__ int local_g_floats(int Mn, int q) { return Mn * 64 > 2 * q ? Mn * 64 : 2 * q; }
 __host__ __device__ __forceinline__ size_t local_warp_smem(int Mn, int q) {
   // rounded to 16 bytes: the next warp's FP64 row must stay 8-byte aligned for odd q
   return ((size_t)local_g_floats(Mn, q) * 4 + 64 * 8 + (size_t)q * 4 + 15) & ~size_t(15);
@@ -113,8 +113,8 @@ __global__ void __launch_bounds__(kLocalWarps * 32, BSIDMAP_APP_MINB) k_local_bw
   extern __shared__ __align__(128) unsigned char s_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* base = s_raw + (size_t)warp * local_warp_smem(MN, p.q);
-  float* sS = reinterpret_cast<float*>(base);                 // S(D), q floats
-  double* row = reinterpret_cast<double*>(sS + local_g_floats(MN, p.q));  // beta_{i+1} [slot]
+  double* sS = reinterpret_cast<double*>(base);               // S(D), q doubles
+  double* row = reinterpret_cast<double*>(base + (size_t)local_g_floats(MN, p.q) * 4);  // beta_{i+1} [slot]
   uint32_t* sC = reinterpret_cast<uint32_t*>(row + 64);
   const int f = blockIdx.x * kLocalWarps + warp;
   if (f >= p.F) return;
@@ -185,24 +185,24 @@ __global__ void __launch_bounds__(kLocalWarps * 32, BSIDMAP_APP_MINB) k_local_bw
         const float P = pri ? __ldg(pri + D) : 1.f;
         ba = fmaf(P, ta, ba);
         bb = fmaf(P, tb, bb);
-        float c = fmaf(wa, ta, wb * tb);
+        double c = (double)fmaf(wa, ta, wb * tb);  // the sum over the windows in FP64
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        if (lane == 0) sS[D] = c * P;
+        if (lane == 0) sS[D] = c * (double)P;
       }
     }
     __syncwarp();
     // L_i(D) = S(D) / sum_D S(D)   (eqn:L; equal to the literal 1/lambda_N, reading R2)
     {
-      float tot = 0.f;
+      double tot = 0.0;
       if (live)
         for (int D = lane; D < p.q; D += 32) tot += sS[D];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-      const bool ok = live && tot > 0.f;
-      const float inv = ok ? 1.f / tot : 0.f;
+      const bool ok = live && tot > 0.0;
+      const double inv = ok ? 1.0 / tot : 0.0;
       float* Lrow = Lf + (size_t)i * p.q;
-      for (int D = lane; D < p.q; D += 32) Lrow[D] = ok ? sS[D] * inv : 0.f;
+      for (int D = lane; D < p.q; D += 32) Lrow[D] = ok ? (float)(sS[D] * inv) : 0.f;
       if (!ok) {
         if (lane == 0) p.status[f] = kFrameUnderflow;
         return;

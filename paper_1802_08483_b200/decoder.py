@@ -182,11 +182,13 @@ def drift_pmf(T, Pi, Pd, lo, hi):
     return out
 
 
-def drift_limits(T, Pi, Pd, Pr=1e-10):
-    """(m_T^-, m_T^+) with exclusion probability Pr (bsidmap_drift_limits)."""
+def drift_limits(T, Pi, Pd, Pr=1e-10, rule="greedy"):
+    """(m_T^-, m_T^+) with exclusion probability Pr: rule "greedy" = bsidmap_drift_limits (smallest
+    interval around 0, total excluded mass < Pr), "tails" = bsidmap_drift_limits_tails."""
     lib = _lib.load()
     lo, hi = ctypes.c_int(), ctypes.c_int()
-    _lib.check(lib.bsidmap_drift_limits(int(T), float(Pi), float(Pd), float(Pr), ctypes.byref(lo), ctypes.byref(hi)))
+    fn = {"greedy": lib.bsidmap_drift_limits, "tails": lib.bsidmap_drift_limits_tails}[rule]
+    _lib.check(fn(int(T), float(Pi), float(Pd), float(Pr), ctypes.byref(lo), ctypes.byref(hi)))
     return lo.value, hi.value
 
 

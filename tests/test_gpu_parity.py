@@ -259,24 +259,6 @@ def test_alpha_beta_overlap_subbatches_bit_identical(name, frames, monkeypatch):
     assert_parity(outs[1][0], outs[1][1], run_oracle(cfg, b, range(3)), range(3))
 
 
-@pytest.mark.parametrize("name,frames,mt", [("C1", 13, None), ("C2", 9, None), ("C2", 5, (-100, 100))])
-def test_app_four_window_kernel(name, frames, mt, monkeypatch):
-    """k_app_x4 (four windows per lane, half-warp tiles) against the oracle and
-    against the two-window kernel: odd frame counts leave the last warp's second half-tile
-    empty; the widened m_tau (M_tau = 201, four tiles per frame) takes the Lacc path."""
-    cfg = small_cfg(name) if mt is None else small_cfg(name, mt=mt)
-    b = bsidgen.make_batch(cfg, 21, frames)
-    monkeypatch.setenv("BSIDMAP_APP_X4", "1")
-    d4, L4, st4 = run_gpu(cfg, b, 3)
-    assert d4.plan(frames)["app_windows_per_lane"] == 4
-    monkeypatch.setenv("BSIDMAP_APP_X4", "0")
-    d2, L2, st2 = run_gpu(cfg, b, 3)
-    assert d2.plan(frames)["app_windows_per_lane"] != 4
-    np.testing.assert_array_equal(st4, st2)
-    np.testing.assert_allclose(L4, L2, rtol=2e-5, atol=1e-30)
-    assert_parity(L4, st4, run_oracle(cfg, b))
-
-
 @pytest.mark.parametrize("name,frames", [("C1", 9), ("C2", 7), ("C4", 2), ("C3", 3), ("C5r", 2)])
 def test_app_two_folded_rows(name, frames, monkeypatch):
     """APP pass with the last TWO lattice rows folded into its weights (row n-1 transposed,

@@ -1,9 +1,14 @@
 """Summarise an ncu --set full report and a launch list into profiles/.
-usage: python tools/ncu_summary.py <tag> <gpurun_out/dir> <config>"""
+usage: python tools/ncu_summary.py <tag> <gpurun_out/dir> <config> <frames>
+The capture directory holds digest.txt (the library source digest at capture time, tools/gpu_prof.sh);
+bench.py uses an entry only at the same digest and batch size."""
 import csv, io, json, os, subprocess, sys
 from collections import defaultdict
 
-tag, src, cfg = sys.argv[1], sys.argv[2], sys.argv[3]
+tag, src, cfg, frames = sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4])
+digest = open(os.path.join(src, "digest.txt")).read().strip()
+FP32_OPS = {"ffma": 2, "ffma2": 4, "fadd": 1, "fadd2": 2, "fmul": 1, "fmul2": 2}
+FP64_OPS = {"dfma": 2, "dadd": 1, "dmul": 1}
 os.makedirs("profiles", exist_ok=True)
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "smsp__issue_active.avg.pct_of_peak_sustained_active",
@@ -12,7 +17,8 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
            "smsp__inst_executed.sum", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
-           "sm__cycles_elapsed.avg.per_second", "launch__grid_size", "launch__block_size"]
+           "sm__cycles_elapsed.avg.per_second", "launch__grid_size", "launch__block_size"] + \
+          [f"smsp__sass_thread_inst_executed_op_{o}_pred_on.sum" for o in list(FP32_OPS) + list(FP64_OPS)]
 raw = subprocess.run(["ncu", "-i", os.path.join(src, "prof.ncu-rep"), "--page", "raw", "--csv"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
@@ -51,9 +57,19 @@ for d in kernels:
         fp = float(fp) / 100.0
     except ValueError:
         fp = None
+    def ops(table):
+        tot = 0.0
+        for o, w in table.items():
+            v = d.get(f"smsp__sass_thread_inst_executed_op_{o}_pred_on.sum", ("", ""))[0].replace(",", "")
+            try:
+                tot += w * float(v)
+            except ValueError:
+                return None
+        return tot
     entry[key] = {"kernel": name, "dram_bytes_per_launch": (rd + wr) if rd is not None and wr is not None else None,
-                  "time_ms": float(d["gpu__time_duration.sum"][0]) if "gpu__time_duration.sum" in d else None,
-                  "fma_pipe_active": fp, "round": tag}
+                  "time_ms": float(d["gpu__time_duration.sum"][0].replace(",", "")) if "gpu__time_duration.sum" in d else None,
+                  "fma_pipe_active": fp, "fp32_flops_executed": ops(FP32_OPS), "fp64_flops_executed": ops(FP64_OPS),
+                  "round": tag, "src_digest": digest, "frames": frames}
     lines.append(f"## {name}")
     for m in METRICS:
         if m in d:
