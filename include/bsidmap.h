@@ -81,6 +81,9 @@ typedef struct bsidmap_decoder bsidmap_decoder; /* opaque; owns the device codeb
  *   BSIDMAP_AB_SUB=k   alpha/beta side-stream sub-batches (1 = off; default: 2 when 2F <= #SMs)
  *   BSIDMAP_APP_KP=k   APP prefix-sharing length (0 = off; default ~log2(q) - 1)
  *   BSIDMAP_APP_KS=k   lattice rows folded into the APP weights (1 or 2; default 2 for register-heavy shapes)
+ *   BSIDMAP_LIVE_APP=0 tiled APP over every window instead of the live-window APP (default 1)
+ *   BSIDMAP_LIVE_EPS=e live-window threshold (default 2^-128; 0 = skip exactly-zero windows only)
+ *   BSIDMAP_APP_G=g    frames per warp of the live-window APP (default: up to 8)
  *   BSIDMAP_AB_CTA_STAGES=k, BSIDMAP_AB_CTA_THREADS=t  ring depth / block size of the CTA alpha/beta
  *                      kernel (M_tau > 128; defaults: 1 stage when 2F >= 4 #SMs, ~M_tau/2 threads)
  */

@@ -25,6 +25,7 @@ __global__ void k_frame_init(const DecodeParams p);
 __global__ void k_finalize(const DecodeParams p);
 __global__ void k_zero_failed(const DecodeParams p);
 __global__ void k_extrinsic(const DecodeParams p, float* E);
+__global__ void k_live(const DecodeParams p);
 struct McParams {
   uint64_t seed;
   long first;
@@ -90,6 +91,9 @@ struct bsidmap_decoder {
   int num_sms = 148;
   int app_kp = -1;                      // pass-2 prefix length override (-1 = automatic)
   int app_ks = -1;                      // rows folded into the APP weights (-1 = automatic; BSIDMAP_APP_KS)
+  double live_eps = 0x1p-128;           // live-window threshold of the APP pass (reading R18; BSIDMAP_LIVE_EPS)
+  int live_app = 1;                     // live-window APP where the core has it (BSIDMAP_LIVE_APP=0: tiled APP)
+  int app_G = 0;                        // its frames per warp (0 = automatic; BSIDMAP_APP_G)
   cudaStream_t s_ab = nullptr;
   cudaEvent_t ev_p1[kMaxAbSub] = {}, ev_ab[kMaxAbSub] = {};
   cudaEvent_t ev_abt[2] = {};           // alpha/beta stream busy time (timed decodes)
@@ -117,8 +121,9 @@ int cuda_fail(bsidmap_decoder* d, cudaError_t e, const char* what) {
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t gsum, gamma, alpha, beta, lacc, total;
+  size_t gsum, gamma, alpha, beta, lacc, live, total;
 };
+
 
 // Bytes per frame of each workspace array (the paper's memory estimate).
 // Storage schedules.  kSchedLocal is the paper's local storage: gamma computed in
@@ -141,6 +146,15 @@ int resolve_sched(const bsidmap_decoder* d, int mode) {
   return kSchedGammaSum;
 }
 
+// The Gamma-sum schedule runs the live-window APP (k_app_live.cuh) where the lattice core has one and
+// one frame per warp fits in shared memory (two folded rows: the larger tables).
+bool uses_live_app(const bsidmap_decoder* d, int sched) {
+  if (sched != kSchedGammaSum || !d->live_app || d->kern.app_live[0][0] == nullptr) return false;
+  const size_t need = d->kern.app_live_W == 2 ? kX2Warps * app_live_x2_warp_smem(d->q, d->Mn, 2, 1)
+                                              : app_live_x1_cta_tables(d->Mn, 2) + kX2Warps * app_live_x1_warp_smem(d->q, 1);
+  return need <= 227u * 1024;
+}
+
 const char* sched_name(int s) {
   return s == kSchedStored ? "stored"
          : s == kSchedLocal ? "recompute-local"
@@ -155,8 +169,10 @@ Layout layout(const bsidmap_decoder* d, long F, int sched) {
   l.gamma = sched == kSchedStored ? align_up((size_t)F * d->N * d->q * d->Mn * d->Mt * sizeof(float)) : 0;
   l.alpha = align_up((size_t)F * (d->N + 1) * d->Mt * sizeof(double));
   l.beta = local ? 0 : l.alpha;
-  l.lacc = local ? 0 : align_up((size_t)F * d->N * d->q * sizeof(double));
-  l.total = l.gsum + l.gamma + l.alpha + l.beta + l.lacc;
+  const bool live = uses_live_app(d, sched);
+  l.lacc = (local || live) ? 0 : align_up((size_t)F * d->N * d->q * sizeof(double));
+  l.live = live ? align_up((size_t)F * d->N * sizeof(int2)) : 0;
+  l.total = l.gsum + l.gamma + l.alpha + l.beta + l.lacc + l.live;
   return l;
 }
 
@@ -176,6 +192,8 @@ struct Plan {
   void (*app_kernel)(const DecodeParams);  // pass-2 kernel (prefix-sharing instance where available)
   int app_kp;                              // its prefix length (0 = none)
   int app_ks;                              // lattice rows folded into the APP weights (1 or 2)
+  bool app_live;                           // app_kernel is the live-window APP (k_app_live.cuh)
+  int app_G;                               // its frames per warp
 };
 
 size_t budget(const bsidmap_decoder* d) {
@@ -273,6 +291,25 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
     P->app_kernel = P->app_kp > 0 ? d->kern.app_pre_ks2[P->app_kp - 2] : d->kern.app_ks2;
     P->app_smem = d->kern.app_W == 2 ? app_x2_smem(d->q, d->Mn, 2) : app_x1_smem(d->q, d->Mn, 2);
   }
+  // live-window APP (k_app_live.cuh): only the windows of each (frame, i) row whose posterior mass
+  // exceeds eps (k_live), packed G frames per warp; the warps write the L rows themselves
+  P->app_live = uses_live_app(d, mode);
+  P->app_G = 1;
+  if (P->app_live) {
+    // up to 8 frames per warp (fewer partly filled rounds); fewer where the grid would not fill the
+    // GPU or the per-frame sums would not fit in shared memory
+    const long rows = (long)chunk * d->N;
+    int G = d->app_G > 0 ? std::min(d->app_G, kLiveMaxG) : (int)std::max(1L, std::min(8L, rows / (32L * d->num_sms)));
+    auto smem = [&](int g) {
+      return d->kern.app_live_W == 2 ? kX2Warps * app_live_x2_warp_smem(d->q, d->Mn, P->app_ks, g)
+                                     : app_live_x1_cta_tables(d->Mn, P->app_ks) + kX2Warps * app_live_x1_warp_smem(d->q, g);
+    };
+    while (G > 1 && smem(G) > 227u * 1024) G--;
+    P->app_kernel = d->kern.app_live[P->app_ks - 1][P->app_kp > 0 ? P->app_kp - 1 : 0];
+    P->app_G = G;
+    P->app_smem = smem(G);
+    P->direct_L = true;
+  }
   // alpha/beta overlap (Gamma-sum only): measured on B200 it only pays where the alpha/beta grid
   // cannot fill the GPU (one CTA per frame and direction, 2F <= #SMs: C5 at 32 frames/GPU,
   // 401 vs 424 ms); with a full grid the recursions compete with the lattice passes for issue
@@ -332,6 +369,7 @@ void fill_params(const bsidmap_decoder* d, DecodeParams* p) {
     p->Cst[k] = reinterpret_cast<const int*>(ob + d->ord_off[4 + 3 * k]);
   }
   p->lc = d->lc;
+  p->live_eps = d->live_eps;
 }
 
 void bind_ws(const bsidmap_decoder* d, const Layout& l, DecodeParams* p) {
@@ -344,7 +382,9 @@ void bind_ws(const bsidmap_decoder* d, const Layout& l, DecodeParams* p) {
   b += l.alpha;
   p->beta = reinterpret_cast<double*>(b);
   b += l.beta;
-  p->Lacc = reinterpret_cast<double*>(b);
+  p->Lacc = l.lacc ? reinterpret_cast<double*>(b) : nullptr;
+  b += l.lacc;
+  p->live = l.live ? reinterpret_cast<int2*>(b) : nullptr;
 }
 
 void record(bsidmap_decoder* d, int k, cudaStream_t s) {
@@ -374,6 +414,7 @@ DecodeParams sub_params(const DecodeParams& p, int f0, int nf) {
   s.alpha += (size_t)f0 * (N + 1) * Mt;
   if (s.beta) s.beta += (size_t)f0 * (N + 1) * Mt;
   if (s.Lacc) s.Lacc += (size_t)f0 * N * q;
+  if (s.live) s.live += (size_t)f0 * N;
   s.L += (size_t)f0 * N * q;
   return s;
 }
@@ -433,6 +474,19 @@ void launch_alpha_beta(bsidmap_decoder* d, const Plan& P, const DecodeParams& p,
 }
 
 void launch_pass2(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s) {
+  if (P.app_live) {  // live windows of every (frame, i) row, then the packed APP over them
+    const long rows = (long)p.F * d->N;
+    k_live<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(p);
+    d->launches++;
+    p.app_G = P.app_G;
+    const unsigned gx = (unsigned)(((p.F + P.app_G - 1) / P.app_G + kX2Warps - 1) / kX2Warps);
+    for_i_slices(d->N, [&](int i0, int ni) {
+      p.i_base = i0;
+      P.app_kernel<<<dim3(gx, ni), kLatticeThreads, P.app_smem, s>>>(p);
+      d->launches++;
+    });
+    return;
+  }
   const long lanes = (long)p.F * d->Mt;
   const unsigned gx_tile =
       (unsigned)(((long)p.F * tiles_per_frame_w(d->Mt, d->kern.app_W) + kX2Warps - 1) / kX2Warps);
@@ -636,6 +690,9 @@ int bsidmap_create(bsidmap_decoder** out, int q, int n, int N, const uint32_t* c
   if (const char* v = std::getenv("BSIDMAP_AB_CTA_THREADS")) d->ab_threads = std::max(0, std::atoi(v)) & ~31;
   if (const char* v = std::getenv("BSIDMAP_APP_KP")) d->app_kp = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("BSIDMAP_APP_KS")) d->app_ks = std::atoi(v) == 2 ? 2 : 1;
+  if (const char* v = std::getenv("BSIDMAP_LIVE_EPS")) d->live_eps = std::max(0.0, std::atof(v));
+  if (const char* v = std::getenv("BSIDMAP_LIVE_APP")) d->live_app = std::atoi(v) != 0;
+  if (const char* v = std::getenv("BSIDMAP_APP_G")) d->app_G = std::max(0, std::atoi(v));
   // lattice constants (eqn:F, Q-dot); row 0 = insertions only, F_{0,j} = 2^s (Pi/2)^j
   const double Pt = 1.0 - Pi - Pd;
   // G = F / Pd^r grows by at most Pd^-n over the lattice: keep 2^s Pd^-n q M_n below FLT_MAX / 2^10
@@ -889,12 +946,13 @@ int bsidmap_plan_info(bsidmap_decoder* d, int F, char* buf, size_t len) {
       "\"lattice_grid\": [%ld, %d], \"lattice_block\": %d, \"alpha_beta_grid\": [%d, 2], \"alpha_beta_block\": %d, "
       "\"workspace_bytes\": %zu, \"windows_per_lane\": %d, \"q\": %d, \"n\": %d, \"N\": %d, \"Mn\": %d, \"Mtau\": %d, "
       "\"alpha_beta_overlap_subbatches\": %d, \"app_prefix_bits\": %d, \"app_windows_per_lane\": %d, "
-      "\"app_folded_rows\": %d}",
+      "\"app_folded_rows\": %d, \"app_live\": %d, \"app_frames_per_warp\": %d, \"live_eps\": %.6g}",
       sched_name(P.mode), F, P.chunk, P.nchunks, d->spec ? "spec" : "generic",
       d->kern.W == 2 ? ((long)P.chunk * tiles_per_frame(d->Mt) + kX2Warps - 1) / kX2Warps
                      : (lanes + kLatticeThreads - 1) / kLatticeThreads,
       d->N, kLatticeThreads, P.chunk, P.ab_warp ? kAbWarpThreads : P.ab_threads,
-      layout(d, P.chunk, P.mode).total, d->kern.W, d->q, d->n, d->N, d->Mn, d->Mt, std::min(P.ab_sub, P.chunk), P.app_kp, d->kern.app_W, P.app_ks);
+      layout(d, P.chunk, P.mode).total, d->kern.W, d->q, d->n, d->N, d->Mn, d->Mt, std::min(P.ab_sub, P.chunk), P.app_kp, P.app_live ? d->kern.app_live_W : d->kern.app_W, P.app_ks,
+      P.app_live ? 1 : 0, P.app_G, d->live_eps);
   return nb;
 }
 

@@ -13,28 +13,48 @@
 // pass 1 of those shapes stays on the pair class kernel at 3 CTAs/SM (k_lattice_x2.cuh; the scalar
 // class kernel measured slower: tools/exp_p1x2.sh)
 
-#define BSIDMAP_SPEC_UNIT(IDX, NN, LO, MN)                                               \
-  namespace bsidmap {                                                                    \
-  bool spec_unit_##IDX(int n, int lo, int Mn, CoreKernels* out) {                        \
-    if (n != NN || lo != LO || Mn != MN) return false;                                   \
-    *out = make_core_kernels_x2<SpecCoreX2<NN, LO, MN>>(SpecCoreX2<NN, LO, MN>::nodes()); \
-    out->ab_cta = k_alpha_beta_cta<MN>;                                                   \
-    local_cta_kernels<SpecCore<NN, LO, MN>>(out);                                          \
-    if (SpecCoreX2<NN, LO, MN>::kMinBlocks <= 2 && MN <= BSIDMAP_SCALAR_MN_MAX) { /* measured: scalar APP wins (C3, C5) */ \
-      out->app = k_app_x1<SpecCore<NN, LO, MN>, 0>;                                     \
-      out->app_pre[0] = k_app_x1<SpecCore<NN, LO, MN>, 2>;                              \
-      out->app_pre[1] = k_app_x1<SpecCore<NN, LO, MN>, 3>;                              \
-      out->app_pre[2] = k_app_x1<SpecCore<NN, LO, MN>, 4>;                              \
-      out->app_ks2 = k_app_x1<SpecCore<NN, LO, MN>, 0, 2>;                              \
-      out->app_pre_ks2[0] = k_app_x1<SpecCore<NN, LO, MN>, 2, 2>;                       \
-      out->app_pre_ks2[1] = k_app_x1<SpecCore<NN, LO, MN>, 3, 2>;                       \
-      out->app_pre_ks2[2] = k_app_x1<SpecCore<NN, LO, MN>, 4, 2>;                       \
-      /* fold two rows where the per-symbol tail is short (C3: 90.4 -> 85.6 ms; C5, n = 12: 110 -> 113) */ \
-      out->app_ks_auto = NN <= 10 ? 2 : 1;                                              \
-      out->app_W = 1;                                                                   \
-    }                                                                                   \
-    return true;                                                                         \
-  }                                                                                      \
+namespace bsidmap {
+// Kernel table of one fully unrolled shape (n, m_n^-, M_n).
+template <int NN, int LO, int MN>
+CoreKernels spec_kernels() {
+  CoreKernels k = make_core_kernels_x2<SpecCoreX2<NN, LO, MN>>(SpecCoreX2<NN, LO, MN>::nodes());
+  k.ab_cta = k_alpha_beta_cta<MN>;
+  local_cta_kernels<SpecCore<NN, LO, MN>>(&k);
+  if constexpr (SpecCoreX2<NN, LO, MN>::kMinBlocks <= 2 && MN <= BSIDMAP_SCALAR_MN_MAX) {
+    // register-heavy pair shapes: the scalar-core APP measured faster (C3, C5)
+    using S = SpecCore<NN, LO, MN>;
+    k.app = k_app_x1<S, 0>;
+    k.app_pre[0] = k_app_x1<S, 2>;
+    k.app_pre[1] = k_app_x1<S, 3>;
+    k.app_pre[2] = k_app_x1<S, 4>;
+    k.app_ks2 = k_app_x1<S, 0, 2>;
+    k.app_pre_ks2[0] = k_app_x1<S, 2, 2>;
+    k.app_pre_ks2[1] = k_app_x1<S, 3, 2>;
+    k.app_pre_ks2[2] = k_app_x1<S, 4, 2>;
+    // fold two rows where the per-symbol tail is short (C3: 90.4 -> 85.6 ms; C5, n = 12: 110 -> 113)
+    k.app_ks_auto = NN <= 10 ? 2 : 1;
+    k.app_live[0][0] = k_app_live_x1<S, 0, 1>;
+    k.app_live[0][1] = k_app_live_x1<S, 2, 1>;
+    k.app_live[0][2] = k_app_live_x1<S, 3, 1>;
+    k.app_live[0][3] = k_app_live_x1<S, 4, 1>;
+    k.app_live[1][0] = k_app_live_x1<S, 0, 2>;
+    k.app_live[1][1] = k_app_live_x1<S, 2, 2>;
+    k.app_live[1][2] = k_app_live_x1<S, 3, 2>;
+    k.app_live[1][3] = k_app_live_x1<S, 4, 2>;
+    k.app_live_W = 1;
+    k.app_W = 1;
+  }
+  return k;
+}
+}  // namespace bsidmap
+
+#define BSIDMAP_SPEC_UNIT(IDX, NN, LO, MN)                        \
+  namespace bsidmap {                                             \
+  bool spec_unit_##IDX(int n, int lo, int Mn, CoreKernels* out) { \
+    if (n != NN || lo != LO || Mn != MN) return false;            \
+    *out = spec_kernels<NN, LO, MN>();                            \
+    return true;                                                  \
+  }                                                               \
   }
 
 #define BSIDMAP_GEN_CASE(MN) \

@@ -306,6 +306,8 @@ struct CoreKernels {
   void (*app_ks2)(const DecodeParams);     // pair-core APP with the last two rows folded (KP = 0)
   void (*app_pre_ks2[3])(const DecodeParams);  // ... with prefix sharing KP = 2, 3, 4
   int app_ks_auto;                         // default folded rows of this core's APP kernel
+  void (*app_live[2][4])(const DecodeParams);  // live-window APP [KS - 1][KP = 0, 2, 3, 4] (spec only)
+  int app_live_W;                          // its windows per lane (1 scalar, 2 pair core)
   void (*app_stored)(const DecodeParams);
   void (*gamma_dump)(const DecodeParams);
   long nodes;  // corridor nodes per lattice (0 = generic core: computed on host)
@@ -333,6 +335,9 @@ CoreKernels make_core_kernels(long nodes) {
   k.app_ks2 = nullptr;
   k.app_ks_auto = 1;
   k.app_pre_ks2[0] = k.app_pre_ks2[1] = k.app_pre_ks2[2] = nullptr;
+  for (auto& r : k.app_live)
+    for (auto& fn : r) fn = nullptr;
+  k.app_live_W = 0;
   k.app_stored = k_app_stored<Core::Mn>;
   k.gamma_dump = k_gamma_dump<Core>;
   k.nodes = nodes;

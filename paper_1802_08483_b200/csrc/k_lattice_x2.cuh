@@ -723,6 +723,9 @@ __global__ void __launch_bounds__(kLatticeThreads) k_gamma_dump_x2(const DecodeP
 
 template <class Core>
 CoreKernels make_core_kernels_x2(long nodes);  // defined in k_local_x2.cuh (needs the local kernels)
+}  // namespace bsidmap
+#include "k_app_live.cuh"
+namespace bsidmap {
 
 template <class Core>
 CoreKernels make_core_kernels_x2_base(long nodes) {
@@ -741,6 +744,15 @@ CoreKernels make_core_kernels_x2_base(long nodes) {
   k.app_pre_ks2[0] = k_app_x2<Core, 2, 2>;
   k.app_pre_ks2[1] = k_app_x2<Core, 3, 2>;
   k.app_pre_ks2[2] = k_app_x2<Core, 4, 2>;
+  k.app_live[0][0] = k_app_live_x2<Core, 0, 1>;
+  k.app_live[0][1] = k_app_live_x2<Core, 2, 1>;
+  k.app_live[0][2] = k_app_live_x2<Core, 3, 1>;
+  k.app_live[0][3] = k_app_live_x2<Core, 4, 1>;
+  k.app_live[1][0] = k_app_live_x2<Core, 0, 2>;
+  k.app_live[1][1] = k_app_live_x2<Core, 2, 2>;
+  k.app_live[1][2] = k_app_live_x2<Core, 3, 2>;
+  k.app_live[1][3] = k_app_live_x2<Core, 4, 2>;
+  k.app_live_W = 2;
   k.app_stored = k_app_stored<Core::Mn>;
   k.gamma_dump = k_gamma_dump_x2<Core>;
   k.nodes = nodes;

@@ -65,6 +65,44 @@ __global__ void k_extrinsic(const DecodeParams p, float* E) {
   }
 }
 
+// Live windows of the APP pass (row a4, eqn:L).  Window (i, m') adds
+//   sum_k alpha_i(m') gamma_i(m', m'+k, D) beta_{i+1}(m'+k)
+// to S_i(D); summed over D and k that is alpha_i(m') beta~_i(m'), beta~_i the unnormalised beta_i of
+// eqn:beta -- c_i alpha_i(m') beta_i(m'), the posterior mass of drift m' at symbol boundary i times
+// the row constant c_i sum_m alpha_i beta_i = sum_D S_i(D).  A window with
+// alpha_i(m') beta_i(m') <= eps sum_m alpha_i(m) beta_i(m) therefore moves every L_i(D) by at most eps,
+// and all skipped windows together by at most M_tau eps (reading R18: eps = 2^-128, M_tau eps
+// < 1e-35, far below the 1e-4 relative gate at its 1e-30 floor; eps = 0 skips exact zeros only).
+// Writes the smallest state range holding every live window, its length rounded up to even (the pair
+// core runs two adjacent windows per lane).  One warp per (frame, i) row.
+__global__ void k_live(const DecodeParams p) {
+  const long row = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= (long)p.F * p.N) return;
+  const int f = (int)(row / p.N), i = (int)(row - (long)f * p.N);
+  int2 out = make_int2(0, 0);
+  if (p.status[f] == kFrameOk) {
+    const double* a = p.alpha + ((size_t)f * (p.N + 1) + i) * p.Mt;
+    const double* b = p.beta + ((size_t)f * (p.N + 1) + i) * p.Mt;
+    double s = 0.0;
+    for (int m = lane; m < p.Mt; m += 32) s += a[m] * b[m];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const double thr = s * p.live_eps;
+    int lo = 0x7fffffff, hi = -1;
+    for (int m = lane; m < p.Mt; m += 32) {
+      if (a[m] * b[m] > thr) {
+        lo = min(lo, m);
+        hi = max(hi, m);
+      }
+    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if (s > 0.0 && hi >= lo) out = make_int2(lo, (hi - lo + 2) & ~1);
+  }
+  if (lane == 0) p.live[row] = out;
+}
+
 // One warp per (frame, i) row.
 __global__ void k_finalize(const DecodeParams p) {
   const long row = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);

@@ -150,3 +150,36 @@ def test_cta_alpha_beta_ring_depth_bit_identical():
     np.testing.assert_array_equal(st2, st1)
     np.testing.assert_array_equal(L2, L1)
     assert_parity(L1, st1, run_oracle(cfg, b, frames=[0, 1]), frames=[0, 1])
+
+
+def _floor_priors(b, rng):
+    """Priors spanning ~30 decades: the transmitted symbol 1, every other symbol 10^-u with u drawn
+    in [12, 27] -- the oracle's L then has many entries between ~1e-35 and ~1e-20, around the 1e-30
+    floor of the relative-error gate (reading R11)."""
+    F, N = b.msg.shape
+    q = b.cfg.q
+    u = rng.uniform(12.0, 27.0, size=(F, N, q))
+    P = 10.0 ** -u
+    np.put_along_axis(P, b.msg[:, :, None].astype(np.int64), 1.0, axis=2)
+    P /= P.sum(2, keepdims=True)
+    return P.astype(np.float32)
+
+
+@pytest.mark.parametrize("name,N,frames", [("C2", 100, 6), ("C1", 10, 40), ("C5", 24, 2)])
+def test_app_dynamic_range_near_the_floor(name, N, frames):
+    """L entries near the 1e-30 floor (R11), fed by extreme priors and by low-weight windows
+    (windows far from the posterior drift carry alpha*beta weights many decades below the tile's
+    largest): the per-window FP32 terms, the FP64 sums over windows and symbols and the FP64
+    normalisation must hold the 1e-4 relative gate there too.  C2: one 64-state tile writes L
+    directly; C5's shape: several tiles per frame (FP64 atomics + k_finalize)."""
+    import dataclasses
+    cfg = dataclasses.replace(bsidgen.configs()[name], N=N, priors=True)
+    b = bsidgen.make_batch(cfg, 5, frames)
+    b.priors = _floor_priors(b, np.random.default_rng(11))
+    res = run_oracle(cfg, b)
+    Lo = np.concatenate([r["L"].ravel() for r in res])
+    near = ((Lo > 1e-34) & (Lo < 1e-26)).sum()
+    assert near >= 20, near   # the case really exercises the floor
+    for mode in (2, 3):
+        _, L, st = run_gpu(cfg, b, mode)
+        assert_parity(L, st, res)

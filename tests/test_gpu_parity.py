@@ -459,3 +459,67 @@ def test_decode_captures_into_cuda_graph():
     torch.cuda.synchronize()
     assert torch.equal(L, L_eager)
     assert (st == 0).all()
+
+
+# ------------------------------------------------------- live-window APP (k_live + k_app_live_*)
+
+def _cfg_n(name, N):
+    import dataclasses
+    cfg = bsidgen.configs()[name]
+    return cfg if N is None else dataclasses.replace(cfg, N=N)
+
+
+@pytest.mark.parametrize("name,N,frames,G", [
+    ("C1", None, 300, None), ("C2", None, 400, None), ("C2", None, 37, 3), ("C2", None, 9, 16),
+    ("C3", 40, 5, 2), ("C4", 30, 3, None), ("C5", 30, 5, 4), ("C5", 30, 3, 1)])
+def test_live_window_app(name, N, frames, G, monkeypatch):
+    """The APP over live windows only (reading R18): k_live marks each (frame, i) row's
+    windows with posterior mass above eps = 2^-128 of the row's, k_app_live_* packs G frames per
+    warp and walks their live windows in rounds.  Against the FP64 oracle at the north-star gate,
+    with eps = 0 (exactly-zero windows skipped only) and against the tiled APP over every window.
+    G = 16 with 9 frames: one warp, frames of every round count; 400 C2 frames: the automatic G."""
+    cfg = _cfg_n(name, N)
+    b = bsidgen.make_batch(cfg, 40, frames)
+    if G is not None:
+        monkeypatch.setenv("BSIDMAP_APP_G", str(G))
+    d, L, st = run_gpu(cfg, b, 3)
+    pl = d.plan(frames)
+    assert pl["app_live"] == 1 and pl["mode"] == "recompute-gammasum"
+    if G is not None:
+        assert pl["app_frames_per_warp"] == G
+    res = run_oracle(cfg, b)
+    assert_parity(L, st, res)
+    monkeypatch.setenv("BSIDMAP_LIVE_EPS", "0")
+    _, L0, st0 = run_gpu(cfg, b, 3)
+    assert_parity(L0, st0, res)
+    monkeypatch.delenv("BSIDMAP_LIVE_EPS")
+    monkeypatch.setenv("BSIDMAP_LIVE_APP", "0")
+    dt, Lt, stt = run_gpu(cfg, b, 3)
+    assert dt.plan(frames)["app_live"] == 0
+    np.testing.assert_array_equal(st, stt)
+    np.testing.assert_allclose(L, Lt, rtol=2e-5, atol=1e-34)
+
+
+def test_live_window_app_mixed_status():
+    """Frames whose end drift is out of range (status DRIFT_OUT_OF_RANGE: no live windows) and a
+    frame made UNDERFLOW sit between OK frames of one warp's G frames."""
+    cfg = small_cfg("C1", Pi=0.0, Pd=0.0, Ps=0.0, mn=(0, 0), mt=(-2, 2))
+    b = bsidgen.make_batch(cfg, 0, 12)
+    b.rho[3] = cfg.tau + 3                      # drift +3 > m_tau^+
+    b.rx = np.concatenate([b.rx, np.zeros((12, 2), np.uint32)], 1)
+    b.offsets = np.arange(12, dtype=np.int64) * b.rx.shape[1]
+    C0 = set(int(w) for w in b.C[0])
+    bad = next(w for w in range(1 << cfg.n) if w not in C0)
+    bits = b.bits(6)
+    bits[:cfg.n] = [(bad >> t) & 1 for t in range(cfg.n)]
+    b.rx[6] = bsidgen.pack_bits(bits, b.rx.shape[1])
+    import os as _os
+    _os.environ["BSIDMAP_APP_G"] = "8"
+    try:
+        d, L, st = run_gpu(cfg, b, 3)
+    finally:
+        del _os.environ["BSIDMAP_APP_G"]
+    assert d.plan(12)["app_live"] == 1
+    res = run_oracle(cfg, b)
+    assert st[3] == 1 and res[6]["status"] == oracle.UNDERFLOW and st[6] == 2
+    assert_parity(L, st, res)
