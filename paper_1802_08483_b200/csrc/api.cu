@@ -92,7 +92,6 @@ struct bsidmap_decoder {
   int app_kp = -1;                      // pass-2 prefix length override (-1 = automatic)
   int app_ks = -1;                      // rows folded into the APP weights (-1 = automatic; BSIDMAP_APP_KS)
   double live_eps = 0x1p-128;           // live-window threshold of the APP pass (reading R18; BSIDMAP_LIVE_EPS)
-  int live_app = 1;                     // live-window APP where the core has it (BSIDMAP_LIVE_APP=0: tiled APP)
   int app_G = 0;                        // its frames per warp (0 = automatic; BSIDMAP_APP_G)
   cudaStream_t s_ab = nullptr;
   cudaEvent_t ev_p1[kMaxAbSub] = {}, ev_ab[kMaxAbSub] = {};
@@ -146,13 +145,17 @@ int resolve_sched(const bsidmap_decoder* d, int mode) {
   return kSchedGammaSum;
 }
 
-// The Gamma-sum schedule runs the live-window APP (k_app_live.cuh) where the lattice core has one and
-// one frame per warp fits in shared memory (two folded rows: the larger tables).
-bool uses_live_app(const bsidmap_decoder* d, int sched) {
-  if (sched != kSchedGammaSum || !d->live_app || d->kern.app_live[0][0] == nullptr) return false;
-  const size_t need = d->kern.app_live_W == 2 ? kX2Warps * app_live_x2_warp_smem(d->q, d->Mn, 2, 1)
-                                              : app_live_x1_cta_tables(d->Mn, 2) + kX2Warps * app_live_x1_warp_smem(d->q, 1);
+// One frame per warp of the live-window APP with one folded row fits in shared memory.
+bool live_app_smem_fits(const CoreKernels& k, int q, int Mn) {
+  const size_t need = k.app_live_W == 2 ? kX2Warps * app_live_x2_warp_smem(q, Mn, 1, 1)
+                                        : app_live_x1_cta_tables(Mn, 1) + kX2Warps * app_live_x1_warp_smem(q, 1);
   return need <= 227u * 1024;
+}
+
+// The Gamma-sum schedule runs the live-window APP (k_app_live.cuh) on the spec cores.
+bool uses_live_app(const bsidmap_decoder* d, int sched) {
+  if (sched != kSchedGammaSum || d->kern.app_live[0][0] == nullptr) return false;
+  return live_app_smem_fits(d->kern, d->q, d->Mn);
 }
 
 const char* sched_name(int s) {
@@ -258,14 +261,6 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
     P->ab_warp = d->kern.ab_warp[k];
     P->ab_smem = ab_warp_bytes;
   }
-  const size_t nwin = kLatticeThreads;
-  P->app_smem = nwin * sizeof(double) + (size_t)kAppSegCap * std::min(d->q, kAppDChunk) * sizeof(double) +
-                nwin * app_tstride(d->q) * 4 + (size_t)d->q * 4;
-  if (mode != kSchedStored && d->kern.W == 2)
-    P->app_smem = d->kern.app_W == 2 ? app_x2_smem(d->q, d->Mn) : app_x1_smem(d->q);
-  // tiled APP with one warp tile per frame writes L directly (no accumulators / finalize)
-  P->direct_L = mode == kSchedLocal || mode == kSchedLocalCta ||
-                (mode == kSchedGammaSum && d->kern.W == 2 && tiles_per_frame_w(d->Mt, d->kern.app_W) == 1);
   P->local_smem = (size_t)kLocalWarps * local_warp_smem(d->Mn, d->q);
   if (mode == kSchedLocalCta) {  // CTA local schedule: the larger of the two passes' smem
     const int Mtp = (d->Mt + 3) & ~3;
@@ -273,42 +268,43 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   }
   // pass 1: hoist the last K lattice rows out of the symbol loop (K = 3 for q > 24, else 2)
   P->l1_kernel = (d->q > 24 && d->kern.gamma_sum_k3) ? d->kern.gamma_sum_k3 : d->kern.gamma_sum;
-  // pass 2: share lattice rows 1..KP between symbols with equal first KP codeword bits
-  P->app_kp = (mode == kSchedStored) ? 0 : app_prefix_bits(d->q, d->n);
-  if (d->app_kp >= 0) P->app_kp = (d->app_kp == 0 || d->app_kp > d->n - 2) ? 0 : std::min(4, std::max(2, d->app_kp));
-  P->app_kernel = (mode == kSchedStored) ? d->kern.app_stored : d->kern.app;
-  if (P->app_kp > 0 && d->kern.app_pre[P->app_kp - 2])
-    P->app_kernel = d->kern.app_pre[P->app_kp - 2];
-  else
-    P->app_kp = 0;
-  // last two lattice rows folded into the APP weights (pair core, four smem tables per lane)
+  // pass 2 (APP, row a4).  Local schedules: inside k_local_*_bwd.  Stored gamma: k_app_stored.
+  // Gamma-sum on a spec core: the live-window APP (k_app_live.cuh) -- only the windows of each
+  // (frame, i) row whose posterior mass exceeds eps (k_live), packed G frames per warp, the warps
+  // writing the L rows themselves.  Generic core: k_app (FP64 atomics into Lacc, then k_finalize).
+  P->direct_L = mode == kSchedLocal || mode == kSchedLocalCta;
+  P->app_kp = 0;
   P->app_ks = 1;
-  // automatic: only for the register-heavy pair cores (2 CTAs/SM anyway, so the two extra smem
-  // tables cost no occupancy): C4 pass 2 89.1 -> 84.9 ms; C2 (4 -> 3 CTAs/SM) 57.2 -> 69.7 ms
-  const int ks = d->app_ks > 0 ? d->app_ks : d->kern.app_ks_auto;
-  if (mode == kSchedGammaSum && d->kern.app_ks2 && ks == 2 && d->n >= 3) {
-    P->app_ks = 2;
-    P->app_kernel = P->app_kp > 0 ? d->kern.app_pre_ks2[P->app_kp - 2] : d->kern.app_ks2;
-    P->app_smem = d->kern.app_W == 2 ? app_x2_smem(d->q, d->Mn, 2) : app_x1_smem(d->q, d->Mn, 2);
-  }
-  // live-window APP (k_app_live.cuh): only the windows of each (frame, i) row whose posterior mass
-  // exceeds eps (k_live), packed G frames per warp; the warps write the L rows themselves
-  P->app_live = uses_live_app(d, mode);
+  P->app_live = false;
   P->app_G = 1;
-  if (P->app_live) {
+  const size_t nwin = kLatticeThreads;
+  P->app_smem = nwin * sizeof(double) + (size_t)kAppSegCap * std::min(d->q, kAppDChunk) * sizeof(double) +
+                nwin * app_tstride(d->q) * 4 + (size_t)d->q * 4;
+  P->app_kernel = mode == kSchedStored ? d->kern.app_stored : d->kern.app;
+  if (uses_live_app(d, mode)) {
+    P->app_live = true;
+    P->direct_L = true;
+    // share lattice rows 1..KP between symbols with equal first KP codeword bits
+    P->app_kp = app_prefix_bits(d->q, d->n);
+    if (d->app_kp >= 0) P->app_kp = (d->app_kp == 0 || d->app_kp > d->n - 2) ? 0 : std::min(4, std::max(2, d->app_kp));
+    // fold the last two lattice rows into the weights (four tables per lane in smem) for the
+    // register-heavy cores (2 CTAs/SM anyway: C4 89.1 -> 84.9 ms, C3 90.4 -> 85.6 ms; C2 at 4 -> 3
+    // CTAs/SM 57.2 -> 69.7 ms, tiled kernels of round 1)
+    const int ks = d->app_ks > 0 ? d->app_ks : d->kern.app_ks_auto;
+    P->app_ks = (ks == 2 && d->n >= 3) ? 2 : 1;
+    auto smem = [&](int ksv, int g) {
+      return d->kern.app_live_W == 2 ? kX2Warps * app_live_x2_warp_smem(d->q, d->Mn, ksv, g)
+                                     : app_live_x1_cta_tables(d->Mn, ksv) + kX2Warps * app_live_x1_warp_smem(d->q, g);
+    };
+    if (smem(P->app_ks, 1) > 227u * 1024) P->app_ks = 1;
     // up to 8 frames per warp (fewer partly filled rounds); fewer where the grid would not fill the
     // GPU or the per-frame sums would not fit in shared memory
     const long rows = (long)chunk * d->N;
     int G = d->app_G > 0 ? std::min(d->app_G, kLiveMaxG) : (int)std::max(1L, std::min(8L, rows / (32L * d->num_sms)));
-    auto smem = [&](int g) {
-      return d->kern.app_live_W == 2 ? kX2Warps * app_live_x2_warp_smem(d->q, d->Mn, P->app_ks, g)
-                                     : app_live_x1_cta_tables(d->Mn, P->app_ks) + kX2Warps * app_live_x1_warp_smem(d->q, g);
-    };
-    while (G > 1 && smem(G) > 227u * 1024) G--;
+    while (G > 1 && smem(P->app_ks, G) > 227u * 1024) G--;
     P->app_kernel = d->kern.app_live[P->app_ks - 1][P->app_kp > 0 ? P->app_kp - 1 : 0];
     P->app_G = G;
-    P->app_smem = smem(G);
-    P->direct_L = true;
+    P->app_smem = smem(P->app_ks, G);
   }
   // alpha/beta overlap (Gamma-sum only): measured on B200 it only pays where the alpha/beta grid
   // cannot fill the GPU (one CTA per frame and direction, 2F <= #SMs: C5 at 32 frames/GPU,
@@ -488,14 +484,11 @@ void launch_pass2(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_
     return;
   }
   const long lanes = (long)p.F * d->Mt;
-  const unsigned gx_tile =
-      (unsigned)(((long)p.F * tiles_per_frame_w(d->Mt, d->kern.app_W) + kX2Warps - 1) / kX2Warps);
   const unsigned gx_flat = (unsigned)((lanes + kLatticeThreads - 1) / kLatticeThreads);
-  const unsigned gx = d->kern.W == 2 ? gx_tile : gx_flat;
   auto l2 = P.app_kernel;
   for_i_slices(d->N, [&](int i0, int ni) {
     p.i_base = i0;
-    l2<<<dim3(P.mode == kSchedStored ? gx_flat : gx, ni), kLatticeThreads, P.app_smem, s>>>(p);
+    l2<<<dim3(gx_flat, ni), kLatticeThreads, P.app_smem, s>>>(p);
     d->launches++;
   });
 }
@@ -691,7 +684,6 @@ int bsidmap_create(bsidmap_decoder** out, int q, int n, int N, const uint32_t* c
   if (const char* v = std::getenv("BSIDMAP_APP_KP")) d->app_kp = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("BSIDMAP_APP_KS")) d->app_ks = std::atoi(v) == 2 ? 2 : 1;
   if (const char* v = std::getenv("BSIDMAP_LIVE_EPS")) d->live_eps = std::max(0.0, std::atof(v));
-  if (const char* v = std::getenv("BSIDMAP_LIVE_APP")) d->live_app = std::atoi(v) != 0;
   if (const char* v = std::getenv("BSIDMAP_APP_G")) d->app_G = std::max(0, std::atoi(v));
   // lattice constants (eqn:F, Q-dot); row 0 = insertions only, F_{0,j} = 2^s (Pi/2)^j
   const double Pt = 1.0 - Pi - Pd;
@@ -711,9 +703,9 @@ int bsidmap_create(bsidmap_decoder** out, int q, int n, int N, const uint32_t* c
     const int j = mn_lo + e;
     d->lc.row0[e] = (e < Mn && j >= 0) ? (float)std::ldexp(std::pow(0.5 * Pi, j), seed) : 0.f;
   }
-  // the specialised APP kernels stage one float per (symbol, lane) in shared memory (~544 q bytes
-  // per CTA): very large alphabets use the generic core, whose APP pass stages symbols in chunks
-  d->spec = rescaled && (size_t)q * 544 + 64 * 1024 <= 227u * 1024 && find_spec_kernels(n, mn_lo, Mn, &d->kern);
+  // the spec cores' APP (k_app_live.cuh) stages per-symbol terms in shared memory: very large
+  // alphabets use the generic core, whose APP pass stages symbols in chunks
+  d->spec = rescaled && find_spec_kernels(n, mn_lo, Mn, &d->kern) && live_app_smem_fits(d->kern, q, Mn);
   if (!d->spec && !find_generic_kernels(Mn, &d->kern)) {
     delete d;
     return fail(nullptr, BSIDMAP_EPLAN, "no lattice core for M_n = " + std::to_string(Mn));
@@ -951,7 +943,7 @@ int bsidmap_plan_info(bsidmap_decoder* d, int F, char* buf, size_t len) {
       d->kern.W == 2 ? ((long)P.chunk * tiles_per_frame(d->Mt) + kX2Warps - 1) / kX2Warps
                      : (lanes + kLatticeThreads - 1) / kLatticeThreads,
       d->N, kLatticeThreads, P.chunk, P.ab_warp ? kAbWarpThreads : P.ab_threads,
-      layout(d, P.chunk, P.mode).total, d->kern.W, d->q, d->n, d->N, d->Mn, d->Mt, std::min(P.ab_sub, P.chunk), P.app_kp, P.app_live ? d->kern.app_live_W : d->kern.app_W, P.app_ks,
+      layout(d, P.chunk, P.mode).total, d->kern.W, d->q, d->n, d->N, d->Mn, d->Mt, std::min(P.ab_sub, P.chunk), P.app_kp, P.app_live ? d->kern.app_live_W : 1, P.app_ks,
       P.app_live ? 1 : 0, P.app_G, d->live_eps);
   return nb;
 }

@@ -23,14 +23,6 @@ CoreKernels spec_kernels() {
   if constexpr (SpecCoreX2<NN, LO, MN>::kMinBlocks <= 2 && MN <= BSIDMAP_SCALAR_MN_MAX) {
     // register-heavy pair shapes: the scalar-core APP measured faster (C3, C5)
     using S = SpecCore<NN, LO, MN>;
-    k.app = k_app_x1<S, 0>;
-    k.app_pre[0] = k_app_x1<S, 2>;
-    k.app_pre[1] = k_app_x1<S, 3>;
-    k.app_pre[2] = k_app_x1<S, 4>;
-    k.app_ks2 = k_app_x1<S, 0, 2>;
-    k.app_pre_ks2[0] = k_app_x1<S, 2, 2>;
-    k.app_pre_ks2[1] = k_app_x1<S, 3, 2>;
-    k.app_pre_ks2[2] = k_app_x1<S, 4, 2>;
     // fold two rows where the per-symbol tail is short (C3: 90.4 -> 85.6 ms; C5, n = 12: 110 -> 113)
     k.app_ks_auto = NN <= 10 ? 2 : 1;
     k.app_live[0][0] = k_app_live_x1<S, 0, 1>;
@@ -42,7 +34,6 @@ CoreKernels spec_kernels() {
     k.app_live[1][2] = k_app_live_x1<S, 3, 2>;
     k.app_live[1][3] = k_app_live_x1<S, 4, 2>;
     k.app_live_W = 1;
-    k.app_W = 1;
   }
   return k;
 }

@@ -302,9 +302,6 @@ struct CoreKernels {
   void (*gamma_sum_k3_pri)(const DecodeParams);  // plain kernels read priors themselves)
   void (*gamma_store)(const DecodeParams);
   void (*app)(const DecodeParams);
-  void (*app_pre[3])(const DecodeParams);  // APP with prefix sharing, KP = 2, 3, 4 first codeword bits (spec only)
-  void (*app_ks2)(const DecodeParams);     // pair-core APP with the last two rows folded (KP = 0)
-  void (*app_pre_ks2[3])(const DecodeParams);  // ... with prefix sharing KP = 2, 3, 4
   int app_ks_auto;                         // default folded rows of this core's APP kernel
   void (*app_live[2][4])(const DecodeParams);  // live-window APP [KS - 1][KP = 0, 2, 3, 4] (spec only)
   int app_live_W;                          // its windows per lane (1 scalar, 2 pair core)
@@ -314,7 +311,6 @@ struct CoreKernels {
   int W;       // windows per lane (1 scalar core, 2 packed-pair core)
   int l1_W;    // windows per lane of the pass-1 kernel (the scalar core may serve pass 1 of a pair core)
   bool l1_steps;  // the pass-1 (non-stored) kernels walk kL1Steps symbol indices per CTA
-  int app_W;   // windows per lane of the tiled APP kernel (32 * app_W states per warp tile)
   void (*ab_warp[3])(const DecodeParams);  // warp-per-task alpha/beta for M_tau <= 32, 64, 128 (spec only)
   void (*ab_cta)(const DecodeParams, int);  // CTA-per-task alpha/beta with compile-time M_n (spec only)
   void (*local_fwd)(const DecodeParams);   // fused local schedule, M_tau <= 64 (spec only)
@@ -331,10 +327,7 @@ CoreKernels make_core_kernels(long nodes) {
   k.gamma_sum_pri = k.gamma_sum_k3_pri = nullptr;
   k.gamma_store = k_gamma_sum<Core, true>;
   k.app = k_app<Core>;
-  k.app_pre[0] = k.app_pre[1] = k.app_pre[2] = nullptr;
-  k.app_ks2 = nullptr;
   k.app_ks_auto = 1;
-  k.app_pre_ks2[0] = k.app_pre_ks2[1] = k.app_pre_ks2[2] = nullptr;
   for (auto& r : k.app_live)
     for (auto& fn : r) fn = nullptr;
   k.app_live_W = 0;
@@ -343,7 +336,6 @@ CoreKernels make_core_kernels(long nodes) {
   k.nodes = nodes;
   k.W = 1;
   k.l1_W = 1;
-  k.app_W = 1;
   k.ab_warp[0] = k.ab_warp[1] = k.ab_warp[2] = nullptr;
   k.local_fwd = k.local_bwd = nullptr;
   k.ab_cta = nullptr;

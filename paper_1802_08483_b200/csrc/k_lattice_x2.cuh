@@ -375,317 +375,24 @@ __device__ __forceinline__ void app_weights_pair(const DecodeParams& p, const La
   db = (B.active && hb > 0) ? arow[B.mi] * pow2d(Eb) : 0.0;
 }
 
-// APP pass: 5 CTAs/SM (102 registers; the beta corridor lives in smem) with row pairs measured
-// fastest on B200 for C2 (tools/exp_app.sh: 17.06 ms vs 17.3-18.0 ms for 3-4 CTAs/SM)
-#ifndef BSIDMAP_APP_MINB
-#define BSIDMAP_APP_MINB (Core::kMinBlocks > 2 ? 5 : 2)
-#endif
+// Lattice rows per dispatch group in the APP kernels (row pairs where the register budget allows
+// 3 CTAs/SM)
 #ifndef BSIDMAP_APP_GROUP
 #define BSIDMAP_APP_GROUP (Core::kMinBlocks > 2 ? 2 : 1)
 #endif
-// per-warp staging of the per-lane contributions c(lane, D): [q][33] floats (odd stride), reduced
-// over the lanes once after the D loop instead of one shuffle chain per D
+// the APP kernels with two folded rows: four weight tables per lane in smem
+#ifndef BSIDMAP_APP_MINB_KS2
+#define BSIDMAP_APP_MINB_KS2 (Core::kMinBlocks > 2 ? 3 : 2)
+#endif
+// per-warp staging of per-lane, per-symbol terms: [q][33] (odd stride), reduced over the lanes once
+// after the symbol loop instead of one shuffle chain per symbol
 __host__ __device__ __forceinline__ size_t app_stage_floats(int q) { return (size_t)q * 33; }
-__host__ __device__ __forceinline__ size_t app_x2_smem(int q, int Mn, int ks = 1) {
-  return (size_t)kX2Warps * (2 << (ks - 1)) * Mn * 32 * 8 + (size_t)kX2Warps * (app_stage_floats(q) * 4 + (size_t)q * 8);
-}
 // Symbols are visited in lexicographic codeword order (DecodeParams::Cp, prepared at create) so
 // that lattice rows 1..KP (run_head) are computed once per distinct prefix; KP = 0: natural order.
 // The prefix length that saves the most nodes for random codebooks: ~log2(q) - 1.
 __host__ __device__ __forceinline__ int app_prefix_bits(int q, int n) {
   int kp = q <= 8 ? 2 : q <= 16 ? 3 : 4;
   return kp <= n - 2 ? kp : 0;
-}
-// smem: s_w[kX2Warps][2][M_n][32] (f32x2: the scaled beta corridor of each lane's two windows with
-//       the last lattice row folded in, one table per value of x_n; smem, not registers) |
-//       s_S[kX2Warps][q] (double) | staging [kX2Warps][q][33] (float)
-// prefix sharing keeps the head row live across the symbol loop (+2 M_n registers)
-#ifndef BSIDMAP_APP_MINB_PRE
-#define BSIDMAP_APP_MINB_PRE (Core::kMinBlocks > 2 ? 4 : 2)
-#endif
-// KS = lattice rows folded into the APP weights: 1 = the last row (two tables, by x_n); 2 = the
-// last two rows (four tables, by (x_{n-1}, x_n); row n-1 transposed by SpecCoreX2::row_transpose),
-// so each symbol runs rows 1..n-2 only.  Exact re-association (the rows are linear maps).
-// the weight dot inside the basic block of the last lattice row (rows_then), so it interleaves
-// with the row's insertion chain instead of running as a dependent tail after the branch merge
-#ifndef BSIDMAP_APP_MINB_KS2
-#define BSIDMAP_APP_MINB_KS2 (Core::kMinBlocks > 2 ? 3 : 2)
-#endif
-template <class Core, int KP, int KS = 1>
-__global__ void __launch_bounds__(kLatticeThreads, KS == 2 ? BSIDMAP_APP_MINB_KS2
-                                                           : (KP > 0 ? BSIDMAP_APP_MINB_PRE : BSIDMAP_APP_MINB))
-    k_app_x2(const DecodeParams p) {
-  constexpr int MN = Core::Mn;
-  constexpr int NT = 2 << (KS - 1);  // weight tables per lane
-  constexpr int RL = Core::NNr - KS;  // last lattice row run per symbol
-  extern __shared__ __align__(128) unsigned char smem[];
-  f32x2* s_bt = reinterpret_cast<f32x2*>(smem);
-  double* s_S = reinterpret_cast<double*>(s_bt + kX2Warps * NT * MN * 32);
-  float* s_stage = reinterpret_cast<float*>(s_S + kX2Warps * p.q);
-  const int i = blockIdx.y + p.i_base;
-  // KP > 0: symbols in lexicographic codeword order (prefix groups contiguous); every smem array
-  // below is per warp, so the kernel has no block barrier
-  const uint32_t* Ci = (KP > 0 ? p.Cp : p.C) + (size_t)i * p.q;
-  const uint16_t* Di = p.Dp + (size_t)i * p.q;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int T = tiles_per_frame(p.Mt);
-  const long tile = (long)blockIdx.x * kX2Warps + warp;
-  const int f = (int)(tile / T);
-  if (f >= p.F) return;  // warp-uniform; no block barrier follows
-  const int mia = (int)(tile % T) * kTileSlots + 2 * lane;
-  const LaneGeom A = geom_fm(p, i, f, mia, mia < p.Mt);
-  const LaneGeom B = geom_fm(p, i, f, mia + 1, mia + 1 < p.Mt);
-  const bool frame_ok = p.status[f] == kFrameOk;
-
-  // KS = 1: w1[e] at wt[e*32], w0[e] at wt[(MN+e)*32]; KS = 2: table c = 2 [x_n = 0] + [x_{n-1} = 0]
-  f32x2* wt = s_bt + (size_t)warp * NT * MN * 32 + lane;
-  float wa, wb;
-  int Emax;
-  f32x2 bt[MN];
-  {
-    float ba[MN], bb[MN];
-    double da, db;
-    app_weights_pair<MN>(p, A, B, i, ba, bb, da, db);
-#pragma unroll
-    for (int e = 0; e < MN; e++) bt[e] = pk(ba[e], bb[e]);
-    // common power-of-two scale of the tile's weights (max exponent over the warp)
-    const double dm = fmax(da, db);
-    Emax = __reduce_max_sync(0xffffffffu, dm > 0.0 ? exp2_of(dm) + 2048 : 0) - 2048;
-    const double sc = pow2d(-Emax);
-    wa = (float)(da * sc);
-    wb = (float)(db * sc);
-  }
-  const bool live = __any_sync(0xffffffffu, wa > 0.f || wb > 0.f);
-  double* S = s_S + warp * p.q;
-  float* stg = s_stage + (size_t)warp * app_stage_floats(p.q);
-  if (live) {
-    typename Core::Lane lane_t;
-    Core::init(lane_t, A.active ? load_window(p, A.f, A.s, A.rho) : 0ull,
-               B.active ? load_window(p, B.f, B.s, B.rho) : 0ull, p);
-    if constexpr (KS == 1) {
-      Core::last_row_weights(lane_t, [&](int e) { return bt[e]; }, [&](int e) -> f32x2& { return wt[e * 32]; },
-                             [&](int e) -> f32x2& { return wt[(MN + e) * 32]; });
-    } else {
-      f32x2 w1[MN], w0[MN], wi[MN];
-      Core::last_row_weights(lane_t, [&](int e) { return bt[e]; }, [&](int e) -> f32x2& { return w1[e]; },
-                             [&](int e) -> f32x2& { return w0[e]; });
-      const f32x2 a2 = pk(p.lc.a, p.lc.a);
-      Core::template row_transpose<Core::NNr - 1>(w1, wi, lane_t.q1, a2);  // (x_{n-1}, x_n) = (1, 1)
-#pragma unroll
-      for (int e = 0; e < MN; e++) wt[e * 32] = wi[e];
-      Core::template row_transpose<Core::NNr - 1>(w1, wi, lane_t.q0, a2);  // (0, 1)
-#pragma unroll
-      for (int e = 0; e < MN; e++) wt[(MN + e) * 32] = wi[e];
-      Core::template row_transpose<Core::NNr - 1>(w0, wi, lane_t.q1, a2);  // (1, 0)
-#pragma unroll
-      for (int e = 0; e < MN; e++) wt[(2 * MN + e) * 32] = wi[e];
-      Core::template row_transpose<Core::NNr - 1>(w0, wi, lane_t.q0, a2);  // (0, 0)
-#pragma unroll
-      for (int e = 0; e < MN; e++) wt[(3 * MN + e) * 32] = wi[e];
-    }
-    const float* pri = p.priors ? p.priors + ((size_t)f * p.N + i) * p.q : nullptr;
-    const int nb = p.n - 1;
-    f32x2 fh[MN];  // rows 1..KP of the current prefix
-    XPrefetch xs(Ci, 0, p.q);
-    uint32_t xprev = 0u;
-    for (int k = 0; k < p.q; k++) {
-      const uint32_t x = xs.take(k);
-      f32x2 fo[MN];
-      // t(m', D) = sum_k G_n(m', k, D) bt(m', k) = sum_e G_{n-KS}[e] w[e]  (two chains)
-      const f32x2* W = KS == 1 ? wt + (((x >> nb) & 1u) ? 0 : MN * 32)
-                               : wt + (size_t)((((x >> nb) & 1u) ? 0 : 2) + (((x >> (nb - 1)) & 1u) ? 0 : 1)) * MN * 32;
-      f32x2 t0 = 0ull, t1 = 0ull;
-      auto dot = [&](const f32x2 (&g)[MN]) {
-#pragma unroll
-        for (int e = 0; e < MN; e += 2) {
-          t0 = ffma2(g[e], W[e * 32], t0);
-          if (e + 1 < MN) t1 = ffma2(g[e + 1], W[(e + 1) * 32], t1);
-        }
-      };
-      if constexpr (KP > 0) {
-        if (k == 0 || ((x ^ xprev) & ((1u << KP) - 1u)) != 0u)
-          Core::template run_head<KP, BSIDMAP_APP_GROUP>(lane_t, x, p, fh);
-        xprev = x;
-#pragma unroll
-        for (int e = 0; e < MN; e++) fo[e] = fh[e];
-        Core::template run_tail_to_then<KP, RL, BSIDMAP_APP_GROUP>(lane_t, x, p, fo, dot);
-      } else {
-        Core::template run_to_then<RL, BSIDMAP_APP_GROUP>(lane_t, x, p, fo, dot);
-      }
-      const int D = KP > 0 ? (int)Di[k] : k;
-      stg[D * 33 + lane] = fmaf(wa, lo_of(t0) + lo_of(t1), wb * (hi_of(t0) + hi_of(t1)));
-    }
-    __syncwarp();
-    for (int D = lane; D < p.q; D += 32) {  // S(D) = P(D) sum over the warp's windows (FP64)
-      double c = 0.0;
-#pragma unroll 8
-      for (int l = 0; l < 32; l++) c += (double)stg[D * 33 + l];
-      S[D] = pri ? c * (double)__ldg(pri + D) : c;
-    }
-  }
-  __syncwarp();
-  if (T == 1) {
-    // the warp holds the whole sum over m': L_i(D) = S(D) / sum_D S(D)
-    double tot = 0.0;
-    if (live)
-      for (int D = lane; D < p.q; D += 32) tot += S[D];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    const bool ok = frame_ok && live && tot > 0.0;
-    const double inv = ok ? 1.0 / tot : 0.0;
-    float* Lrow = p.L + ((size_t)f * p.N + i) * p.q;
-    for (int D = lane; D < p.q; D += 32) Lrow[D] = ok ? (float)(S[D] * inv) : 0.f;
-    if (frame_ok && !ok && lane == 0) p.status[f] = kFrameUnderflow;
-  } else if (live) {
-    const double sc = pow2d(Emax);
-    double* acc = p.Lacc + ((size_t)f * p.N + i) * p.q;
-    for (int D = lane; D < p.q; D += 32) {
-      const double v = S[D];
-      if (v > 0.0) atomicAdd(acc + D, v * sc);
-    }
-  }
-}
-
-// Scalar-core APP on frame-aligned 32-state warp tiles (one window per lane): used where the
-// pair core is register-bound (C3, C5) -- also wastes fewer slots (C3: 9 x 32 vs 5 x 64 for 267).
-__host__ __device__ __forceinline__ int tiles_per_frame_w(int Mt, int W) { return (Mt + 32 * W - 1) / (32 * W); }
-__host__ __device__ __forceinline__ size_t app_x1_smem(int q, int Mn = 0, int ks = 1) {
-  return (size_t)kX2Warps * (app_stage_floats(q) * 4 + (size_t)q * 8) + (ks == 2 ? (size_t)4 * Mn * kLatticeThreads * 4 : 0);
-}
-
-#ifndef BSIDMAP_APP1_MINB_PRE
-#define BSIDMAP_APP1_MINB_PRE 3
-#endif
-// KS = 2: the last two rows folded into four per-lane weight tables in shared memory (see k_app_x2)
-template <class Core, int KP, int KS = 1>
-__global__ void __launch_bounds__(kLatticeThreads, (KP > 0 || KS == 2) ? BSIDMAP_APP1_MINB_PRE : kLatticeMinBlocks)
-    k_app_x1(const DecodeParams p) {
-  constexpr int MN = Core::Mn;
-  constexpr int RL = Core::NNr - KS;  // last lattice row run per symbol
-  extern __shared__ __align__(128) unsigned char smem[];
-  double* s_S = reinterpret_cast<double*>(smem);
-  float* s_stage = reinterpret_cast<float*>(s_S + kX2Warps * p.q);
-  float* s_w = s_stage + (size_t)kX2Warps * app_stage_floats(p.q) + threadIdx.x;  // KS = 2: [4][MN][128]
-  const int i = blockIdx.y + p.i_base;
-  const uint32_t* Ci = (KP > 0 ? p.Cp : p.C) + (size_t)i * p.q;
-  const uint16_t* Di = p.Dp + (size_t)i * p.q;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int T = tiles_per_frame_w(p.Mt, 1);
-  const long tile = (long)blockIdx.x * kX2Warps + warp;
-  const int f = (int)(tile / T);
-  if (f >= p.F) return;  // warp-uniform; no block barrier follows
-  const int mi = (int)(tile % T) * 32 + lane;
-  const LaneGeom A = geom_fm(p, i, f, mi, mi < p.Mt);
-  const bool frame_ok = p.status[f] == kFrameOk;
-  float bt[MN];
-  float wa;
-  int Emax;
-  {
-    const double da = app_weights_p2<MN>(p, A, i, bt);  // bt: corridor weights (see app_weights_p2)
-    Emax = __reduce_max_sync(0xffffffffu, da > 0.0 ? exp2_of(da) + 2048 : 0) - 2048;
-    wa = (float)(da * pow2d(-Emax));
-  }
-  const bool live = __any_sync(0xffffffffu, wa > 0.f);
-  double* S = s_S + warp * p.q;
-  float* stg = s_stage + (size_t)warp * app_stage_floats(p.q);
-  if (live) {
-    typename Core::Lane lane_t;
-    Core::init(lane_t, A.active ? load_window(p, A.f, A.s, A.rho) : 0ull, p);
-    float w1[MN], w0[MN];  // last lattice row folded into the weights (one table per x_n)
-    Core::last_row_weights(lane_t, bt, w1, w0);
-    if constexpr (KS == 2) {  // table c = 2 [x_n = 0] + [x_{n-1} = 0], entry e at s_w[(c MN + e) 128]
-      float wi[MN];
-      Core::template row_transpose<Core::NNr - 1>(w1, wi, lane_t.q1, p.lc.a);
-#pragma unroll
-      for (int e = 0; e < MN; e++) s_w[e * kLatticeThreads] = wi[e];
-      Core::template row_transpose<Core::NNr - 1>(w1, wi, lane_t.q0, p.lc.a);
-#pragma unroll
-      for (int e = 0; e < MN; e++) s_w[(MN + e) * kLatticeThreads] = wi[e];
-      Core::template row_transpose<Core::NNr - 1>(w0, wi, lane_t.q1, p.lc.a);
-#pragma unroll
-      for (int e = 0; e < MN; e++) s_w[(2 * MN + e) * kLatticeThreads] = wi[e];
-      Core::template row_transpose<Core::NNr - 1>(w0, wi, lane_t.q0, p.lc.a);
-#pragma unroll
-      for (int e = 0; e < MN; e++) s_w[(3 * MN + e) * kLatticeThreads] = wi[e];
-    }
-    const float* pri = p.priors ? p.priors + ((size_t)f * p.N + i) * p.q : nullptr;
-    const int nb = p.n - 1;
-    float fh[MN];  // rows 1..KP of the current prefix
-    XPrefetch xs(Ci, 0, p.q);
-    uint32_t xprev = 0u;
-    for (int k = 0; k < p.q; k++) {
-      const uint32_t x = xs.take(k);
-      const int D = KP > 0 ? (int)Di[k] : k;
-      float fo[MN];
-      float t0 = 0.f, t1 = 0.f;
-      // KS = 2: the table dot fused into the last row's basic block (rows_then); KS = 1: after it
-      const float* W = s_w + (size_t)((((x >> nb) & 1u) ? 0 : 2) + (((x >> (nb - 1)) & 1u) ? 0 : 1)) * MN * kLatticeThreads;
-      auto dot = [&](const float (&g)[MN]) {
-        if constexpr (KS == 2) {
-#pragma unroll
-          for (int e = 0; e < MN; e += 2) {
-            t0 = fmaf(g[e], W[e * kLatticeThreads], t0);
-            if (e + 1 < MN) t1 = fmaf(g[e + 1], W[(e + 1) * kLatticeThreads], t1);
-          }
-        }
-      };
-      if constexpr (KP > 0) {
-        if (k == 0 || ((x ^ xprev) & ((1u << KP) - 1u)) != 0u) Core::template run_head<KP>(lane_t, x, p, fh);
-        xprev = x;
-#pragma unroll
-        for (int e = 0; e < MN; e++) fo[e] = fh[e];
-        if constexpr (KS == 2) Core::template run_tail_to_then<KP, RL>(lane_t, x, p, fo, dot);
-        else Core::template run_tail_to<KP, RL>(lane_t, x, p, fo);
-      } else {
-        if constexpr (KS == 2) Core::template run_to_then<RL>(lane_t, x, p, fo, dot);
-        else Core::template run_to<RL>(lane_t, x, p, fo);
-      }
-      if constexpr (KS == 2) {
-      } else if ((x >> nb) & 1u) {
-#pragma unroll
-        for (int e = 0; e < MN; e += 2) {
-          t0 = fmaf(fo[e], w1[e], t0);
-          if (e + 1 < MN) t1 = fmaf(fo[e + 1], w1[e + 1], t1);
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < MN; e += 2) {
-          t0 = fmaf(fo[e], w0[e], t0);
-          if (e + 1 < MN) t1 = fmaf(fo[e + 1], w0[e + 1], t1);
-        }
-      }
-      stg[D * 33 + lane] = wa * (t0 + t1);
-    }
-    __syncwarp();
-    for (int D = lane; D < p.q; D += 32) {  // FP64, as k_app_x2
-      double c = 0.0;
-#pragma unroll 8
-      for (int l = 0; l < 32; l++) c += (double)stg[D * 33 + l];
-      S[D] = pri ? c * (double)__ldg(pri + D) : c;
-    }
-  }
-  __syncwarp();
-  if (T == 1) {
-    double tot = 0.0;
-    if (live)
-      for (int D = lane; D < p.q; D += 32) tot += S[D];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    const bool ok = frame_ok && live && tot > 0.0;
-    const double inv = ok ? 1.0 / tot : 0.0;
-    float* Lrow = p.L + ((size_t)f * p.N + i) * p.q;
-    for (int D = lane; D < p.q; D += 32) Lrow[D] = ok ? (float)(S[D] * inv) : 0.f;
-    if (frame_ok && !ok && lane == 0) p.status[f] = kFrameUnderflow;
-  } else if (live) {
-    const double sc = pow2d(Emax);
-    double* acc = p.Lacc + ((size_t)f * p.N + i) * p.q;
-    for (int D = lane; D < p.q; D += 32) {
-      const double v = S[D];
-      if (v > 0.0) atomicAdd(acc + D, v * sc);
-    }
-  }
 }
 
 template <class Core>
@@ -735,15 +442,8 @@ CoreKernels make_core_kernels_x2_base(long nodes) {
   k.gamma_sum_pri = k_gamma_sum_x2_cls<Core, 2, true>;
   k.gamma_sum_k3_pri = k_gamma_sum_x2_cls<Core, 3, true>;
   k.gamma_store = k_gamma_sum_x2<Core, true>;
-  k.app = k_app_x2<Core, 0>;
-  k.app_pre[0] = k_app_x2<Core, 2>;
-  k.app_pre[1] = k_app_x2<Core, 3>;
-  k.app_pre[2] = k_app_x2<Core, 4>;
-  k.app_ks2 = k_app_x2<Core, 0, 2>;
+  k.app = nullptr;
   k.app_ks_auto = Core::kMinBlocks <= 2 ? 2 : 1;
-  k.app_pre_ks2[0] = k_app_x2<Core, 2, 2>;
-  k.app_pre_ks2[1] = k_app_x2<Core, 3, 2>;
-  k.app_pre_ks2[2] = k_app_x2<Core, 4, 2>;
   k.app_live[0][0] = k_app_live_x2<Core, 0, 1>;
   k.app_live[0][1] = k_app_live_x2<Core, 2, 1>;
   k.app_live[0][2] = k_app_live_x2<Core, 3, 1>;
@@ -759,7 +459,6 @@ CoreKernels make_core_kernels_x2_base(long nodes) {
   k.W = 2;
   k.l1_W = 2;
   k.l1_steps = true;
-  k.app_W = 2;
   k.ab_warp[0] = k_alpha_beta_warp<1, Core::Mn>;
   k.ab_warp[1] = k_alpha_beta_warp<2, Core::Mn>;
   k.ab_warp[2] = k_alpha_beta_warp<4, Core::Mn>;

@@ -107,8 +107,9 @@ __global__ void __launch_bounds__(kLocalWarps * 32, Core::kMinBlocks) k_local_fw
   }
 }
 
+// 5 CTAs/SM where the pair core allows 3 (as the round-1 tiled APP kernel it derives from)
 template <class Core>
-__global__ void __launch_bounds__(kLocalWarps * 32, BSIDMAP_APP_MINB) k_local_bwd(const DecodeParams p) {
+__global__ void __launch_bounds__(kLocalWarps * 32, Core::kMinBlocks > 2 ? 5 : 2) k_local_bwd(const DecodeParams p) {
   constexpr int MN = Core::Mn;
   extern __shared__ __align__(128) unsigned char s_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

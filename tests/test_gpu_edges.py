@@ -170,8 +170,8 @@ def test_app_dynamic_range_near_the_floor(name, N, frames):
     """L entries near the 1e-30 floor (R11), fed by extreme priors and by low-weight windows
     (windows far from the posterior drift carry alpha*beta weights many decades below the tile's
     largest): the per-window FP32 terms, the FP64 sums over windows and symbols and the FP64
-    normalisation must hold the 1e-4 relative gate there too.  C2: one 64-state tile writes L
-    directly; C5's shape: several tiles per frame (FP64 atomics + k_finalize)."""
+    normalisation must hold the 1e-4 relative gate there too.  Both spec APP cores: the pair core
+    (C1, C2 shapes) and the scalar core (C5 shape, several rounds of live windows per frame)."""
     import dataclasses
     cfg = dataclasses.replace(bsidgen.configs()[name], N=N, priors=True)
     b = bsidgen.make_batch(cfg, 5, frames)
