@@ -1,5 +1,7 @@
 """Summarise an ncu --set full report and a launch list into profiles/.
-usage: python tools/ncu_summary.py <tag> <gpurun_out/dir> <config> <frames>
+usage: python tools/ncu_summary.py <tag> <gpurun_out/dir> <config> <frames> [--no-write]
+--no-write: print the summary only (on the GPU box); the report is read from prof.ncu-rep or, when
+that was deleted, from raw.csv (ncu --page raw --csv) in the same directory.
 The capture directory holds digest.txt (the library source digest at capture time, tools/gpu_prof.sh);
 bench.py uses an entry only at the same digest and batch size."""
 import csv, io, json, os, subprocess, sys
@@ -19,8 +21,12 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "smsp__inst_executed.sum", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
            "sm__cycles_elapsed.avg.per_second", "launch__grid_size", "launch__block_size"] + \
           [f"smsp__sass_thread_inst_executed_op_{o}_pred_on.sum" for o in list(FP32_OPS) + list(FP64_OPS)]
-raw = subprocess.run(["ncu", "-i", os.path.join(src, "prof.ncu-rep"), "--page", "raw", "--csv"],
-                     capture_output=True, text=True).stdout
+NO_WRITE = "--no-write" in sys.argv
+if os.path.exists(os.path.join(src, "prof.ncu-rep")):
+    raw = subprocess.run(["ncu", "-i", os.path.join(src, "prof.ncu-rep"), "--page", "raw", "--csv"],
+                         capture_output=True, text=True).stdout
+else:
+    raw = open(os.path.join(src, "raw.csv")).read()
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units = rows[0], rows[1]
 kernels = []
@@ -50,7 +56,8 @@ lines = [f"# ncu summary {tag} ({cfg}, bench launch configuration)", "",
          "Per-launch device times under ncu are cold-cache and serialised: compare shares, not absolutes.", ""]
 for d in kernels:
     name = d["kernel"]
-    key = "lattice_pass1" if "gamma_sum" in name else "lattice_pass2" if "k_app" in name else "alpha_beta"
+    key = ("lattice_pass1" if "gamma_sum" in name else "lattice_pass2" if "k_app" in name else
+           "live" if "k_live" in name else "alpha_beta")
     rd, wr = gb(d.get("dram__bytes_read.sum", ("", ""))), gb(d.get("dram__bytes_write.sum", ("", "")))
     fp = d.get("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", ("", ""))[0]
     try:
@@ -89,7 +96,9 @@ if os.path.exists(launch_csv):
     for k, v in t.items():
         share = f"{100 * sum(v) / tot:.1f}%" if "bsidmap" in k else "-"
         lines.append(f"| `{k[:90]}` | {len(v)} | {sum(v) / len(v) / 1e6:.3f} | {share} |")
-    open(f"profiles/{tag}_launches.csv", "w").write("".join(body))
-open(f"profiles/{tag}_ncu_{cfg}.md", "w").write("\n".join(lines) + "\n")
-json.dump(summ, open("profiles/ncu_summary.json", "w"), indent=1)
+    if not NO_WRITE:
+        open(f"profiles/{tag}_{cfg}_launches.csv", "w").write("".join(body))
+if not NO_WRITE:
+    open(f"profiles/{tag}_ncu_{cfg}.md", "w").write("\n".join(lines) + "\n")
+    json.dump(summ, open("profiles/ncu_summary.json", "w"), indent=1)
 print("\n".join(lines))
