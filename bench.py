@@ -58,7 +58,7 @@ def parse():
 
 def workload(args):
     import dataclasses
-    cfg = bsidgen.configs()[args.config]
+    cfg = bsidgen.all_configs()[args.config]
     if args.N is not None and args.N != cfg.N:
         cfg = dataclasses.replace(cfg, N=args.N, name=f"{cfg.name}@N{args.N}")
     return cfg

@@ -217,6 +217,18 @@ def configs():
     }
 
 
+def extra_configs():
+    """Shapes outside BASELINE.json (no compiled unit: the decoder compiles their unrolled core at
+    create, jit.cu).  J1: a q = 32, n = 9 code on a Pi = Pd = 0.03 channel, the C2 batch size."""
+    return {
+        "J1": Config("J1", q=32, n=9, N=100, Pi=0.03, Pd=0.03, Ps=0.0, frames=65536, seed=MASTER_SEED + 11),
+    }
+
+
+def all_configs():
+    return {**configs(), **extra_configs()}
+
+
 @dataclasses.dataclass
 class Batch:
     cfg: Config

@@ -179,7 +179,8 @@ long bsidmap_last_launch_count(const bsidmap_decoder *d);
 
 /*
  * Human/JSON-readable launch plan for num_frames frames (mode, chunking, grid and block
- * sizes, lattice core: "spec" fully unrolled or "generic"), written to buf (NUL-terminated).
+ * sizes, lattice core: "spec" fully unrolled and compiled into the library, "jit" fully unrolled
+ * and compiled at create, or "generic"), written to buf (NUL-terminated).
  * Returns the length, or a negative error code.
  */
 int bsidmap_plan_info(bsidmap_decoder *d, int num_frames, char *buf, size_t buf_len);
@@ -190,6 +191,16 @@ int bsidmap_plan_info(bsidmap_decoder *d, int num_frames, char *buf, size_t buf_
  * host rho[] -- the algorithmic work counters used by the roofline.
  */
 long bsidmap_lattice_nodes(const bsidmap_decoder *d);
+
+/*
+ * Run-time compiled lattice cores (the paper's templates over the code and channel sizes,
+ * P:1055-1079, for any shape).  bsidmap_create compiles the fully unrolled kernels of a shape
+ * (n, m_n^-, M_n) that has no compiled unit with NVRTC for sm_100a, caches the cubins on disk
+ * (BSIDMAP_JIT_CACHE, default ~/.cache/bsidmap) and loads them once per process; BSIDMAP_JIT=0
+ * keeps the generic core.  This entry only compiles (no device needed): BSIDMAP_OK, or
+ * BSIDMAP_EPLAN with the reason in err (err may be NULL; len bytes incl. NUL).
+ */
+int bsidmap_jit_compile(int n, int mn_lo, int Mn, char *err, size_t len);
 long long bsidmap_valid_lattices(const bsidmap_decoder *d, int num_frames, const int32_t *rho_host);
 
 /*

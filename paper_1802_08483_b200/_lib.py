@@ -66,6 +66,7 @@ SIGNATURES = {
     "bsidmap_drift_pmf": (_i, [_i, _d, _d, _i, _i, _p]),
     "bsidmap_drift_limits": (_i, [_i, _d, _d, _d, _p, _p]),
     "bsidmap_drift_limits_tails": (_i, [_i, _d, _d, _d, _p, _p]),
+    "bsidmap_jit_compile": (_i, [_i, _i, _i, ctypes.c_char_p, _sz]),
     "bsidmap_state_space": (_i, [_i, _i, _d, _d, _d, _p, _p, _p, _p]),
     "bsidmap_phi": (_i, [_i, _d, _d, _i, _i, _i, _p, _p]),
     "bsidmap_mc_generate": (_i, [_p, ctypes.c_uint64, ctypes.c_int64, _i, _i, _p, _p, _p, _p, _p]),

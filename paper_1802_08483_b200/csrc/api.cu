@@ -68,6 +68,8 @@ struct bsidmap_decoder {
   size_t ord_off[8] = {};    // byte offsets: Cp, Dp, Cs2, Ds2, Cst2, Cs3, Ds3, Cst3
   CoreKernels kern{};
   bool spec = false;
+  bool jit = false;                     // spec kernels compiled at run time (jit.cu)
+  std::string jit_err;                  // why a shape without a unit runs on the generic core
   LatticeConst lc{};
   // workspace
   void* ws = nullptr;
@@ -111,6 +113,15 @@ namespace {
 int fail(bsidmap_decoder* d, int code, const std::string& msg) {
   if (d) d->err = msg; else g_err = msg;
   return code;
+}
+
+// Launch a kernel of the core table through cudaLaunchKernel: the table holds either the address
+// of a statically compiled __global__ function or a cudaKernel_t of a run-time compiled shape
+// (jit.cu, cast to the same pointer type), which the runtime accepts in the same place.
+template <class... A>
+void launch_k(void (*fn)(A...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A... args) {
+  void* argv[] = {static_cast<void*>(&args)...};
+  cudaLaunchKernel(reinterpret_cast<const void*>(fn), grid, block, argv, smem, s);
 }
 
 int cuda_fail(bsidmap_decoder* d, cudaError_t e, const char* what) {
@@ -454,7 +465,7 @@ void launch_pass1(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_
   for_i_slices(d->N, [&](int i0, int ni) {
     p.i_base = i0;
     p.i_end = i0 + ni;
-    l1<<<dim3(gx1, (unsigned)((ni + steps - 1) / steps)), kLatticeThreads, P.l1_smem, s>>>(p);
+    launch_k(l1, dim3(gx1, (unsigned)((ni + steps - 1) / steps)), kLatticeThreads, P.l1_smem, s, p);
     d->launches++;
   });
 }
@@ -462,9 +473,9 @@ void launch_pass1(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_
 void launch_alpha_beta(bsidmap_decoder* d, const Plan& P, const DecodeParams& p, cudaStream_t s) {
   if (P.ab_warp) {
     const long tasks = 2L * p.F, per = kAbWarpThreads / 32;
-    P.ab_warp<<<(unsigned)((tasks + per - 1) / per), kAbWarpThreads, P.ab_smem, s>>>(p);
+    launch_k(P.ab_warp, (unsigned)((tasks + per - 1) / per), kAbWarpThreads, P.ab_smem, s, p);
   } else {
-    P.ab_cta<<<dim3(p.F, 2), P.ab_threads, P.ab_smem, s>>>(p, P.ab_stages);
+    launch_k(P.ab_cta, dim3(p.F, 2), P.ab_threads, P.ab_smem, s, p, P.ab_stages);
   }
   d->launches++;
 }
@@ -478,7 +489,7 @@ void launch_pass2(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_
     const unsigned gx = (unsigned)(((p.F + P.app_G - 1) / P.app_G + kX2Warps - 1) / kX2Warps);
     for_i_slices(d->N, [&](int i0, int ni) {
       p.i_base = i0;
-      P.app_kernel<<<dim3(gx, ni), kLatticeThreads, P.app_smem, s>>>(p);
+      launch_k(P.app_kernel, dim3(gx, ni), kLatticeThreads, P.app_smem, s, p);
       d->launches++;
     });
     return;
@@ -488,7 +499,7 @@ void launch_pass2(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_
   auto l2 = P.app_kernel;
   for_i_slices(d->N, [&](int i0, int ni) {
     p.i_base = i0;
-    l2<<<dim3(gx_flat, ni), kLatticeThreads, P.app_smem, s>>>(p);
+    launch_k(l2, dim3(gx_flat, ni), kLatticeThreads, P.app_smem, s, p);
     d->launches++;
   });
 }
@@ -500,10 +511,10 @@ int run_chunk(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s,
   if (P.mode == kSchedLocal) {  // the paper's local schedule: two fused per-frame passes
     const unsigned gl = (unsigned)((p.F + kLocalWarps - 1) / kLocalWarps);
     if (first_chunk) record(d, 1, s);
-    d->kern.local_fwd<<<gl, kLocalWarps * 32, P.local_smem, s>>>(p);
+    launch_k(d->kern.local_fwd, gl, kLocalWarps * 32, P.local_smem, s, p);
     if (first_chunk) record(d, 2, s);
     if (first_chunk) record(d, 3, s);
-    d->kern.local_bwd<<<gl, kLocalWarps * 32, P.local_smem, s>>>(p);
+    launch_k(d->kern.local_bwd, gl, kLocalWarps * 32, P.local_smem, s, p);
     if (first_chunk) record(d, 4, s);
     k_zero_failed<<<p.F, 256, 0, s>>>(p);
     d->launches += 3;
@@ -515,10 +526,10 @@ int run_chunk(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s,
   if (P.mode == kSchedLocalCta) {  // the same schedule, one CTA per frame (M_tau > 64)
     const int kk = d->q > 24 ? 1 : 0, pr = p.priors ? 1 : 0;
     if (first_chunk) record(d, 1, s);
-    d->kern.local_cta_fwd[kk][pr]<<<p.F, kLocalCtaThreads, P.local_smem, s>>>(p);
+    launch_k(d->kern.local_cta_fwd[kk][pr], p.F, kLocalCtaThreads, P.local_smem, s, p);
     if (first_chunk) record(d, 2, s);
     if (first_chunk) record(d, 3, s);
-    d->kern.local_cta_bwd[pr]<<<p.F, kLocalCtaThreads, P.local_smem, s>>>(p);
+    launch_k(d->kern.local_cta_bwd[pr], p.F, kLocalCtaThreads, P.local_smem, s, p);
     if (first_chunk) record(d, 4, s);
     k_zero_failed<<<p.F, 256, 0, s>>>(p);
     d->launches += 3;
@@ -705,7 +716,17 @@ int bsidmap_create(bsidmap_decoder** out, int q, int n, int N, const uint32_t* c
   }
   // the spec cores' APP (k_app_live.cuh) stages per-symbol terms in shared memory: very large
   // alphabets use the generic core, whose APP pass stages symbols in chunks
-  d->spec = rescaled && find_spec_kernels(n, mn_lo, Mn, &d->kern) && live_app_smem_fits(d->kern, q, Mn);
+  const bool unit = rescaled && find_spec_kernels(n, mn_lo, Mn, &d->kern);
+  d->spec = unit && live_app_smem_fits(d->kern, q, Mn);
+  if (rescaled && !unit) {  // no compiled unit for this shape: compile its unrolled core now
+    const char* jv = std::getenv("BSIDMAP_JIT");
+    if (jv && std::atoi(jv) == 0) {
+      d->jit_err = "BSIDMAP_JIT=0";
+    } else if (cudaSetDevice(device) == cudaSuccess && jit_spec_kernels(n, mn_lo, Mn, &d->kern, &d->jit_err, false)) {
+      d->spec = d->jit = live_app_smem_fits(d->kern, q, Mn);
+      if (!d->jit) d->jit_err = "alphabet too large for the live-window APP's shared memory";
+    }
+  }
   if (!d->spec && !find_generic_kernels(Mn, &d->kern)) {
     delete d;
     return fail(nullptr, BSIDMAP_EPLAN, "no lattice core for M_n = " + std::to_string(Mn));
@@ -938,14 +959,23 @@ int bsidmap_plan_info(bsidmap_decoder* d, int F, char* buf, size_t len) {
       "\"lattice_grid\": [%ld, %d], \"lattice_block\": %d, \"alpha_beta_grid\": [%d, 2], \"alpha_beta_block\": %d, "
       "\"workspace_bytes\": %zu, \"windows_per_lane\": %d, \"q\": %d, \"n\": %d, \"N\": %d, \"Mn\": %d, \"Mtau\": %d, "
       "\"alpha_beta_overlap_subbatches\": %d, \"app_prefix_bits\": %d, \"app_windows_per_lane\": %d, "
-      "\"app_folded_rows\": %d, \"app_live\": %d, \"app_frames_per_warp\": %d, \"live_eps\": %.6g}",
-      sched_name(P.mode), F, P.chunk, P.nchunks, d->spec ? "spec" : "generic",
+      "\"app_folded_rows\": %d, \"app_live\": %d, \"app_frames_per_warp\": %d, \"live_eps\": %.6g, "
+      "\"jit_error\": \"%s\"}",
+      sched_name(P.mode), F, P.chunk, P.nchunks, d->jit ? "jit" : d->spec ? "spec" : "generic",
       d->kern.W == 2 ? ((long)P.chunk * tiles_per_frame(d->Mt) + kX2Warps - 1) / kX2Warps
                      : (lanes + kLatticeThreads - 1) / kLatticeThreads,
       d->N, kLatticeThreads, P.chunk, P.ab_warp ? kAbWarpThreads : P.ab_threads,
       layout(d, P.chunk, P.mode).total, d->kern.W, d->q, d->n, d->N, d->Mn, d->Mt, std::min(P.ab_sub, P.chunk), P.app_kp, P.app_live ? d->kern.app_live_W : 1, P.app_ks,
-      P.app_live ? 1 : 0, P.app_G, d->live_eps);
+      P.app_live ? 1 : 0, P.app_G, d->live_eps, d->jit_err.c_str());
   return nb;
+}
+
+int bsidmap_jit_compile(int n, int mn_lo, int Mn, char* err, size_t len) {
+  std::string e;
+  CoreKernels k{};
+  const bool ok = jit_spec_kernels(n, mn_lo, Mn, &k, &e, true);
+  if (err && len) std::snprintf(err, len, "%s", e.c_str());
+  return ok ? BSIDMAP_OK : fail(nullptr, BSIDMAP_EPLAN, e);
 }
 
 long bsidmap_lattice_nodes(const bsidmap_decoder* d) {
@@ -984,7 +1014,7 @@ int bsidmap_debug_gamma(bsidmap_decoder* d, int F, const uint32_t* rx, const int
   k_frame_init<<<(F + 255) / 256, 256, 0, s>>>(p);
   const unsigned gx = d->kern.W == 2 ? (unsigned)(((long)F * tiles_per_frame(d->Mt) + kX2Warps - 1) / kX2Warps)
                                      : (unsigned)(((long)F * d->Mt + kLatticeThreads - 1) / kLatticeThreads);
-  d->kern.gamma_dump<<<gx, kLatticeThreads, d->q * 4, s>>>(p);
+  launch_k(d->kern.gamma_dump, gx, kLatticeThreads, (size_t)d->q * 4, s, p);
   e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   cudaFree(st);

@@ -4,8 +4,18 @@
 // drift limits m_n^-/m_n^+ (corridor, M_n) and m_tau^-/m_tau^+ (trellis
 // states, M_tau), channel Pi, Pd, Ps.
 #pragma once
+#ifdef __CUDACC_RTC__  // run-time compiled shapes (jit.cu, NVRTC): no host headers
+typedef unsigned char uint8_t;
+typedef unsigned short uint16_t;
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+typedef int int32_t;
+typedef long long int64_t;
+typedef unsigned long size_t;
+#else
 #include <cstdint>
 #include <cuda_runtime.h>
+#endif
 
 namespace bsidmap {
 

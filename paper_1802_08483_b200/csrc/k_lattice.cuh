@@ -15,6 +15,9 @@
 // Grid: blockIdx.y = symbol index i (+ p.i_base), x over the flat lane index
 // g = f M_tau + (m' - m_tau^-) of the chunk's frames; one lane = one window.
 #pragma once
+#ifndef __CUDACC_RTC__
+#include <string>
+#endif
 #include "lattice.cuh"
 #include "lattice_x2.cuh"
 #include "k_alphabeta_warp.cuh"
@@ -345,8 +348,11 @@ CoreKernels make_core_kernels(long nodes) {
   return k;
 }
 
-// Registry (defined in the instantiation units).
+#ifndef __CUDACC_RTC__
+// Registry (defined in the instantiation units) and the run-time compiled shapes (jit.cu).
 bool find_spec_kernels(int n, int mn_lo, int Mn, CoreKernels* out);
 bool find_generic_kernels(int Mn, CoreKernels* out);
+bool jit_spec_kernels(int n, int mn_lo, int Mn, CoreKernels* out, std::string* err, bool compile_only);
+#endif
 
 }  // namespace bsidmap

@@ -1,6 +1,8 @@
 // tma.cuh -- mbarrier + TMA bulk-copy (cp.async.bulk) helpers, sm_90+/sm_100a PTX.
 #pragma once
+#ifndef __CUDACC_RTC__
 #include <cstdint>
+#endif
 
 namespace bsidmap {
 

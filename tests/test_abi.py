@@ -93,3 +93,16 @@ def test_c_example_builds_and_links():
     r = subprocess.run(["make", "-C", root, "examples/decode_host"], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     assert os.path.exists(exe)
+
+
+def test_jit_compiles_a_shape_without_a_unit(tmp_path, monkeypatch):
+    """NVRTC compiles the unrolled kernels of a shape with no compiled unit (J1's corridor) for
+    sm_100a without a device, into five cached programs; shapes beyond the unrolled cores' bounds
+    are refused with a reason (the decoder then keeps the generic core)."""
+    monkeypatch.setenv("BSIDMAP_JIT_CACHE", str(tmp_path))
+    lib = _lib.load()
+    buf = ctypes.create_string_buffer(4096)
+    assert lib.bsidmap_jit_compile(9, -7, 17, buf, 4096) == _lib.BSIDMAP_OK, buf.value
+    assert len(list(tmp_path.iterdir())) == 5
+    assert lib.bsidmap_jit_compile(40, -1, 24, buf, 4096) == _lib.BSIDMAP_EPLAN
+    assert b"corridor nodes" in buf.value

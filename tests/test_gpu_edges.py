@@ -87,7 +87,8 @@ def test_spec_shapes_random_channels(shape, seed):
         assert_parity(L, st, res)
 
 
-def test_large_alphabet_uses_generic_core():
+def test_large_alphabet_uses_generic_core(monkeypatch):
+    monkeypatch.setenv("BSIDMAP_JIT", "0")
     """q = 512 on C2's lattice shape: the specialised APP kernels would need more shared memory than
     a CTA has, so the decoder takes the generic core; parity against the oracle in all schedules."""
     cfg = bsidgen.Config("bigq", q=512, n=10, N=3, Pi=0.01, Pd=0.01, Ps=0.001, frames=0, seed=31,

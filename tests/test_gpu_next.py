@@ -68,7 +68,8 @@ def test_soft_boundary_priors_parity(name, mode):
     assert worst <= TOL, worst
 
 
-def test_soft_boundary_generic_core():
+def test_soft_boundary_generic_core(monkeypatch):
+    monkeypatch.setenv("BSIDMAP_JIT", "0")
     cfg = bsidgen.Config("S", q=5, n=4, N=9, Pi=0.03, Pd=0.02, Ps=0.01, frames=0, seed=77)
     b, a0, bN = _soft_batch(cfg, 9, seed=5)
     d = _dec().from_config(cfg, b.C, mode=3, device=0)

@@ -156,7 +156,8 @@ def _random_cfg(rng, k):
 
 
 @pytest.mark.parametrize("k", range(10))
-def test_random_shapes_generic_core(k):
+def test_random_shapes_generic_core(k, monkeypatch):
+    monkeypatch.setenv("BSIDMAP_JIT", "0")   # the generic core (run-time compiled cores: test_gpu_jit.py)
     rng = np.random.default_rng(k)
     cfg = _random_cfg(rng, k)
     F = int(rng.integers(1, 40))
