@@ -179,7 +179,7 @@ const char* sched_name(int s) {
 Layout layout(const bsidmap_decoder* d, long F, int sched) {
   Layout l{};
   const bool local = sched == kSchedLocal || sched == kSchedLocalCta;
-  l.gsum = local ? 0 : align_up((size_t)F * d->N * d->Mn * ((d->Mt + 3) & ~3) * sizeof(float));
+  l.gsum = local ? 0 : align_up((size_t)F * d->N * d->Mn * gsum_stride(d->Mt) * sizeof(float));
   l.gamma = sched == kSchedStored ? align_up((size_t)F * d->N * d->q * d->Mn * d->Mt * sizeof(float)) : 0;
   l.alpha = align_up((size_t)F * (d->N + 1) * d->Mt * sizeof(double));
   l.beta = local ? 0 : l.alpha;
@@ -252,7 +252,7 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   // block size depends on M_tau only, so chunking does not change the arithmetic.
   P->ab_threads = std::min(1024, std::max(64, ((d->Mt + 1) / 2 + 31) / 32 * 32));
   {  // TMA ring depth: up to 4 stages of Gamma_i blocks within ~200 KB of shared memory
-    const int Mtp = (d->Mt + 3) & ~3;
+    const int Mtp = gsum_stride(d->Mt);
     const size_t blk = (size_t)d->Mn * Mtp * 4;
     P->ab_stages = (int)std::max<size_t>(1, std::min<size_t>(4, (200u * 1024 - 2 * (size_t)Mtp * 8 - 600) / blk));
     if (2L * chunk >= 4L * d->num_sms) P->ab_stages = 1;
@@ -266,7 +266,7 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   P->ab_cta = d->kern.ab_cta ? d->kern.ab_cta : k_alpha_beta_cta<0>;
   const int spt = (d->Mt + 31) / 32;
   const int spt_k = spt == 3 ? 4 : spt;
-  const size_t ab_warp_bytes = (size_t)(kAbWarpThreads / 32) * ab_warp_smem(spt_k, d->Mn, (d->Mt + 3) & ~3);
+  const size_t ab_warp_bytes = (size_t)(kAbWarpThreads / 32) * ab_warp_smem(spt_k, d->Mn, gsum_stride(d->Mt));
   if (d->kern.ab_warp[0] && spt <= 4 && ab_warp_bytes <= 100 * 1024) {
     const int k = spt == 1 ? 0 : spt == 2 ? 1 : 2;
     P->ab_warp = d->kern.ab_warp[k];
@@ -365,7 +365,7 @@ void fill_params(const bsidmap_decoder* d, DecodeParams* p) {
   p->q = d->q; p->n = d->n; p->N = d->N;
   p->mn_lo = d->mn_lo; p->mn_hi = d->mn_hi; p->Mn = d->Mn;
   p->mt_lo = d->mt_lo; p->mt_hi = d->mt_hi; p->Mt = d->Mt;
-  p->Mtp = (d->Mt + 3) & ~3;
+  p->Mtp = gsum_stride(d->Mt);
   p->C = d->d_C;
   const char* ob = static_cast<const char*>(d->d_orders);
   p->Cp = reinterpret_cast<const uint32_t*>(ob + d->ord_off[0]);

@@ -82,6 +82,11 @@ struct DecodeParams {
   LatticeConst lc;
 };
 
+// Row stride of Gsum: M_tau rounded up to whole 32-byte sectors (8 floats) -- every Gamma row starts
+// a sector and the pass-1 kernels also write the padding, so no sector is ever partially written
+// (a partial sector costs a DRAM read to fill on eviction); 16-byte multiple as TMA bulk copies need.
+__host__ __device__ __forceinline__ int gsum_stride(int Mt) { return (Mt + 7) & ~7; }
+
 // Boundary row of frame f at state index m: alpha_0 (fwd) / beta_N (bwd), point masses by default.
 __device__ __forceinline__ double boundary_row(const DecodeParams& p, int f, int m, bool fwd) {
   if (m >= p.Mt) return 0.0;
