@@ -150,8 +150,8 @@ int resolve_sched(const bsidmap_decoder* d, int mode) {
   // RECOMPUTE: the paper's local schedule where a frame fits one warp tile, else Gamma-sum
   if (d->kern.local_fwd && d->Mt <= kTileSlots) return kSchedLocal;
   if (d->kern.local_cta_bwd[0] && d->Mt <= 4 * kLocalCtaThreads &&
-      local_cta_fwd_smem(d->Mn, (d->Mt + 3) & ~3) <= 227u * 1024 &&
-      local_cta_bwd_smem(d->Mn, (d->Mt + 3) & ~3, d->q) <= 227u * 1024)
+      local_cta_fwd_smem(d->Mn, gsum_stride(d->Mt)) <= 227u * 1024 &&
+      local_cta_bwd_smem(d->Mn, gsum_stride(d->Mt), d->q) <= 227u * 1024)
     return kSchedLocalCta;
   return kSchedGammaSum;
 }
@@ -274,7 +274,7 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   }
   P->local_smem = (size_t)kLocalWarps * local_warp_smem(d->Mn, d->q);
   if (mode == kSchedLocalCta) {  // CTA local schedule: the larger of the two passes' smem
-    const int Mtp = (d->Mt + 3) & ~3;
+    const int Mtp = gsum_stride(d->Mt);
     P->local_smem = std::max(local_cta_fwd_smem(d->Mn, Mtp), local_cta_bwd_smem(d->Mn, Mtp, d->q));
   }
   // pass 1: hoist the last K lattice rows out of the symbol loop (K = 3 for q > 24, else 2)

@@ -197,9 +197,7 @@ __global__ void __launch_bounds__(kLatticeThreads, KS == 2 ? BSIDMAP_APP_MINB_KS
           if (k == 0 || ((x ^ xprev) & ((1u << KP) - 1u)) != 0u)
             Core::template run_head<KP, BSIDMAP_APP_GROUP>(lane_t, x, p, fh);
           xprev = x;
-#pragma unroll
-          for (int u = 0; u < MN; u++) fo[u] = fh[u];
-          Core::template run_tail_to_then<KP, RL, BSIDMAP_APP_GROUP>(lane_t, x, p, fo, dot);
+          Core::template run_tail_from_then<KP, RL, BSIDMAP_APP_GROUP>(lane_t, x, p, fh, fo, dot);
         } else {
           Core::template run_to_then<RL, BSIDMAP_APP_GROUP>(lane_t, x, p, fo, dot);
         }
@@ -296,10 +294,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_LIVE1_MINB) k_app_liv
         if constexpr (KP > 0) {
           if (k == 0 || ((x ^ xprev) & ((1u << KP) - 1u)) != 0u) Core::template run_head<KP>(lane_t, x, p, fh);
           xprev = x;
-#pragma unroll
-          for (int u = 0; u < MN; u++) fo[u] = fh[u];
-          if constexpr (KS == 2) Core::template run_tail_to_then<KP, RL>(lane_t, x, p, fo, dot);
-          else Core::template run_tail_to<KP, RL>(lane_t, x, p, fo);
+          Core::template run_tail_from<KP, RL, KS == 2>(lane_t, x, p, fh, fo, dot);
         } else {
           if constexpr (KS == 2) Core::template run_to_then<RL>(lane_t, x, p, fo, dot);
           else Core::template run_to<RL>(lane_t, x, p, fo);

@@ -67,14 +67,6 @@ __device__ __forceinline__ bool out_valid(const DecodeParams&, const LaneGeom& G
   return (G.vmask >> e) & 1u;
 }
 
-// The lane of the last state M_tau - 1 also zeroes the padding [M_tau, Mtp) of its Gamma rows
-// (gsum_stride): every 32-byte sector of a row is then written whole.
-__device__ __forceinline__ void gsum_pad(const DecodeParams& p, const LaneGeom& G, int i) {
-  if (!G.in || G.mi != p.Mt - 1) return;
-  float* out = p.Gsum + ((size_t)G.f * p.N + i) * p.Mn * p.Mtp;
-  for (int e = 0; e < p.Mn; e++)
-    for (int c = p.Mt; c < p.Mtp; c++) out[(size_t)e * p.Mtp + c] = 0.f;
-}
 
 template <class Core, bool kStoreGamma>
 __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_sum(const DecodeParams p) {
@@ -123,7 +115,6 @@ __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_su
 #pragma unroll
     for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, G, e) ? sc * acc[e] : 0.f;
   }
-  gsum_pad(p, G, i);
 }
 
 constexpr int kAppDChunk = 64;  // symbols per smem staging round of the APP passes

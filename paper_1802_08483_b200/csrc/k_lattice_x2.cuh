@@ -147,8 +147,6 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_
 #pragma unroll
     for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, B, e) ? sc * hi_of(acc[e]) : 0.f;
   }
-  gsum_pad(p, A, i);
-  gsum_pad(p, B, i);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -257,8 +255,6 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1C_MINB) k_gamma_sum
 #pragma unroll
       for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, B, e) ? sc * hi_of(acc[e]) : 0.f;
     }
-    gsum_pad(p, A, i);
-    gsum_pad(p, B, i);
   }
 }
 
@@ -325,7 +321,6 @@ __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_su
 #pragma unroll
       for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, G, e) ? sc * acc[e] : 0.f;
     }
-    gsum_pad(p, G, i);
   }
 }
 

@@ -67,29 +67,38 @@ struct SpecCore {
     }
   }
 
-  template <int R, bool kRescaled>
-  __device__ __forceinline__ static void row(float (&f)[MN], const float (&Q)[J + 1], const LatticeConst& lc) {
+  // Row R from row R-1 held in s into d (kInPlace: d is s, see SpecCoreX2::row_from).
+  template <int R, bool kRescaled, bool kInPlace = true>
+  __device__ __forceinline__ static void row_from(float (&d)[MN], const float (&s)[MN], const float (&Q)[J + 1],
+                                                  const LatticeConst& lc) {
     constexpr bool kLast = (R == NN);
     float prev = 0.f;
 #pragma unroll
     for (int e = 0; e < MN; e++) {
       const int j = R + LO + e;  // lattice column of this node
-      if (j < 0) continue;       // left of column 0: structurally zero, stays 0
+      if (j < 0) {               // left of column 0: structurally zero, stays 0
+        if constexpr (!kInPlace) d[e] = 0.f;
+        continue;
+      }
       float v;
       if (j == 0) {
         // column 0 is reached by deletions only: F_{r,0} = Pd F_{r-1,0}, i.e. G_{r,0} = G_{r-1,0}
-        v = kRescaled ? f[e + 1] : lc.b * f[e + 1];
+        v = kRescaled ? s[e + 1] : lc.b * s[e + 1];
       } else {
         float u;
         if (e + 1 < MN)  // deletion Pd F_{r-1,j} + transmission Q F_{r-1,j-1}
-          u = kRescaled ? fmaf(Q[j], f[e], f[e + 1]) : fmaf(Q[j], f[e], lc.b * f[e + 1]);
+          u = kRescaled ? fmaf(Q[j], s[e], s[e + 1]) : fmaf(Q[j], s[e], lc.b * s[e + 1]);
         else
-          u = Q[j] * f[e];
+          u = Q[j] * s[e];
         v = (!kLast && e > 0) ? fmaf(lc.a, prev, u) : u;  // insertion 1/2 Pi F_{r,j-1}
       }
-      f[e] = v;
+      d[e] = v;
       prev = v;
     }
+  }
+  template <int R, bool kRescaled>
+  __device__ __forceinline__ static void row(float (&f)[MN], const float (&Q)[J + 1], const LatticeConst& lc) {
+    row_from<R, kRescaled, true>(f, f, Q, lc);
   }
 
   // Rows are issued in pairs: a 4-way branch on (x_R, x_{R+1}) puts rows R and R+1
@@ -190,6 +199,46 @@ struct SpecCore {
   __device__ __forceinline__ static void run_tail_to_then(const Lane& L, uint32_t x, const DecodeParams& p,
                                                           float (&f)[MN], Tail& tail) {
     rows_then<KP + 1, RL>(f, x, L, p.lc, tail);
+  }
+  // Rows KP+1..RL from the shared prefix row fh into f, then tail(f) in the last group's basic block
+  // (kTail; else no tail): the first group reads fh and writes f, so fh is not copied first.  Same
+  // operations in the same order as copying fh to f and calling run_tail_to(_then) (bit-identical).
+  template <int KP, int RL, bool kTail, class Tail>
+  __device__ __forceinline__ static void run_tail_from(const Lane& L, uint32_t x, const DecodeParams& p,
+                                                       const float (&fh)[MN], float (&f)[MN], Tail& tail) {
+    constexpr int R = KP + 1;
+    constexpr int G = BSIDMAP_SCALAR_GROUP;
+    const LatticeConst& lc = p.lc;
+    if constexpr (R > RL) {
+#pragma unroll
+      for (int e = 0; e < MN; e++) f[e] = fh[e];
+      if constexpr (kTail) tail(f);
+    } else if constexpr (G >= 2 && R + 1 <= RL) {
+      constexpr bool kEnd = kTail && (R + 1 == RL);
+      switch ((x >> (R - 1)) & 3u) {
+        case 0u: row_from<R, true, false>(f, fh, L.q0, lc); row<R + 1, true>(f, L.q0, lc); if constexpr (kEnd) tail(f); break;
+        case 1u: row_from<R, true, false>(f, fh, L.q1, lc); row<R + 1, true>(f, L.q0, lc); if constexpr (kEnd) tail(f); break;
+        case 2u: row_from<R, true, false>(f, fh, L.q0, lc); row<R + 1, true>(f, L.q1, lc); if constexpr (kEnd) tail(f); break;
+        default: row_from<R, true, false>(f, fh, L.q1, lc); row<R + 1, true>(f, L.q1, lc); if constexpr (kEnd) tail(f); break;
+      }
+      if constexpr (R + 2 <= RL) {
+        if constexpr (kTail) rows_then<R + 2, RL>(f, x, L, lc, tail);
+        else rows<R + 2, RL>(f, x, L, lc);
+      }
+    } else {
+      constexpr bool kEnd = kTail && (R == RL);
+      if ((x >> (R - 1)) & 1u) {
+        row_from<R, true, false>(f, fh, L.q1, lc);
+        if constexpr (kEnd) tail(f);
+      } else {
+        row_from<R, true, false>(f, fh, L.q0, lc);
+        if constexpr (kEnd) tail(f);
+      }
+      if constexpr (R + 1 <= RL) {
+        if constexpr (kTail) rows_then<R + 1, RL>(f, x, L, lc, tail);
+        else rows<R + 1, RL>(f, x, L, lc);
+      }
+    }
   }
   // Transpose of lattice row R < n (SpecCoreX2::row_transpose): weights on G_R -> weights on G_{R-1}.
   template <int R>

@@ -63,24 +63,35 @@ struct SpecCoreX2 {
     }
   }
 
-  template <int R>
-  __device__ __forceinline__ static void row(f32x2 (&f)[MN], const f32x2 (&Q)[J + 1], f32x2 a2) {
+  // Row R from row R-1 held in s into d (kInPlace: d is s; node e reads s[e], s[e+1] before d[e] is
+  // written, so the update runs in place).  A separate d lets a consumer keep s (the APP's shared
+  // prefix row) without copying it first.
+  template <int R, bool kInPlace = true>
+  __device__ __forceinline__ static void row_from(f32x2 (&d)[MN], const f32x2 (&s)[MN], const f32x2 (&Q)[J + 1],
+                                                  f32x2 a2) {
     constexpr bool kLast = (R == NN);
     f32x2 prev = 0ull;
 #pragma unroll
     for (int e = 0; e < MN; e++) {
       const int j = R + LO + e;
-      if (j < 0) continue;  // structurally zero
+      if (j < 0) {  // structurally zero
+        if constexpr (!kInPlace) d[e] = 0ull;
+        continue;
+      }
       f32x2 v;
       if (j == 0) {
-        v = f[e + 1];  // column 0: deletions only, G_{r,0} = G_{r-1,0}
+        v = s[e + 1];  // column 0: deletions only, G_{r,0} = G_{r-1,0}
       } else {
-        const f32x2 u = (e + 1 < MN) ? ffma2(Q[j], f[e], f[e + 1]) : fmul2(Q[j], f[e]);
+        const f32x2 u = (e + 1 < MN) ? ffma2(Q[j], s[e], s[e + 1]) : fmul2(Q[j], s[e]);
         v = (!kLast && e > 0) ? ffma2(a2, prev, u) : u;
       }
-      f[e] = v;
+      d[e] = v;
       prev = v;
     }
+  }
+  template <int R>
+  __device__ __forceinline__ static void row(f32x2 (&f)[MN], const f32x2 (&Q)[J + 1], f32x2 a2) {
+    row_from<R, true>(f, f, Q, a2);
   }
 
   // Rows are issued in groups of G (1, 2 or 3): a 2^G-way branch on (x_R .. x_{R+G-1}) puts the
@@ -218,6 +229,39 @@ struct SpecCoreX2 {
   __device__ __forceinline__ static void run_tail_to_then(const Lane& L, uint32_t x, const DecodeParams& p,
                                                           f32x2 (&f)[MN], Tail& tail) {
     rows_then<KP + 1, G, RL>(f, x, L, pk(p.lc.a, p.lc.a), tail);
+  }
+  // The same from the shared prefix row fh into f: the first row group reads fh and writes f (no
+  // copy of fh), the rest runs in place on f.  Same operations in the same order as copying fh to f
+  // and calling run_tail_to_then (bit-identical).
+  template <int KP, int RL, int G, class Tail>
+  __device__ __forceinline__ static void run_tail_from_then(const Lane& L, uint32_t x, const DecodeParams& p,
+                                                            const f32x2 (&fh)[MN], f32x2 (&f)[MN], Tail& tail) {
+    constexpr int R = KP + 1;
+    const f32x2 a2 = pk(p.lc.a, p.lc.a);
+    if constexpr (R > RL) {
+#pragma unroll
+      for (int e = 0; e < MN; e++) f[e] = fh[e];
+      tail(f);
+    } else if constexpr (G >= 2 && R + 1 <= RL) {
+      constexpr bool kEnd = (R + 1 == RL);
+      switch ((x >> (R - 1)) & 3u) {
+        case 0u: row_from<R, false>(f, fh, L.q0, a2); row<R + 1>(f, L.q0, a2); if constexpr (kEnd) tail(f); break;
+        case 1u: row_from<R, false>(f, fh, L.q1, a2); row<R + 1>(f, L.q0, a2); if constexpr (kEnd) tail(f); break;
+        case 2u: row_from<R, false>(f, fh, L.q0, a2); row<R + 1>(f, L.q1, a2); if constexpr (kEnd) tail(f); break;
+        default: row_from<R, false>(f, fh, L.q1, a2); row<R + 1>(f, L.q1, a2); if constexpr (kEnd) tail(f); break;
+      }
+      if constexpr (!kEnd) rows_then<R + 2, G, RL>(f, x, L, a2, tail);
+    } else {
+      constexpr bool kEnd = (R == RL);
+      if ((x >> (R - 1)) & 1u) {
+        row_from<R, false>(f, fh, L.q1, a2);
+        if constexpr (kEnd) tail(f);
+      } else {
+        row_from<R, false>(f, fh, L.q0, a2);
+        if constexpr (kEnd) tail(f);
+      }
+      if constexpr (!kEnd) rows_then<R + 1, G, RL>(f, x, L, a2, tail);
+    }
   }
 
   // Transpose of lattice row R (R < n) with Q-dot table Q: weights w on the row's outputs G_R ->
