@@ -328,7 +328,8 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   else
     P->ab_sub = (!P->ab_warp && 2L * chunk <= d->num_sms) ? 2 : 1;
   P->l1_smem = (d->kern.gamma_sum_k3 && mode != kSchedStored)
-                   ? (size_t)d->Mn * kLatticeThreads * 8 + (size_t)d->q * 6 + 64 + 16
+                   ? (size_t)d->Mn * kLatticeThreads * 8 + (size_t)d->q * 6 + 64 + 16 +
+                         d->kern.l1_head_bytes[P->l1_kernel == d->kern.gamma_sum_k3 ? 1 : 0]
                    : (size_t)d->q * 4;
   return BSIDMAP_OK;
 }

@@ -25,7 +25,7 @@
 #include <thread>
 #include <vector>
 
-#include "k_lattice.cuh"
+#include "k_lattice_x2.cuh"
 
 namespace {
 
@@ -295,6 +295,9 @@ bool jit_spec_kernels(int n, int lo, int Mn, CoreKernels* out, std::string* err,
   k.app_ks_auto = scalar_app ? (n <= 10 ? 2 : 1) : (minb3 ? 1 : 2);
   k.app_live_W = scalar_app ? 1 : 2;
   k.nodes = (long)n * Mn - (long)lo * (lo - 1) / 2;
+  // pass-1 head tables (k_lattice_x2.cuh l1_head_rows), at the class kernel's CTAs per SM (BSIDMAP_L1C_MINB)
+  const int l1_minb = minb3 ? 4 : (Mn <= 20 ? 3 : 2);
+  for (int K = 2; K <= 3; K++) k.l1_head_bytes[K - 2] = l1_head_bytes(l1_head_rows(n, lo, Mn, K, l1_minb), lo, Mn);
   k.W = 2;
   k.l1_W = 2;
   k.l1_steps = true;

@@ -309,6 +309,7 @@ struct CoreKernels {
   int app_ks_auto;                         // default folded rows of this core's APP kernel
   void (*app_live[2][4])(const DecodeParams);  // live-window APP [KS - 1][KP = 0, 2, 3, 4] (spec only)
   int app_live_W;                          // its windows per lane (1 scalar, 2 pair core)
+  size_t l1_head_bytes[2];                 // pass-1 head-table smem of the K = 2, 3 class kernels
   void (*app_stored)(const DecodeParams);
   void (*gamma_dump)(const DecodeParams);
   long nodes;  // corridor nodes per lattice (0 = generic core: computed on host)
@@ -335,6 +336,7 @@ CoreKernels make_core_kernels(long nodes) {
   for (auto& r : k.app_live)
     for (auto& fn : r) fn = nullptr;
   k.app_live_W = 0;
+  k.l1_head_bytes[0] = k.l1_head_bytes[1] = 0;
   k.app_stored = k_app_stored<Core::Mn>;
   k.gamma_dump = k_gamma_dump<Core>;
   k.nodes = nodes;

@@ -176,12 +176,32 @@ __device__ __forceinline__ LaneGeom geom_step(const DecodeParams& p, const WinBa
   return G;
 }
 
+// Head tables of pass 1: lattice rows 1..KH depend only on the codeword's first KH bits, so at each
+// symbol index the lane computes them once for the 2^KH prefixes (both windows) and keeps row KH of
+// each in shared memory (its private column, no barrier); every symbol then starts from its prefix's
+// row instead of computing rows 1..KH (and initialising row 0): C2 saves rows 1-2, 17 of its 89
+// pass-1 nodes per symbol.  Same operations per node: bit-identical.  KH is the largest of 2, 1, 0
+// whose tables (structurally-zero nodes left out) fit beside s_res at the kernel's CTAs per SM.
+__host__ __device__ constexpr int l1_head_e0(int R, int LO) { return (R + LO) < 0 ? -(R + LO) : 0; }
+__host__ __device__ constexpr size_t l1_head_bytes(int KH, int LO, int MN) {
+  return KH == 0 ? 0 : (size_t)(1 << KH) * (size_t)(MN - l1_head_e0(KH, LO)) * kLatticeThreads * 8;
+}
+__host__ __device__ constexpr int l1_head_rows(int NN, int LO, int MN, int K, int minb) {
+  // s_res [MN][128] f32x2 beside the tables; 227 KB per SM shared by minb CTAs, 2 KB margin each
+  return (2 <= NN - K && l1_head_bytes(2, LO, MN) + (size_t)MN * kLatticeThreads * 8 + 2048 <= 227u * 1024 / minb) ? 2
+       : (1 <= NN - K && l1_head_bytes(1, LO, MN) + (size_t)MN * kLatticeThreads * 8 + 2048 <= 227u * 1024 / minb) ? 1
+                                                                                                                   : 0;
+}
+
 template <class Core, int K, bool kPri = true>
 __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1C_MINB) k_gamma_sum_x2_cls(const DecodeParams p) {
   constexpr int MN = Core::Mn;
   constexpr int NC = 1 << K;
+  constexpr int KH = l1_head_rows(Core::NNr, Core::Lo, MN, K, BSIDMAP_L1C_MINB);
+  constexpr int E0 = l1_head_e0(KH, Core::Lo);
   extern __shared__ __align__(128) unsigned char smem[];
   f32x2* s_res = reinterpret_cast<f32x2*>(smem);  // [MN][128] per-lane result (private column, no barrier)
+  f32x2* s_head = s_res + MN * kLatticeThreads + threadIdx.x;  // [2^KH][MN - E0][128]: this lane's column
   const long ga = (long)blockIdx.x * (2 * blockDim.x) + threadIdx.x;
   const WinBase ba = win_base(p, ga), bb = win_base(p, ga + blockDim.x);
   const int i0 = p.i_base + blockIdx.y * p.i_steps, i1 = min(i0 + p.i_steps, p.i_end);
@@ -202,6 +222,15 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1C_MINB) k_gamma_sum
     if (__any_sync(0xffffffffu, A.active || B.active)) {
       typename Core::Lane lane;
       Core::init(lane, A.active ? win_bits(wa, A.s) : 0ull, B.active ? win_bits(wb, B.s) : 0ull, p);
+      if constexpr (KH > 0) {  // rows 1..KH of every prefix, once per symbol index
+#pragma unroll 1
+        for (int pf = 0; pf < (1 << KH); pf++) {
+          f32x2 h[MN];
+          Core::template run_head<KH, 1>(lane, (uint32_t)pf, p, h);
+#pragma unroll
+          for (int e = E0; e < MN; e++) s_head[(pf * (MN - E0) + (e - E0)) * kLatticeThreads] = h[e];
+        }
+      }
       const float* pa = p.priors ? p.priors + ((size_t)A.f * p.N + i) * p.q : nullptr;
       const float* pb = p.priors ? p.priors + ((size_t)B.f * p.N + i) * p.q : nullptr;
       f32x2* res = s_res + threadIdx.x;  // res[e * 128]: the sum over the finished classes
@@ -236,7 +265,14 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1C_MINB) k_gamma_sum
         };
         // the class-sum update inside the last row group's basic block (rows_then); uniform priors:
         // the common factor 1/q is applied at the store
-        Core::template run_prefix_then<K, BSIDMAP_L1_GROUP>(lane, x, p, fo, add);
+        if constexpr (KH > 0) {
+          const f32x2* hp = s_head + (x & ((1u << KH) - 1u)) * (MN - E0) * kLatticeThreads;
+#pragma unroll
+          for (int e = 0; e < MN; e++) fo[e] = e < E0 ? 0ull : hp[(e < E0 ? 0 : e - E0) * kLatticeThreads];
+          Core::template run_from_then<KH + 1, Core::NNr - K, BSIDMAP_L1_GROUP>(lane, x, p, fo, add);
+        } else {
+          Core::template run_prefix_then<K, BSIDMAP_L1_GROUP>(lane, x, p, fo, add);
+        }
       }
       Core::template apply_last_rows<K>(lane, cur, p, acc);
       if (!first) {
@@ -453,6 +489,12 @@ CoreKernels make_core_kernels_x2_base(long nodes) {
   k.app_live[1][2] = k_app_live_x2<Core, 3, 2>;
   k.app_live[1][3] = k_app_live_x2<Core, 4, 2>;
   k.app_live_W = 2;
+  {
+    using Core_ = Core;
+    constexpr int minb = BSIDMAP_L1C_MINB;
+    for (int K = 2; K <= 3; K++)
+      k.l1_head_bytes[K - 2] = l1_head_bytes(l1_head_rows(Core_::NNr, Core_::Lo, Core_::Mn, K, minb), Core_::Lo, Core_::Mn);
+  }
   k.app_stored = k_app_stored<Core::Mn>;
   k.gamma_dump = k_gamma_dump_x2<Core>;
   k.nodes = nodes;

@@ -43,6 +43,7 @@ template <int NN, int LO, int MN>
 struct SpecCoreX2 {
   static constexpr int Mn = MN;
   static constexpr int NNr = NN;  // lattice rows n
+  static constexpr int Lo = LO;   // m_n^-
   static constexpr int W = 2;
   static constexpr int J = NN + LO + MN - 1;  // last window column n + m_n^+
   static_assert(MN >= 1 && MN <= kMaxMn && LO <= 0 && LO + MN - 1 >= 0 && J <= kMaxWindow, "shape");
@@ -149,6 +150,14 @@ struct SpecCoreX2 {
     for (int e = 0; e < MN; e++) f[e] = pk(p.lc.row0[e], p.lc.row0[e]);
     rows<1, G, KP>(f, x, L, pk(p.lc.a, p.lc.a));
   }
+  // Rows R0..RL on f (already holding row R0 - 1), then tail(f) in the last group's basic block.
+  template <int R0, int RL, int G, class Tail>
+  __device__ __forceinline__ static void run_from_then(const Lane& L, uint32_t x, const DecodeParams& p,
+                                                       f32x2 (&f)[MN], Tail& tail) {
+    rows_then<R0, G, RL>(f, x, L, pk(p.lc.a, p.lc.a), tail);
+  }
+  // First node of row R that can be non-zero (nodes e with column R + m_n^- + e < 0 are structurally 0).
+  static constexpr int row_e0(int R) { return (R + LO) < 0 ? -(R + LO) : 0; }
   template <int KP, int G = 1>
   __device__ __forceinline__ static void run_tail(const Lane& L, uint32_t x, const DecodeParams& p, f32x2 (&f)[MN]) {
     rows<KP + 1, G, NN - 1>(f, x, L, pk(p.lc.a, p.lc.a));
