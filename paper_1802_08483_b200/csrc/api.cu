@@ -259,8 +259,12 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
     if (d->ab_stages > 0) P->ab_stages = d->ab_stages;
     if (d->ab_threads > 0) P->ab_threads = std::min(1024, d->ab_threads);
     P->ab_smem = ab_cta_smem(d->Mn, Mtp, P->ab_stages);
-    if (mode != kSchedLocal && mode != kSchedLocalCta && P->ab_smem > 227u * 1024)
-      return fail(d, BSIDMAP_EPLAN, "M_n x M_tau too large for the shared-memory Gamma ring of the alpha/beta kernel");
+    if (P->ab_smem > 227u * 1024) {  // a Gamma_i block beyond shared memory: read it from global (L2)
+      P->ab_stages = 0;
+      P->ab_smem = ab_cta_smem(d->Mn, Mtp, 0);
+      if (mode != kSchedLocal && mode != kSchedLocalCta && P->ab_smem > 227u * 1024)
+        return fail(d, BSIDMAP_EPLAN, "M_tau too large for the alpha/beta state rows in shared memory");
+    }
   }
   P->ab_warp = nullptr;
   P->ab_cta = d->kern.ab_cta ? d->kern.ab_cta : k_alpha_beta_cta<0>;

@@ -41,7 +41,9 @@ __global__ void __launch_bounds__(1024) k_alpha_beta_cta(const DecodeParams p, i
   const float* Gf = p.Gsum + (size_t)f * N * Mn * Mtp;
   const uint32_t blk = (uint32_t)(Mn * Mtp * 4);
   auto gblock = [&](int step) { return Gf + (size_t)(fwd ? step : N - 1 - step) * Mn * Mtp; };
-  if (tid == 0) {
+  // stages == 0: a Gamma_i block larger than shared memory (wide trellises, e.g. C4's channel at
+  // N = 1e5: M_n x M_tau x 4 > 227 KB) -- the CTA reads it straight from global memory (L2)
+  if (tid == 0 && stages > 0) {
     for (int s = 0; s < stages; s++) mbar_init(bars + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int s = 0; s < stages && s < N; s++) {
@@ -63,9 +65,9 @@ __global__ void __launch_bounds__(1024) k_alpha_beta_cta(const DecodeParams p, i
   const int m_lo_in = lo + Mn - 1, m_hi_in = Mt - 1 + lo;
   double inv_c = 1.0;  // scale of the current row (any constant: every row is normalised by its sum)
   for (int step = 0; step < N; step++) {
-    const int stage = step % stages;
-    mbar_wait(bars + stage, (uint32_t)(step / stages) & 1u);
-    const float* G = ring + (size_t)stage * Mn * Mtp;
+    const int stage = stages > 0 ? step % stages : 0;
+    if (stages > 0) mbar_wait(bars + stage, (uint32_t)(step / stages) & 1u);
+    const float* G = stages > 0 ? ring + (size_t)stage * Mn * Mtp : gblock(step);
     const double* cur = Rb + (step & 1) * RW + Mn;
     double* nxt = Rb + ((step + 1) & 1) * RW + Mn;
     double ps = 0.0;
@@ -105,7 +107,7 @@ __global__ void __launch_bounds__(1024) k_alpha_beta_cta(const DecodeParams p, i
     double* pp = part + ((step + 1) & 1) * 32;
     if (lane == 0) pp[warp] = ps;
     __syncthreads();  // nxt and the partials are complete; the ring stage is consumed
-    if (tid == 0 && step + stages < N) {
+    if (tid == 0 && stages > 0 && step + stages < N) {
       mbar_expect_tx(bars + stage, blk);
       tma_bulk_g2s(ring + (size_t)stage * Mn * Mtp, gblock(step + stages), blk, bars + stage);
     }
@@ -115,7 +117,7 @@ __global__ void __launch_bounds__(1024) k_alpha_beta_cta(const DecodeParams p, i
     if (!(c > 0.0)) {  // all-zero row: Y impossible under the limits (reading R14)
       if (tid == 0) {
         p.status[f] = kFrameUnderflow;
-        for (int t = step + 1; t < N && t <= step + stages; t++)  // drain issued copies
+        for (int t = step + 1; stages > 0 && t < N && t <= step + stages; t++)  // drain issued copies
           mbar_wait(bars + t % stages, (uint32_t)(t / stages) & 1u);
       }
       return;

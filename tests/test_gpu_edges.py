@@ -184,3 +184,18 @@ def test_app_dynamic_range_near_the_floor(name, N, frames):
     for mode in (2, 3):
         _, L, st = run_gpu(cfg, b, mode)
         assert_parity(L, st, res)
+
+
+def test_wide_trellis_alpha_beta_reads_gamma_from_global():
+    """A trellis whose Gamma_i block (M_n x M_tau FP32) exceeds shared memory -- C4's code and
+    channel (M_n = 26) with M_tau = 2401 (the width C4's channel needs at N ~ 1.5e5): the CTA alpha/beta
+    recursion reads Gamma_i from global memory instead of the TMA ring (every schedule
+    used to fail with EPLAN there).  Against the FP64 oracle in the Gamma-sum and stored schedules."""
+    import dataclasses
+    cfg = dataclasses.replace(bsidgen.configs()["C4"], N=12, mt=(-1200, 1200))
+    assert cfg.Mn * ((cfg.Mt + 7) // 8 * 8) * 4 > 227 * 1024
+    b = bsidgen.make_batch(cfg, 3, 3)
+    res = run_oracle(cfg, b)
+    for mode in (3, 1):
+        d, L, st = run_gpu(cfg, b, mode)
+        assert_parity(L, st, res)
