@@ -65,24 +65,27 @@ __device__ __forceinline__ int live_slot(const LiveRows& r, int G, int e) {
   return g;
 }
 
-// Per-frame FP64 sums of the staged per-lane terms: lanes of one frame are contiguous.
+// Per-frame FP64 sums of the staged per-lane terms: the lanes of one frame are contiguous and each
+// frame's sum continues from where its previous round left it, so S(D) is the sequential sum over the
+// frame's live windows in state order whatever the packing (G, the round a frame starts in): the
+// result does not depend on the batch size, chunking or sharding.
 template <class T>
 __device__ __forceinline__ void live_reduce(const DecodeParams& p, const T* stg, const double* sc, const int* sg,
                                             double* S, int lane) {
   for (int D = lane; D < p.q; D += 32) {
-    double acc = 0.0;
     int cur = sg[0];
+    double acc = cur >= 0 ? S[cur * p.q + D] : 0.0;
 #pragma unroll 4
     for (int l = 0; l < 32; l++) {
       const int gl = sg[l];
       if (gl != cur) {
-        if (cur >= 0) S[cur * p.q + D] += acc;
-        acc = 0.0;
+        if (cur >= 0) S[cur * p.q + D] = acc;
         cur = gl;
+        acc = cur >= 0 ? S[cur * p.q + D] : 0.0;
       }
-      acc += sc ? (double)stg[D * 33 + l] * sc[l] : (double)stg[D * 33 + l];
+      if (cur >= 0) acc += sc ? (double)stg[D * 33 + l] * sc[l] : (double)stg[D * 33 + l];
     }
-    if (cur >= 0) S[cur * p.q + D] += acc;
+    if (cur >= 0) S[cur * p.q + D] = acc;
   }
 }
 
@@ -149,7 +152,7 @@ __global__ void __launch_bounds__(kLatticeThreads, KS == 2 ? BSIDMAP_APP_MINB_KS
 #pragma unroll
       for (int u = 0; u < MN; u++) bt[u] = pk(ba[u], bb[u]);
     }
-    sg[lane] = (da > 0.0 || db > 0.0) ? g : -1;
+    sg[lane] = in ? g : -1;  // the frame's lanes stay one segment (a window of weight 0 adds 0.0)
     if (__any_sync(0xffffffffu, da > 0.0 || db > 0.0)) {
       typename Core::Lane lane_t;
       Core::init(lane_t, A.active ? load_window(p, A.f, A.s, A.rho) : 0ull,
@@ -202,7 +205,8 @@ __global__ void __launch_bounds__(kLatticeThreads, KS == 2 ? BSIDMAP_APP_MINB_KS
           Core::template run_to_then<RL, BSIDMAP_APP_GROUP>(lane_t, x, p, fo, dot);
         }
         const int D = KP > 0 ? (int)Di[k] : k;
-        stg[D * 33 + lane] = fma(da, (double)(lo_of(t0) + lo_of(t1)), db * (double)(hi_of(t0) + hi_of(t1)));
+        stg[D * 33 + lane] =
+            (da > 0.0 || db > 0.0) ? fma(da, (double)(lo_of(t0) + lo_of(t1)), db * (double)(hi_of(t0) + hi_of(t1))) : 0.0;
       }
     } else {
       for (int D = 0; D < p.q; D++) stg[D * 33 + lane] = 0.0;
@@ -250,7 +254,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_LIVE1_MINB) k_app_liv
     const double da = app_weights_p2<MN>(p, A, i, bt);
     const int E = da > 0.0 ? exp2_of(da) : 0;
     const float wa = (float)(da * pow2d(-E));
-    sg[lane] = da > 0.0 ? g : -1;
+    sg[lane] = in ? g : -1;  // the frame's lanes stay one segment (a window of weight 0 adds 0.0)
     sc[lane] = pow2d(E);
     if (__any_sync(0xffffffffu, da > 0.0)) {
       typename Core::Lane lane_t;
@@ -314,7 +318,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_LIVE1_MINB) k_app_liv
             }
           }
         }
-        stg[D * 33 + lane] = wa * (t0 + t1);
+        stg[D * 33 + lane] = da > 0.0 ? wa * (t0 + t1) : 0.f;
       }
     } else {
       for (int D = 0; D < p.q; D++) stg[D * 33 + lane] = 0.f;

@@ -100,7 +100,10 @@ __global__ void k_live(const DecodeParams p) {
     hi = __reduce_max_sync(0xffffffffu, hi);
     if (s > 0.0 && hi >= lo) out = make_int2(lo, (hi - lo + 2) & ~1);
   }
-  if (lane == 0) p.live[row] = out;
+  if (lane == 0) {
+    p.live[row] = out;
+    if (p.live_total && out.y) atomicAdd(p.live_total, (unsigned long long)out.y);
+  }
 }
 
 // One warp per (frame, i) row.
