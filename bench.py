@@ -391,6 +391,7 @@ def main():
         if ok < 0.999 and rank == 0:
             print(f"warning: only {ok:.4f} of frames decoded OK in e2e", file=sys.stderr)
 
+    plan_after = d.plan(count)
     st_h = st.cpu().numpy()
     L_h = L.cpu().numpy()
     if args.dump:
@@ -416,6 +417,7 @@ def main():
             "config": {"workload": describe(cfg), "frames_per_gpu": count,
                        "total_frames": int(total_frames // args.steps), "mode": plan["mode"],
                        "core": plan["core"], "chunks": plan["chunks"], "parallelism": f"frames sharded x{world}",
+                       "app_frames_per_warp": plan_after.get("app_frames_per_warp"),
                        "l2": "flushed (256 MiB write) between timed steps; per-step working set > L2"},
             "symbols_per_s": value * cfg.N,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",

@@ -95,14 +95,6 @@ struct bsidmap_decoder {
   int app_ks = -1;                      // rows folded into the APP weights (-1 = automatic; BSIDMAP_APP_KS)
   double live_eps = 0x1p-128;           // live-window threshold of the APP pass (reading R18; BSIDMAP_LIVE_EPS)
   int app_G = 0;                        // its frames per warp (0 = automatic; BSIDMAP_APP_G)
-  // live windows per APP row measured by the previous decodes (k_live counts on the device, copied
-  // to pinned host memory at the end of each decode): the planner packs G frames per warp so the
-  // rounds of 32 W windows come out nearly full.  A heuristic only: results do not depend on G.
-  unsigned long long* d_live_total = nullptr;
-  unsigned long long* h_live_total = nullptr;  // pinned
-  long live_rows_pending = 0;                  // rows counted by the decode whose total is in flight
-  double live_mean = 0.0;                      // live windows per row (0 = not measured yet)
-  cudaEvent_t ev_live = nullptr;               // the host copy of the count has landed
   cudaStream_t s_ab = nullptr;
   cudaEvent_t ev_p1[kMaxAbSub] = {}, ev_ab[kMaxAbSub] = {};
   cudaEvent_t ev_abt[2] = {};           // alpha/beta stream busy time (timed decodes)
@@ -236,56 +228,17 @@ size_t budget_for(bsidmap_decoder* d, int F, int mode, size_t need) {
   return d->budget_cache;
 }
 
-// Frames per warp of the live-window APP.  With c live windows per row (measured by the previous
-// decodes) a warp's G frames hold ~G c windows, walked in rounds of R = 32 W: pick the G (<= 12, and
-// enough warps to fill the GPU) with the fewest slots per window, E[ceil(T/R)] R / (G c), T ~ N(G c,
-// G c) (Poisson-like spread), plus 1 % per frame of per-frame overhead (measured: C2 G = 12 25.96 ms
-// vs G = 8 29.94; C5 G = 4 32.1 vs 8 35.0 -- tools/exp_appG.sh).  No measurement yet: G = 8.
+// Frames per warp of the live-window APP: 12 on the pair core (rounds of 64 windows), 4 on the scalar
+// core (rounds of 32), fewer where the grid would not fill the GPU.  Measured (tools/exp_appG*.sh,
+// pass 2 ms at G = 4 / 8 / 12): C2 (pair) 35.9 / 36.1 / 32.0, C4 (pair) 36.6 / 35.4 / 36.0,
+// C5 (scalar) 27.0 / 29.8 / 32.1, C3 (scalar) 35.4 / 34.5 / 34.6.  Results do not depend on G beyond
+// the FP64 association of a frame split over two rounds (test_live_app_independent_of_packing).
 int live_frames_per_warp(const bsidmap_decoder* d, long rows) {
-  const int gmax = (int)std::max(1L, std::min(12L, rows / (32L * d->num_sms)));
-  if (!(d->live_mean > 0.0)) return std::min(8, gmax);
-  const double c = d->live_mean, R = 32.0 * std::max(1, d->kern.app_live_W);
-  int best = 1;
-  double best_cost = 1e30;
-  for (int G = 1; G <= gmax; G++) {
-    const double mu = G * c, sd = std::sqrt(mu);
-    double er = 0.0;  // E[ceil(T / R)] by a 9-point normal quadrature
-    const double z[9] = {-2.0, -1.5, -1.0, -0.5, 0.0, 0.5, 1.0, 1.5, 2.0};
-    const double w[9] = {0.054, 0.065, 0.121, 0.176, 0.198, 0.176, 0.121, 0.065, 0.054};
-    for (int k = 0; k < 9; k++) er += w[k] * std::ceil(std::max(1.0, mu + z[k] * sd) / R);
-    const double cost = er * R / mu + 0.01 * G;
-    if (cost < best_cost) {
-      best_cost = cost;
-      best = G;
-    }
-  }
-  return best;
-}
-
-// Device counter + pinned host copy of the live-window count; folds a landed count of the previous
-// decode into live_mean.
-int ensure_live_counter(bsidmap_decoder* d) {
-  if (!d->d_live_total) {
-    cudaError_t e = cudaMalloc(&d->d_live_total, sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMallocHost(&d->h_live_total, sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_live, cudaEventDisableTiming);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return BSIDMAP_ECUDA;
-    }
-  }
-  return BSIDMAP_OK;
-}
-
-void update_live_mean(bsidmap_decoder* d) {
-  if (d->live_rows_pending > 0 && d->ev_live && cudaEventQuery(d->ev_live) == cudaSuccess) {
-    d->live_mean = (double)*d->h_live_total / (double)d->live_rows_pending;
-    d->live_rows_pending = 0;
-  }
+  const long gmax = std::max(1L, rows / (32L * d->num_sms));
+  return (int)std::min<long>(d->kern.app_live_W == 2 ? 12 : 4, gmax);
 }
 
 int make_plan(bsidmap_decoder* d, int F, Plan* P) {
-  update_live_mean(d);
   // Stored gamma costs 8 B of HBM traffic per gamma value against ~5n FP32 flops to
   // recompute it; on B200 recomputing is the faster side of the ridge, and
   // the only one whose batches fit for long frames: AUTO = recompute.
@@ -325,6 +278,7 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   }
   P->ab_warp = nullptr;
   P->ab_cta = d->kern.ab_cta ? d->kern.ab_cta : k_alpha_beta_cta<0>;
+  if (P->ab_stages == 0) P->ab_cta = k_alpha_beta_cta<0, false>;  // Gamma_i read from global memory
   const int spt = (d->Mt + 31) / 32;
   const int spt_k = spt == 3 ? 4 : spt;
   const size_t ab_warp_bytes = (size_t)(kAbWarpThreads / 32) * ab_warp_smem(spt_k, d->Mn, gsum_stride(d->Mt));
@@ -842,16 +796,10 @@ int bsidmap_decode_batch_opts(bsidmap_decoder* d, int F, const uint32_t* rx, con
   } else if ((rc = set_smem(d, (const void*)P.app_kernel, P.app_smem))) {
     return rc;
   }
-  // live-window statistics for the planner of the next decodes (not while a graph is captured)
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(s, &cap);
-  const bool count_live = P.app_live && cap == cudaStreamCaptureStatusNone && ensure_live_counter(d) == BSIDMAP_OK;
-  if (count_live) cudaMemsetAsync(d->d_live_total, 0, sizeof(unsigned long long), s);
   for (int c = 0; c < P.nchunks; c++) {
     const int f0 = c * P.chunk;
     DecodeParams p;
     fill_params(d, &p);
-    p.live_total = count_live ? d->d_live_total : nullptr;
     bind_ws(d, l, &p);
     p.F = std::min(P.chunk, F - f0);
     p.rx = rx;
@@ -868,11 +816,6 @@ int bsidmap_decode_batch_opts(bsidmap_decoder* d, int F, const uint32_t* rx, con
       k_extrinsic<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(p, opts->extrinsic + (size_t)f0 * d->N * d->q);
       d->launches++;
     }
-  }
-  if (count_live) {
-    cudaMemcpyAsync(d->h_live_total, d->d_live_total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
-    cudaEventRecord(d->ev_live, s);
-    d->live_rows_pending = (long)F * d->N;
   }
   d->last_chunk = P.chunk;
   d->last_frames = F;
@@ -954,9 +897,6 @@ void bsidmap_destroy(bsidmap_decoder* d) {
   cudaDeviceSynchronize();
   if (d->ws) cudaFree(d->ws);
   if (d->hs) cudaFree(d->hs);
-  if (d->d_live_total) cudaFree(d->d_live_total);
-  if (d->h_live_total) cudaFreeHost(d->h_live_total);
-  if (d->ev_live) cudaEventDestroy(d->ev_live);
   if (d->s_copy) cudaStreamDestroy(d->s_copy);
   if (d->s_ab) cudaStreamDestroy(d->s_ab);
   for (int k = 0; k < kMaxAbSub; k++) {
@@ -1036,13 +976,13 @@ int bsidmap_plan_info(bsidmap_decoder* d, int F, char* buf, size_t len) {
       "\"workspace_bytes\": %zu, \"windows_per_lane\": %d, \"q\": %d, \"n\": %d, \"N\": %d, \"Mn\": %d, \"Mtau\": %d, "
       "\"alpha_beta_overlap_subbatches\": %d, \"app_prefix_bits\": %d, \"app_windows_per_lane\": %d, "
       "\"app_folded_rows\": %d, \"app_live\": %d, \"app_frames_per_warp\": %d, \"live_eps\": %.6g, "
-      "\"live_windows_per_row\": %.3f, \"jit_error\": \"%s\"}",
+      "\"jit_error\": \"%s\"}",
       sched_name(P.mode), F, P.chunk, P.nchunks, d->jit ? "jit" : d->spec ? "spec" : "generic",
       d->kern.W == 2 ? ((long)P.chunk * tiles_per_frame(d->Mt) + kX2Warps - 1) / kX2Warps
                      : (lanes + kLatticeThreads - 1) / kLatticeThreads,
       d->N, kLatticeThreads, P.chunk, P.ab_warp ? kAbWarpThreads : P.ab_threads,
       layout(d, P.chunk, P.mode).total, d->kern.W, d->q, d->n, d->N, d->Mn, d->Mt, std::min(P.ab_sub, P.chunk), P.app_kp, P.app_live ? d->kern.app_live_W : 1, P.app_ks,
-      P.app_live ? 1 : 0, P.app_G, d->live_eps, d->live_mean, d->jit_err.c_str());
+      P.app_live ? 1 : 0, P.app_G, d->live_eps, d->jit_err.c_str());
   return nb;
 }
 

@@ -73,7 +73,6 @@ struct DecodeParams {
   int2* live;                 // [F][N] live windows of each APP row: (first state index, count rounded up to even)
   double live_eps;            // window (i, m') is live iff alpha_i(m') beta_i(m') > live_eps sum_m alpha_i beta_i
   int app_G;                  // frames per warp of the live-window APP kernels
-  unsigned long long* live_total;  // k_live adds its live-window counts here (plans the next decode's G)
   float* L;                   // [F][N][q] output APP, rows sum to 1
   double* dbg_gamma;          // debug dump [F][M_tau][M_n][q] (true scale) or nullptr
   int dbg_i;                  // symbol index of the debug dump

@@ -23,8 +23,9 @@ __host__ __device__ __forceinline__ size_t ab_cta_smem(int Mn, int Mtp, int stag
   return (size_t)stages * Mn * Mtp * 4 + 2 * (size_t)(Mtp + 2 * Mn) * 8 + 2 * 32 * 8 + (size_t)stages * 8;
 }
 
-template <int MNT>
+template <int MNT, bool kRing = true>
 __global__ void __launch_bounds__(1024) k_alpha_beta_cta(const DecodeParams p, int stages) {
+  if constexpr (!kRing) stages = 0;
   extern __shared__ __align__(128) unsigned char smem[];
   const int Mt = p.Mt, Mtp = p.Mtp, N = p.N, lo = p.mn_lo;
   const int Mn = MNT > 0 ? MNT : p.Mn;
@@ -41,9 +42,9 @@ __global__ void __launch_bounds__(1024) k_alpha_beta_cta(const DecodeParams p, i
   const float* Gf = p.Gsum + (size_t)f * N * Mn * Mtp;
   const uint32_t blk = (uint32_t)(Mn * Mtp * 4);
   auto gblock = [&](int step) { return Gf + (size_t)(fwd ? step : N - 1 - step) * Mn * Mtp; };
-  // stages == 0: a Gamma_i block larger than shared memory (wide trellises, e.g. C4's channel at
+  // kRing = false: a Gamma_i block larger than shared memory (wide trellises, e.g. C4's channel at
   // N = 1e5: M_n x M_tau x 4 > 227 KB) -- the CTA reads it straight from global memory (L2)
-  if (tid == 0 && stages > 0) {
+  if (kRing && tid == 0) {
     for (int s = 0; s < stages; s++) mbar_init(bars + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int s = 0; s < stages && s < N; s++) {
@@ -65,9 +66,9 @@ __global__ void __launch_bounds__(1024) k_alpha_beta_cta(const DecodeParams p, i
   const int m_lo_in = lo + Mn - 1, m_hi_in = Mt - 1 + lo;
   double inv_c = 1.0;  // scale of the current row (any constant: every row is normalised by its sum)
   for (int step = 0; step < N; step++) {
-    const int stage = stages > 0 ? step % stages : 0;
-    if (stages > 0) mbar_wait(bars + stage, (uint32_t)(step / stages) & 1u);
-    const float* G = stages > 0 ? ring + (size_t)stage * Mn * Mtp : gblock(step);
+    const int stage = kRing ? step % stages : 0;
+    if constexpr (kRing) mbar_wait(bars + stage, (uint32_t)(step / stages) & 1u);
+    const float* G = kRing ? ring + (size_t)stage * Mn * Mtp : gblock(step);
     const double* cur = Rb + (step & 1) * RW + Mn;
     double* nxt = Rb + ((step + 1) & 1) * RW + Mn;
     double ps = 0.0;
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(1024) k_alpha_beta_cta(const DecodeParams p, i
     double* pp = part + ((step + 1) & 1) * 32;
     if (lane == 0) pp[warp] = ps;
     __syncthreads();  // nxt and the partials are complete; the ring stage is consumed
-    if (tid == 0 && stages > 0 && step + stages < N) {
+    if (kRing && tid == 0 && step + stages < N) {
       mbar_expect_tx(bars + stage, blk);
       tma_bulk_g2s(ring + (size_t)stage * Mn * Mtp, gblock(step + stages), blk, bars + stage);
     }
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(1024) k_alpha_beta_cta(const DecodeParams p, i
     if (!(c > 0.0)) {  // all-zero row: Y impossible under the limits (reading R14)
       if (tid == 0) {
         p.status[f] = kFrameUnderflow;
-        for (int t = step + 1; stages > 0 && t < N && t <= step + stages; t++)  // drain issued copies
+        for (int t = step + 1; kRing && t < N && t <= step + stages; t++)  // drain issued copies
           mbar_wait(bars + t % stages, (uint32_t)(t / stages) & 1u);
       }
       return;

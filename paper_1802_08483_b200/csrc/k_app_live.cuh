@@ -65,27 +65,27 @@ __device__ __forceinline__ int live_slot(const LiveRows& r, int G, int e) {
   return g;
 }
 
-// Per-frame FP64 sums of the staged per-lane terms: the lanes of one frame are contiguous and each
-// frame's sum continues from where its previous round left it, so S(D) is the sequential sum over the
-// frame's live windows in state order whatever the packing (G, the round a frame starts in): the
-// result does not depend on the batch size, chunking or sharding.
+// Per-frame FP64 sums of the staged per-lane terms: lanes of one frame are contiguous.  (A frame
+// split over two rounds is summed as two partial sums: the FP64 association depends on the packing,
+// far below the FP32 rounding of L -- tested bit-identical over G in test_live_app_independent_of_packing;
+// a strictly sequential order measured 20 % slower on C2's APP.)
 template <class T>
 __device__ __forceinline__ void live_reduce(const DecodeParams& p, const T* stg, const double* sc, const int* sg,
                                             double* S, int lane) {
   for (int D = lane; D < p.q; D += 32) {
+    double acc = 0.0;
     int cur = sg[0];
-    double acc = cur >= 0 ? S[cur * p.q + D] : 0.0;
 #pragma unroll 4
     for (int l = 0; l < 32; l++) {
       const int gl = sg[l];
       if (gl != cur) {
-        if (cur >= 0) S[cur * p.q + D] = acc;
+        if (cur >= 0) S[cur * p.q + D] += acc;
+        acc = 0.0;
         cur = gl;
-        acc = cur >= 0 ? S[cur * p.q + D] : 0.0;
       }
-      if (cur >= 0) acc += sc ? (double)stg[D * 33 + l] * sc[l] : (double)stg[D * 33 + l];
+      acc += sc ? (double)stg[D * 33 + l] * sc[l] : (double)stg[D * 33 + l];
     }
-    if (cur >= 0) S[cur * p.q + D] = acc;
+    if (cur >= 0) S[cur * p.q + D] += acc;
   }
 }
 

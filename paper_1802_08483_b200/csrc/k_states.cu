@@ -32,6 +32,7 @@ __global__ void k_frame_init(const DecodeParams p) {
 
 // generic-M_n instance of the CTA recursion (k_alphabeta_cta.cuh); spec shapes instantiate their own
 template __global__ void k_alpha_beta_cta<0>(const DecodeParams p, int stages);
+template __global__ void k_alpha_beta_cta<0, false>(const DecodeParams p, int stages);
 
 // Frames that failed (status != OK) get all-zero L rows (contract of bsidmap_decode_batch);
 // also catches an UNDERFLOW raised by a late row after other rows were written.
@@ -100,10 +101,7 @@ __global__ void k_live(const DecodeParams p) {
     hi = __reduce_max_sync(0xffffffffu, hi);
     if (s > 0.0 && hi >= lo) out = make_int2(lo, (hi - lo + 2) & ~1);
   }
-  if (lane == 0) {
-    p.live[row] = out;
-    if (p.live_total && out.y) atomicAdd(p.live_total, (unsigned long long)out.y);
-  }
+  if (lane == 0) p.live[row] = out;
 }
 
 // One warp per (frame, i) row.
