@@ -228,14 +228,14 @@ size_t budget_for(bsidmap_decoder* d, int F, int mode, size_t need) {
   return d->budget_cache;
 }
 
-// Frames per warp of the live-window APP: 12 on the pair core (rounds of 64 windows), 4 on the scalar
-// core (rounds of 32), fewer where the grid would not fill the GPU.  Measured (tools/exp_appG*.sh,
+// Frames per warp of the live-window APP: 12 on the pair core (rounds of 64 windows), 8 / 4 on the
+// scalar core (rounds of 32) for q <= 32 / larger, fewer where the grid would not fill the GPU.  Measured (tools/exp_appG*.sh,
 // pass 2 ms at G = 4 / 8 / 12): C2 (pair) 35.9 / 36.1 / 32.0, C4 (pair) 36.6 / 35.4 / 36.0,
 // C5 (scalar) 27.0 / 29.8 / 32.1, C3 (scalar) 35.4 / 34.5 / 34.6.  Results do not depend on G beyond
 // the FP64 association of a frame split over two rounds (test_live_app_independent_of_packing).
 int live_frames_per_warp(const bsidmap_decoder* d, long rows) {
   const long gmax = std::max(1L, rows / (32L * d->num_sms));
-  return (int)std::min<long>(d->kern.app_live_W == 2 ? 12 : 4, gmax);
+  return (int)std::min<long>(d->kern.app_live_W == 2 ? 12 : d->q <= 32 ? 8 : 4, gmax);
 }
 
 int make_plan(bsidmap_decoder* d, int F, Plan* P) {

@@ -9,6 +9,10 @@
 #ifndef BSIDMAP_SCALAR_MN_MAX
 #define BSIDMAP_SCALAR_MN_MAX 20
 #endif
+// the APP of those shapes on the scalar core (one window per lane)
+#ifndef BSIDMAP_SCALAR_APP_MN_MAX
+#define BSIDMAP_SCALAR_APP_MN_MAX BSIDMAP_SCALAR_MN_MAX
+#endif
 
 // pass 1 of those shapes stays on the pair class kernel at 3 CTAs/SM (k_lattice_x2.cuh; the scalar
 // class kernel measured slower: tools/exp_p1x2.sh)
@@ -20,7 +24,7 @@ CoreKernels spec_kernels() {
   CoreKernels k = make_core_kernels_x2<SpecCoreX2<NN, LO, MN>>(SpecCoreX2<NN, LO, MN>::nodes());
   k.ab_cta = k_alpha_beta_cta<MN>;
   local_cta_kernels<SpecCore<NN, LO, MN>>(&k);
-  if constexpr (SpecCoreX2<NN, LO, MN>::kMinBlocks <= 2 && MN <= BSIDMAP_SCALAR_MN_MAX) {
+  if constexpr (SpecCoreX2<NN, LO, MN>::kMinBlocks <= 2 && MN <= BSIDMAP_SCALAR_APP_MN_MAX) {
     // register-heavy pair shapes: the scalar-core APP measured faster (C3, C5)
     using S = SpecCore<NN, LO, MN>;
     // fold two rows where the per-symbol tail is short (C3: 90.4 -> 85.6 ms; C5, n = 12: 110 -> 113)
