@@ -963,6 +963,20 @@ int bsidmap_phase_times(bsidmap_decoder* d, float* ms, int n_max) {
 
 long bsidmap_last_launch_count(const bsidmap_decoder* d) { return d ? d->launches : 0; }
 
+namespace {
+// A message as the body of a JSON string: quotes and backslashes dropped, control characters as
+// spaces, at most max_len characters.
+std::string json_text(const std::string& m, size_t max_len) {
+  std::string o;
+  for (char c : m) {
+    if (o.size() >= max_len) break;
+    if (c == '"' || c == '\\') continue;
+    o += (static_cast<unsigned char>(c) < 0x20) ? ' ' : c;
+  }
+  return o;
+}
+}  // namespace
+
 int bsidmap_plan_info(bsidmap_decoder* d, int F, char* buf, size_t len) {
   if (!d || !buf || F < 1) return fail(d, BSIDMAP_EINVAL, "bad arguments");
   Plan P;
@@ -982,7 +996,7 @@ int bsidmap_plan_info(bsidmap_decoder* d, int F, char* buf, size_t len) {
                      : (lanes + kLatticeThreads - 1) / kLatticeThreads,
       d->N, kLatticeThreads, P.chunk, P.ab_warp ? kAbWarpThreads : P.ab_threads,
       layout(d, P.chunk, P.mode).total, d->kern.W, d->q, d->n, d->N, d->Mn, d->Mt, std::min(P.ab_sub, P.chunk), P.app_kp, P.app_live ? d->kern.app_live_W : 1, P.app_ks,
-      P.app_live ? 1 : 0, P.app_G, d->live_eps, d->jit_err.c_str());
+      P.app_live ? 1 : 0, P.app_G, d->live_eps, json_text(d->jit_err, 300).c_str());
   return nb;
 }
 
