@@ -81,10 +81,11 @@ __device__ __forceinline__ int exp2_of(double x) {  // floor(log2 x) for normal 
 #define BSIDMAP_L1C_MINB \
   (Core::kMinBlocks > 2 ? 4 : (Core::Mn <= BSIDMAP_SCALAR_MN_MAX ? BSIDMAP_L1C_MINB_LOW : Core::kMinBlocks))
 #endif
-// row pairs (ILP) in pass 1 (register-heavy shapes too: C3 pass 1 59.7 -> 58.3 ms, C5 equal;
-// tools/exp_p1g.sh)
+// row pairs (ILP) in pass 1 where the register budget allows 3 CTAs/SM; the register-heavy shapes
+// measured mixed (tools/exp_p1g.sh, r02m: C3 pass 1 59.7 -> 58.4 ms, C5 equal, C4 69.1 -> 72.3,
+// J1 143 -> 149), so they keep single rows
 #ifndef BSIDMAP_L1_GROUP
-#define BSIDMAP_L1_GROUP 2
+#define BSIDMAP_L1_GROUP (Core::kMinBlocks > 2 ? 2 : 1)
 #endif
 template <class Core, bool kStoreGamma>
 __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_x2(const DecodeParams p) {
