@@ -313,9 +313,8 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
     // share lattice rows 1..KP between symbols with equal first KP codeword bits
     P->app_kp = app_prefix_bits(d->q, d->n);
     if (d->app_kp >= 0) P->app_kp = (d->app_kp == 0 || d->app_kp > d->n - 2) ? 0 : std::min(4, std::max(2, d->app_kp));
-    // fold the last two lattice rows into the weights (four tables per lane in smem) for the
-    // register-heavy cores (2 CTAs/SM anyway: C4 89.1 -> 84.9 ms, C3 90.4 -> 85.6 ms; C2 at 4 -> 3
-    // CTAs/SM 57.2 -> 69.7 ms, tiled kernels of round 1)
+    // fold the last one or two lattice rows into the weights (the core's app_ks_auto: two on the
+    // scalar core, one on the pair core, by measurement; tools/exp_appkpks.sh)
     const int ks = d->app_ks > 0 ? d->app_ks : d->kern.app_ks_auto;
     P->app_ks = (ks == 2 && d->n >= 3) ? 2 : 1;
     auto smem = [&](int ksv, int g) {

@@ -27,8 +27,9 @@ CoreKernels spec_kernels() {
   if constexpr (SpecCoreX2<NN, LO, MN>::kMinBlocks <= 2 && MN <= BSIDMAP_SCALAR_APP_MN_MAX) {
     // register-heavy pair shapes: the scalar-core APP measured faster (C3, C5)
     using S = SpecCore<NN, LO, MN>;
-    // fold two rows where the per-symbol tail is short (C3: 90.4 -> 85.6 ms; C5, n = 12: 110 -> 113)
-    k.app_ks_auto = NN <= 10 ? 2 : 1;
+    // two folded rows on the scalar core (live-window APP: C3 pass 2 34.5 -> 32.4 ms, C5 26.8 -> 26.4;
+    // tools/exp_appkpks.sh)
+    k.app_ks_auto = 2;
     k.app_live[0][0] = k_app_live_x1<S, 0, 1>;
     k.app_live[0][1] = k_app_live_x1<S, 2, 1>;
     k.app_live[0][2] = k_app_live_x1<S, 3, 1>;

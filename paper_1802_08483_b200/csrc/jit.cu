@@ -292,7 +292,7 @@ bool jit_spec_kernels(int n, int lo, int Mn, CoreKernels* out, std::string* err,
   k.local_cta_bwd[0] = as_fn<F1>(ks[i++]);
   k.local_cta_bwd[1] = as_fn<F1>(ks[i++]);
   k.app = nullptr;
-  k.app_ks_auto = scalar_app ? (n <= 10 ? 2 : 1) : (minb3 ? 1 : 2);
+  k.app_ks_auto = scalar_app ? 2 : 1;  // as spec_kernels<> (inst.cuh) and make_core_kernels_x2_base
   k.app_live_W = scalar_app ? 1 : 2;
   k.nodes = (long)n * Mn - (long)lo * (lo - 1) / 2;
   // pass-1 head tables (k_lattice_x2.cuh l1_head_rows), at the class kernel's CTAs per SM (BSIDMAP_L1C_MINB)

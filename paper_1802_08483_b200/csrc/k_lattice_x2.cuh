@@ -481,7 +481,9 @@ CoreKernels make_core_kernels_x2_base(long nodes) {
   k.gamma_sum_k3_pri = k_gamma_sum_x2_cls<Core, 3, true>;
   k.gamma_store = k_gamma_sum_x2<Core, true>;
   k.app = nullptr;
-  k.app_ks_auto = Core::kMinBlocks <= 2 ? 2 : 1;
+  // one folded row on the pair core: two (four smem weight tables per lane) measured slower with the
+  // live-window APP (C4 pass 2 33.7 vs 23.7 ms, C2 29.4 vs 26.1; tools/exp_appkpks.sh)
+  k.app_ks_auto = 1;
   k.app_live[0][0] = k_app_live_x2<Core, 0, 1>;
   k.app_live[0][1] = k_app_live_x2<Core, 2, 1>;
   k.app_live[0][2] = k_app_live_x2<Core, 3, 1>;
