@@ -279,7 +279,8 @@ def test_app_two_folded_rows(name, frames, monkeypatch):
     assert d1.plan(frames)["app_folded_rows"] == 1
     monkeypatch.delenv("BSIDMAP_APP_KS")
     auto = _dec().from_config(cfg, b.C, mode=3, device=0).plan(frames)["app_folded_rows"]
-    assert auto == (1 if name in ("C1", "C2", "C5r") else 2)  # register-heavy shapes with short tails
+    # one folded row on the pair core (C1, C2, C4), two on the scalar APP core (C3, C5)
+    assert auto == (1 if name in ("C1", "C2", "C4") else 2)
     np.testing.assert_array_equal(st2, st1)
     np.testing.assert_allclose(L2, L1, rtol=2e-5, atol=1e-30)
     assert_parity(L2, st2, run_oracle(cfg, b))

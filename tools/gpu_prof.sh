@@ -5,7 +5,7 @@
 # at most 64 MiB) and kept only when KEEP_REP=1.  The source digest the capture was taken at goes
 # beside it (bench.py refuses a stale capture).
 # usage (under gpurun): bash tools/gpu_prof.sh <tag> <config> [frames] [extra bench args...]
-TAG=${1:-r02}; CFG=${2:-C2}; NF=${3:-}; shift 3 2>/dev/null
+TAG=${1:-r02}; CFG=${2:-C2}; NF=${3:-}; shift $(( $# < 3 ? $# : 3 ))
 OUT=gpurun_out/$TAG/$CFG; mkdir -p $OUT
 FR=${NF:+--frames $NF}
 python -c "from paper_1802_08483_b200._lib import source_digest; print(source_digest())" > $OUT/digest.txt
