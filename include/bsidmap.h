@@ -54,10 +54,13 @@ typedef struct bsidmap_decoder bsidmap_decoder; /* opaque; owns the device codeb
 #define BSIDMAP_MODE_AUTO 0      /* planner choice (= GAMMASUM, the fastest on B200) */
 #define BSIDMAP_MODE_STORED 1    /* paper's global storage: every gamma stored in HBM, read back for L */
 #define BSIDMAP_MODE_RECOMPUTE 2 /* paper's memory-reduced (local storage) schedule: gamma computed in
-                                    the alpha pass and again in the combined beta + L pass, only alpha rows kept
-                                    (fused per-frame passes with a specialised lattice core: one warp per frame
-                                    for M_tau <= 64, one CTA per frame for 64 < M_tau <= 1024; otherwise the
-                                    GAMMASUM schedule runs) */
+                                    a forward (alpha) sweep and again in a backward (beta + L) sweep.  On the
+                                    specialised / run-time compiled cores: in slabs of symbol indices (Gamma of
+                                    two slabs, all alpha rows, beta rows of three slabs; the backward sweep
+                                    recomputes gamma only where alpha != 0, R19).  Otherwise (or with
+                                    BSIDMAP_SLAB=0) fused per-frame passes keeping only alpha rows: one warp per
+                                    frame for M_tau <= 64, one CTA per frame for 64 < M_tau <= 1024; beyond that
+                                    the GAMMASUM schedule runs */
 #define BSIDMAP_MODE_GAMMASUM 3  /* memory-reduced variant with parallel passes: Gamma = sum_D gamma, alpha and
                                     beta kept; gamma recomputed once for L */
 
@@ -80,10 +83,14 @@ typedef struct bsidmap_decoder bsidmap_decoder; /* opaque; owns the device codeb
  * the defaults are the measured-fastest choices):
  *   BSIDMAP_AB_SUB=k   alpha/beta side-stream sub-batches (1 = off; default: 2 when 2F <= #SMs)
  *   BSIDMAP_APP_KP=k   APP prefix-sharing length (0 = off; default ~log2(q) - 1)
- *   BSIDMAP_APP_KS=k   lattice rows folded into the APP weights (1 or 2; default 2 for register-heavy shapes)
- *   BSIDMAP_LIVE_APP=0 tiled APP over every window instead of the live-window APP (default 1)
+ *   BSIDMAP_APP_KS=k   lattice rows folded into the APP weights (1 or 2; default 1 on the pair core,
+ *                      2 on the scalar APP core)
  *   BSIDMAP_LIVE_EPS=e live-window threshold (default 2^-128; 0 = skip exactly-zero windows only)
- *   BSIDMAP_APP_G=g    frames per warp of the live-window APP (default: up to 8)
+ *   BSIDMAP_APP_G=g    frames per warp of the live-window APP (default: up to 12 / 8 / 4)
+ *   BSIDMAP_JIT=0      shapes without a compiled unit run on the generic core (default: compiled at create)
+ *   BSIDMAP_SLAB=0     RECOMPUTE runs the per-frame local kernels instead of the slab schedule
+ *   BSIDMAP_SLAB_LEN=B symbol indices per slab (default: ~4 waves of pass-1 CTAs per slab)
+ *   BSIDMAP_SLAB_ASKIP=0  the backward sweep recomputes Gamma for every window (default: alpha != 0 only)
  *   BSIDMAP_AB_CTA_STAGES=k, BSIDMAP_AB_CTA_THREADS=t  ring depth / block size of the CTA alpha/beta
  *                      kernel (M_tau > 128; defaults: 1 stage when 2F >= 4 #SMs, ~M_tau/2 threads)
  */

@@ -69,6 +69,9 @@ struct bsidmap_decoder {
   CoreKernels kern{};
   bool spec = false;
   bool jit = false;                     // spec kernels compiled at run time (jit.cu)
+  bool slab_ok = false;                 // RECOMPUTE may run the slab schedule (spec cores)
+  int slab_fixed = 0;                   // symbol indices per slab (0 = automatic)
+  bool slab_askip = true;               // backward sweep: Gamma only where alpha != 0 (BSIDMAP_SLAB_ASKIP)
   std::string jit_err;                  // why a shape without a unit runs on the generic core
   LatticeConst lc{};
   // workspace
@@ -140,14 +143,36 @@ struct Layout {
 // the alpha pass and again in the beta + L pass, only alpha rows kept.  kSchedGammaSum keeps
 // Gamma = sum_D gamma between two parallel lattice passes.  kSchedStored keeps every gamma.
 // kSchedLocalCta is the same schedule with one CTA per frame (M_tau > 64).
-enum Sched { kSchedStored = 1, kSchedLocal = 2, kSchedGammaSum = 3, kSchedLocalCta = 4 };
+// kSchedSlab is the local storage in slabs of B symbol indices (the B200 form of P:483-522; DESIGN
+// 5): a forward sweep computes Gamma for one slab at a time (the fully parallel pass-1 kernel) and
+// runs alpha through it, a backward sweep recomputes Gamma only where alpha_i(m') != 0 (reading R19),
+// runs beta through it and the live-window APP over it; alpha and beta rows are kept, Gamma only
+// for two slabs in flight.
+enum Sched { kSchedStored = 1, kSchedLocal = 2, kSchedGammaSum = 3, kSchedLocalCta = 4, kSchedSlab = 5 };
+
+// Windows per Gamma slab: pass 1 of one slab is ~8 waves of 3 CTAs (256 windows x 8 symbol indices
+// each) on every SM; the slab length is a multiple of the pass-1 CTA's 8 symbol indices.  Measured
+// (C5, 32 frames; tools/exp_slab.py): slabs of 64 / 128 / 256 symbol indices 375 / 362 / 348 ms.
+constexpr long kSlabWindows = 8L * 3 * 256 * 8 * 148;
+int slab_len(const bsidmap_decoder* d, long F) {
+  if (d->slab_fixed > 0) return std::min(d->slab_fixed, d->N);  // BSIDMAP_SLAB_LEN (tests: many slabs at small N)
+  const long per_i = std::max(1L, F * d->Mt);
+  long B = (kSlabWindows + per_i - 1) / per_i;
+  B = (B + 7) / 8 * 8;
+  return (int)std::max(1L, std::min<long>(B, d->N));
+}
+// beta rows the slab schedule keeps per frame: a ring of three slabs (the backward sweep writes slab
+// b while the APP of slab b + 1 reads its rows and the first row of slab b + 2), or all N + 1
+int slab_beta_rows(const bsidmap_decoder* d, int B) { return std::min(d->N + 1, 3 * B); }
 
 int resolve_sched(const bsidmap_decoder* d, int mode) {
   if (mode == BSIDMAP_MODE_STORED) return kSchedStored;
   // AUTO: Gamma-sum -- fully parallel lattice passes; measured fastest on B200 (C2: 140.6 ms vs
   // 148.4 ms for the fused local schedule per 65536 frames, profiles/r01_*)
   if (mode == BSIDMAP_MODE_GAMMASUM || mode == BSIDMAP_MODE_AUTO) return kSchedGammaSum;
-  // RECOMPUTE: the paper's local schedule where a frame fits one warp tile, else Gamma-sum
+  // RECOMPUTE: the slab schedule on the spec cores (the live-window APP), else the paper's local
+  // schedule where a frame fits one warp tile or one CTA, else Gamma-sum
+  if (d->slab_ok && mode == BSIDMAP_MODE_RECOMPUTE) return kSchedSlab;
   if (d->kern.local_fwd && d->Mt <= kTileSlots) return kSchedLocal;
   if (d->kern.local_cta_bwd[0] && d->Mt <= 4 * kLocalCtaThreads &&
       local_cta_fwd_smem(d->Mn, gsum_stride(d->Mt)) <= 227u * 1024 &&
@@ -165,7 +190,7 @@ bool live_app_smem_fits(const CoreKernels& k, int q, int Mn) {
 
 // The Gamma-sum schedule runs the live-window APP (k_app_live.cuh) on the spec cores.
 bool uses_live_app(const bsidmap_decoder* d, int sched) {
-  if (sched != kSchedGammaSum || d->kern.app_live[0][0] == nullptr) return false;
+  if ((sched != kSchedGammaSum && sched != kSchedSlab) || d->kern.app_live[0][0] == nullptr) return false;
   return live_app_smem_fits(d->kern, d->q, d->Mn);
 }
 
@@ -173,16 +198,20 @@ const char* sched_name(int s) {
   return s == kSchedStored ? "stored"
          : s == kSchedLocal ? "recompute-local"
          : s == kSchedLocalCta ? "recompute-local-cta"
+         : s == kSchedSlab     ? "recompute-slab"
                                : "recompute-gammasum";
 }
 
 Layout layout(const bsidmap_decoder* d, long F, int sched) {
   Layout l{};
   const bool local = sched == kSchedLocal || sched == kSchedLocalCta;
-  l.gsum = local ? 0 : align_up((size_t)F * d->N * d->Mn * gsum_stride(d->Mt) * sizeof(float));
+  const size_t blocks = sched == kSchedSlab ? 2 * (size_t)slab_len(d, F) : (size_t)d->N;  // Gamma_i blocks per frame
+  l.gsum = local ? 0 : align_up((size_t)F * blocks * d->Mn * gsum_stride(d->Mt) * sizeof(float));
   l.gamma = sched == kSchedStored ? align_up((size_t)F * d->N * d->q * d->Mn * d->Mt * sizeof(float)) : 0;
   l.alpha = align_up((size_t)F * (d->N + 1) * d->Mt * sizeof(double));
-  l.beta = local ? 0 : l.alpha;
+  l.beta = local ? 0
+         : sched == kSchedSlab ? align_up((size_t)F * slab_beta_rows(d, slab_len(d, F)) * d->Mt * sizeof(double))
+                               : l.alpha;
   const bool live = uses_live_app(d, sched);
   l.lacc = (local || live) ? 0 : align_up((size_t)F * d->N * d->q * sizeof(double));
   l.live = live ? align_up((size_t)F * d->N * sizeof(int2)) : 0;
@@ -208,6 +237,7 @@ struct Plan {
   int app_ks;                              // lattice rows folded into the APP weights (1 or 2)
   bool app_live;                           // app_kernel is the live-window APP (k_app_live.cuh)
   int app_G;                               // its frames per warp
+  int slab;                                // symbol indices per Gamma slab (kSchedSlab)
 };
 
 size_t budget(const bsidmap_decoder* d) {
@@ -246,6 +276,14 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   const size_t per = layout(d, 1, mode).total;
   const size_t bud = budget_for(d, F, mode, layout(d, F, mode).total);
   long chunk = per ? (long)(bud / per) : F;
+  if (mode == kSchedSlab) {  // the Gamma slabs depend on the chunk (automatic length: ~constant bytes)
+    long lo = 0, hi = F;     // largest chunk whose whole layout fits the budget
+    while (lo < hi) {
+      const long mid = (lo + hi + 1) / 2;
+      if (layout(d, mid, mode).total <= bud) lo = mid; else hi = mid - 1;
+    }
+    chunk = lo;
+  }
   if (chunk < 1) return fail(d, BSIDMAP_ENOMEM, "workspace for one frame (" + std::to_string(per) +
                                                     " B) exceeds the budget (" + std::to_string(bud) + " B)");
   chunk = std::min<long>(chunk, F);
@@ -256,6 +294,7 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   P->mode = mode;
   P->chunk = (int)chunk;
   P->nchunks = (int)((F + chunk - 1) / chunk);
+  P->slab = mode == kSchedSlab ? slab_len(d, chunk) : d->N;
   // CTA alpha/beta: ~2 states per thread (smaller blocks, more of them resident per SM), and a
   // single-stage Gamma ring when the grid has several CTAs per SM -- the other resident CTAs hide
   // each one's copy latency (C3: 11.7 -> 7.7 ms, C4: 14.6 -> 11.9 ms; tools/exp_abcta*.sh).  The
@@ -272,7 +311,7 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
     if (P->ab_smem > 227u * 1024) {  // a Gamma_i block beyond shared memory: read it from global (L2)
       P->ab_stages = 0;
       P->ab_smem = ab_cta_smem(d->Mn, Mtp, 0);
-      if (mode != kSchedLocal && mode != kSchedLocalCta && P->ab_smem > 227u * 1024)
+      if (mode != kSchedLocal && mode != kSchedLocalCta && P->ab_smem > 227u * 1024)  // (slab too)
         return fail(d, BSIDMAP_EPLAN, "M_tau too large for the alpha/beta state rows in shared memory");
     }
   }
@@ -324,7 +363,8 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
     if (smem(P->app_ks, 1) > 227u * 1024) P->app_ks = 1;
     // up to 8 frames per warp (fewer partly filled rounds); fewer where the grid would not fill the
     // GPU or the per-frame sums would not fit in shared memory
-    const long rows = (long)chunk * d->N;
+    // rows of one APP launch: the chunk's, or one slab's (slab schedule)
+    const long rows = (long)chunk * (mode == kSchedSlab ? slab_len(d, chunk) : d->N);
     int G = d->app_G > 0 ? std::min(d->app_G, kLiveMaxG) : live_frames_per_warp(d, rows);
     while (G > 1 && smem(P->app_ks, G) > 227u * 1024) G--;
     P->app_kernel = d->kern.app_live[P->app_ks - 1][P->app_kp > 0 ? P->app_kp - 1 : 0];
@@ -336,11 +376,12 @@ int make_plan(bsidmap_decoder* d, int F, Plan* P) {
   // 401 vs 424 ms); with a full grid the recursions compete with the lattice passes for issue
   // slots and the step time is unchanged (C2, C4) or worse (C3: 212 vs 208 ms) -- tools/exp_ab.sh
   if (mode != kSchedGammaSum)
-    P->ab_sub = 1;
+    P->ab_sub = 1;  // (the slab schedule overlaps alpha/beta with the next slab's pass 1 instead)
   else if (d->ab_sub > 0)
     P->ab_sub = std::min(kMaxAbSub, d->ab_sub);
   else
     P->ab_sub = (!P->ab_warp && 2L * chunk <= d->num_sms) ? 2 : 1;
+  if (mode == kSchedSlab && !P->app_live) return fail(d, BSIDMAP_EPLAN, "slab schedule without the live-window APP");
   P->l1_smem = (d->kern.gamma_sum_k3 && mode != kSchedStored)
                    ? (size_t)d->Mn * kLatticeThreads * 8 + (size_t)d->q * 6 + 64 + 16 +
                          d->kern.l1_head_bytes[P->l1_kernel == d->kern.gamma_sum_k3 ? 1 : 0]
@@ -392,6 +433,12 @@ void fill_params(const bsidmap_decoder* d, DecodeParams* p) {
   }
   p->lc = d->lc;
   p->live_eps = d->live_eps;
+  p->gs_N = d->N;  // every Gamma_i block kept (the slab schedule narrows this per slab)
+  p->gs_i0 = 0;
+  p->ab_r0 = 0;    // alpha/beta: the whole recursion, both directions
+  p->ab_r1 = d->N;
+  p->ab_dir = -1;
+  p->beta_rows = d->N + 1;
 }
 
 void bind_ws(const bsidmap_decoder* d, const Layout& l, DecodeParams* p) {
@@ -431,10 +478,10 @@ DecodeParams sub_params(const DecodeParams& p, int f0, int nf) {
   if (s.alpha0) s.alpha0 += (size_t)f0 * Mt;
   if (s.betaN) s.betaN += (size_t)f0 * Mt;
   s.status += f0;
-  if (s.Gsum) s.Gsum += (size_t)f0 * N * p.Mn * p.Mtp;
+  if (s.Gsum) s.Gsum += (size_t)f0 * p.gs_N * p.Mn * p.Mtp;
   if (s.gamma) s.gamma += (size_t)f0 * N * q * p.Mn * Mt;
   s.alpha += (size_t)f0 * (N + 1) * Mt;
-  if (s.beta) s.beta += (size_t)f0 * (N + 1) * Mt;
+  if (s.beta) s.beta += (size_t)f0 * p.beta_rows * Mt;
   if (s.Lacc) s.Lacc += (size_t)f0 * N * q;
   if (s.live) s.live += (size_t)f0 * N;
   s.L += (size_t)f0 * N * q;
@@ -466,7 +513,8 @@ void (*pass1_kernel(const bsidmap_decoder* d, const Plan& P, bool priors))(const
   return l1;
 }
 
-void launch_pass1(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s) {
+void launch_pass1(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s, int ib = 0, int ie = -1) {
+  if (ie < 0) ie = d->N;  // symbol indices [ib, ie)
   const long lanes = (long)p.F * d->Mt;
   const unsigned gx_flat = (unsigned)((lanes + kLatticeThreads - 1) / kLatticeThreads);
   auto l1 = pass1_kernel(d, P, p.priors != nullptr);
@@ -475,11 +523,11 @@ void launch_pass1(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_
   const bool multi = P.mode != kSchedStored && d->kern.l1_steps;
   const unsigned gx1 = d->kern.l1_W == 2 ? (unsigned)((lanes + 2 * kLatticeThreads - 1) / (2 * kLatticeThreads)) : gx_flat;
   int steps = multi ? kL1Steps : 1;
-  while (steps > 1 && (long)gx1 * ((d->N + steps - 1) / steps) < 8L * d->num_sms) steps >>= 1;
+  while (steps > 1 && (long)gx1 * ((ie - ib + steps - 1) / steps) < 8L * d->num_sms) steps >>= 1;
   p.i_steps = steps;
-  for_i_slices(d->N, [&](int i0, int ni) {
-    p.i_base = i0;
-    p.i_end = i0 + ni;
+  for_i_slices(ie - ib, [&](int i0, int ni) {
+    p.i_base = ib + i0;
+    p.i_end = ib + i0 + ni;
     launch_k(l1, dim3(gx1, (unsigned)((ni + steps - 1) / steps)), kLatticeThreads, P.l1_smem, s, p);
     d->launches++;
   });
@@ -487,23 +535,26 @@ void launch_pass1(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_
 
 void launch_alpha_beta(bsidmap_decoder* d, const Plan& P, const DecodeParams& p, cudaStream_t s) {
   if (P.ab_warp) {
-    const long tasks = 2L * p.F, per = kAbWarpThreads / 32;
+    const long tasks = (p.ab_dir < 0 ? 2L : 1L) * p.F, per = kAbWarpThreads / 32;
     launch_k(P.ab_warp, (unsigned)((tasks + per - 1) / per), kAbWarpThreads, P.ab_smem, s, p);
   } else {
-    launch_k(P.ab_cta, dim3(p.F, 2), P.ab_threads, P.ab_smem, s, p, P.ab_stages);
+    launch_k(P.ab_cta, dim3(p.F, p.ab_dir < 0 ? 2 : 1), P.ab_threads, P.ab_smem, s, p, P.ab_stages);
   }
   d->launches++;
 }
 
-void launch_pass2(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s) {
+void launch_pass2(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s, int ib = 0, int ie = -1) {
+  if (ie < 0) ie = d->N;  // symbol indices [ib, ie)
   if (P.app_live) {  // live windows of every (frame, i) row, then the packed APP over them
-    const long rows = (long)p.F * d->N;
+    const long rows = (long)p.F * (ie - ib);
+    p.i_base = ib;
+    p.i_end = ie;
     k_live<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(p);
     d->launches++;
     p.app_G = P.app_G;
     const unsigned gx = (unsigned)(((p.F + P.app_G - 1) / P.app_G + kX2Warps - 1) / kX2Warps);
-    for_i_slices(d->N, [&](int i0, int ni) {
-      p.i_base = i0;
+    for_i_slices(ie - ib, [&](int i0, int ni) {
+      p.i_base = ib + i0;
       launch_k(P.app_kernel, dim3(gx, ni), kLatticeThreads, P.app_smem, s, p);
       d->launches++;
     });
@@ -512,11 +563,77 @@ void launch_pass2(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_
   const long lanes = (long)p.F * d->Mt;
   const unsigned gx_flat = (unsigned)((lanes + kLatticeThreads - 1) / kLatticeThreads);
   auto l2 = P.app_kernel;
-  for_i_slices(d->N, [&](int i0, int ni) {
-    p.i_base = i0;
+  for_i_slices(ie - ib, [&](int i0, int ni) {
+    p.i_base = ib + i0;
     launch_k(l2, dim3(gx_flat, ni), kLatticeThreads, P.app_smem, s, p);
     d->launches++;
   });
+}
+
+// The slab schedule (kSchedSlab).  Gamma lives in two slab buffers (ring halves); slab b of B
+// symbol indices uses half b & 1.  Forward sweep: pass 1 of slab b on the decode stream, alpha
+// through it on the side stream (overlapping pass 1 of slab b + 1).  Backward sweep: pass 1 of slab
+// b again, only for windows with alpha_i(m') != 0 (askip), beta through it on the side stream, and
+// on the decode stream the live-window APP of slab b + 1 (its beta rows are complete by then).
+int run_chunk_slab(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s, bool first_chunk,
+                   bool last_chunk) {
+  int rc = ensure_ab_stream(d);
+  if (rc) return rc;
+  const int N = d->N, B = P.slab, nsl = (N + B - 1) / B;
+  const size_t half = (size_t)p.F * B * d->Mn * p.Mtp;
+  p.beta_rows = slab_beta_rows(d, B);  // the bound workspace holds this many rows per frame
+  float* const ring = p.Gsum;
+  auto slab_params = [&](int b, bool askip) {
+    DecodeParams q = p;
+    q.Gsum = ring + (b & 1) * half;
+    q.gs_N = B;
+    q.gs_i0 = b * B;
+    q.askip = askip ? 1 : 0;
+    return q;
+  };
+  if (first_chunk) record(d, 1, s);
+  for (int b = 0; b < nsl; b++) {  // forward sweep: Gamma slab -> alpha
+    const int i0 = b * B, i1 = std::min(N, i0 + B);
+    DecodeParams q = slab_params(b, false);
+    if (b >= 2) cudaStreamWaitEvent(s, d->ev_ab[b & 1], 0);  // alpha of slab b - 2 read this half
+    launch_pass1(d, P, q, s, i0, i1);
+    cudaEventRecord(d->ev_p1[b & 1], s);
+    cudaStreamWaitEvent(d->s_ab, d->ev_p1[b & 1], 0);
+    q.ab_r0 = i0;
+    q.ab_r1 = i1;
+    q.ab_dir = 0;
+    launch_alpha_beta(d, P, q, d->s_ab);
+    cudaEventRecord(d->ev_ab[b & 1], d->s_ab);
+  }
+  cudaStreamWaitEvent(s, d->ev_ab[(nsl - 1) & 1], 0);  // every alpha row (the backward sweep reads them)
+  if (first_chunk) record(d, 2, s);
+  if (first_chunk) record(d, 3, s);
+  for (int b = nsl - 1; b >= 0; b--) {  // backward sweep: Gamma slab (alpha != 0) -> beta -> APP
+    const int i0 = b * B, i1 = std::min(N, i0 + B);
+    DecodeParams q = slab_params(b, d->slab_askip);
+    if (b + 2 < nsl) cudaStreamWaitEvent(s, d->ev_ab[b & 1], 0);  // beta of slab b + 2 read this half
+    launch_pass1(d, P, q, s, i0, i1);
+    cudaEventRecord(d->ev_p1[b & 1], s);
+    cudaStreamWaitEvent(d->s_ab, d->ev_p1[b & 1], 0);
+    q.ab_r0 = N - i1;
+    q.ab_r1 = N - i0;
+    q.ab_dir = 1;
+    launch_alpha_beta(d, P, q, d->s_ab);
+    cudaEventRecord(d->ev_ab[b & 1], d->s_ab);
+    if (b + 1 < nsl) {  // the APP of slab b + 1: its beta rows are done
+      cudaStreamWaitEvent(s, d->ev_ab[(b + 1) & 1], 0);
+      launch_pass2(d, P, p, s, i1, std::min(N, i1 + B));
+    }
+  }
+  cudaStreamWaitEvent(s, d->ev_ab[0], 0);
+  launch_pass2(d, P, p, s, 0, std::min(N, B));
+  if (first_chunk) record(d, 4, s);
+  k_zero_failed<<<p.F, 256, 0, s>>>(p);
+  d->launches++;
+  if (last_chunk) record(d, 5, s);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(d, e, "kernel launch");
+  return BSIDMAP_OK;
 }
 
 int run_chunk(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s, bool first_chunk, bool last_chunk) {
@@ -553,6 +670,7 @@ int run_chunk(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s,
     if (e != cudaSuccess) return cuda_fail(d, e, "kernel launch");
     return BSIDMAP_OK;
   }
+  if (P.mode == kSchedSlab) return run_chunk_slab(d, P, p, s, first_chunk, last_chunk);
   if (!P.direct_L) cudaMemsetAsync(p.Lacc, 0, (size_t)p.F * d->N * d->q * sizeof(double), s);
   const int S = std::min(P.ab_sub, p.F);
   if (S > 1) {
@@ -742,6 +860,11 @@ int bsidmap_create(bsidmap_decoder** out, int q, int n, int N, const uint32_t* c
       if (!d->jit) d->jit_err = "alphabet too large for the live-window APP's shared memory";
     }
   }
+  // RECOMPUTE runs the slab schedule on the spec cores (BSIDMAP_SLAB=0: the per-frame local kernels)
+  d->slab_ok = d->spec;
+  if (const char* v = std::getenv("BSIDMAP_SLAB")) d->slab_ok = d->slab_ok && std::atoi(v) != 0;
+  if (const char* v = std::getenv("BSIDMAP_SLAB_LEN")) d->slab_fixed = std::max(0, std::atoi(v));
+  if (const char* v = std::getenv("BSIDMAP_SLAB_ASKIP")) d->slab_askip = std::atoi(v) != 0;
   if (!d->spec && !find_generic_kernels(Mn, &d->kern)) {
     delete d;
     return fail(nullptr, BSIDMAP_EPLAN, "no lattice core for M_n = " + std::to_string(Mn));
@@ -989,13 +1112,13 @@ int bsidmap_plan_info(bsidmap_decoder* d, int F, char* buf, size_t len) {
       "\"workspace_bytes\": %zu, \"windows_per_lane\": %d, \"q\": %d, \"n\": %d, \"N\": %d, \"Mn\": %d, \"Mtau\": %d, "
       "\"alpha_beta_overlap_subbatches\": %d, \"app_prefix_bits\": %d, \"app_windows_per_lane\": %d, "
       "\"app_folded_rows\": %d, \"app_live\": %d, \"app_frames_per_warp\": %d, \"live_eps\": %.6g, "
-      "\"jit_error\": \"%s\"}",
+      "\"slab\": %d, \"jit_error\": \"%s\"}",
       sched_name(P.mode), F, P.chunk, P.nchunks, d->jit ? "jit" : d->spec ? "spec" : "generic",
       d->kern.W == 2 ? ((long)P.chunk * tiles_per_frame(d->Mt) + kX2Warps - 1) / kX2Warps
                      : (lanes + kLatticeThreads - 1) / kLatticeThreads,
       d->N, kLatticeThreads, P.chunk, P.ab_warp ? kAbWarpThreads : P.ab_threads,
       layout(d, P.chunk, P.mode).total, d->kern.W, d->q, d->n, d->N, d->Mn, d->Mt, std::min(P.ab_sub, P.chunk), P.app_kp, P.app_live ? d->kern.app_live_W : 1, P.app_ks,
-      P.app_live ? 1 : 0, P.app_G, d->live_eps, json_text(d->jit_err, 300).c_str());
+      P.app_live ? 1 : 0, P.app_G, d->live_eps, P.slab, json_text(d->jit_err, 300).c_str());
   return nb;
 }
 
@@ -1059,6 +1182,8 @@ int bsidmap_debug_states(bsidmap_decoder* d, int F, double* alpha_out, double* b
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (d->last_sched == kSchedLocal || d->last_sched == kSchedLocalCta)
     return fail(d, BSIDMAP_EINVAL, "the local schedule keeps no beta rows");
+  if (d->last_sched == kSchedSlab && slab_beta_rows(d, slab_len(d, d->last_chunk)) != d->N + 1)
+    return fail(d, BSIDMAP_EINVAL, "the slab schedule keeps beta rows for three slabs only");
   const Layout l = layout(d, d->last_chunk, d->last_sched);
   DecodeParams p;
   bind_ws(d, l, &p);

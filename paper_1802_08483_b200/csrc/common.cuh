@@ -79,8 +79,28 @@ struct DecodeParams {
   int i_base;                 // first symbol index of this launch (blockIdx.y offset)
   int i_end;                  // one past the last symbol index of this launch (multi-step kernels)
   int i_steps;                // symbol indices per CTA of the multi-step kernels
+  // Gamma slab (the blocked memory-reduced schedule keeps Gamma_i only for a slab of symbol
+  // indices [gs_i0, gs_i0 + gs_N)): Gamma_i of frame f is block f gs_N + (i - gs_i0) of Gsum.
+  // The Gamma-sum schedule keeps every block: gs_N = N, gs_i0 = 0.
+  int gs_N, gs_i0;
+  int askip;                  // pass 1: only windows with alpha_i(m') != 0 (recomputed Gamma, slab bwd sweep)
+  // alpha/beta launches over part of the recursion: steps [ab_r0, ab_r1) (step s is symbol index s
+  // forward, N - 1 - s backward), directions ab_dir (-1: both, 0: alpha only, 1: beta only); a
+  // range that does not start at step 0 resumes from the stored, normalised row
+  int ab_r0, ab_r1, ab_dir;
+  int beta_rows;              // beta rows kept per frame: N + 1, or a ring of 3 slabs (row i at i % beta_rows)
   LatticeConst lc;
 };
+
+// beta_i of frame f (the whole recursion, or the slab schedule's ring of three slabs of rows).
+__device__ __forceinline__ double* beta_row(const DecodeParams& p, int f, int i) {
+  return p.beta + ((size_t)f * p.beta_rows + (size_t)(i % p.beta_rows)) * p.Mt;
+}
+
+// Gamma_i block of frame f (M_n x Mtp floats) in the Gamma-sum array or the current slab.
+__device__ __forceinline__ float* gsum_block(const DecodeParams& p, int f, int i) {
+  return p.Gsum + ((size_t)f * p.gs_N + (i - p.gs_i0)) * p.Mn * p.Mtp;
+}
 
 // Row stride of Gsum: M_tau rounded up to whole 32-byte sectors (8 floats): every Gamma row starts a
 // sector (and is a 16-byte multiple, as the TMA bulk copies of the alpha/beta kernels need).  Zeroing

@@ -35,42 +35,48 @@ __global__ void __launch_bounds__(1024) k_alpha_beta_cta(const DecodeParams p, i
   double* part = Rb + 2 * RW;
   uint64_t* bars = reinterpret_cast<uint64_t*>(part + 64);
   const int f = blockIdx.x;
-  const bool fwd = blockIdx.y == 0;
+  const bool fwd = p.ab_dir < 0 ? blockIdx.y == 0 : p.ab_dir == 0;
+  const int r0 = p.ab_r0, r1 = p.ab_r1;  // steps of this launch (the whole recursion: 0, N)
   if (p.status[f] != kFrameOk) return;  // uniform over the CTA
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31, nw = (nt + 31) >> 5;
-  double* rows = (fwd ? p.alpha : p.beta) + (size_t)f * (N + 1) * Mt;
-  const float* Gf = p.Gsum + (size_t)f * N * Mn * Mtp;
+  double* const arows = p.alpha + (size_t)f * (N + 1) * Mt;
+  auto row_at = [&](int r) { return fwd ? arows + (size_t)r * Mt : beta_row(p, f, r); };
   const uint32_t blk = (uint32_t)(Mn * Mtp * 4);
-  auto gblock = [&](int step) { return Gf + (size_t)(fwd ? step : N - 1 - step) * Mn * Mtp; };
+  auto gblock = [&](int step) { return gsum_block(p, f, fwd ? step : N - 1 - step); };
   // kRing = false: a Gamma_i block larger than shared memory (wide trellises, e.g. C4's channel at
   // N = 1e5: M_n x M_tau x 4 > 227 KB) -- the CTA reads it straight from global memory (L2)
   if (kRing && tid == 0) {
     for (int s = 0; s < stages; s++) mbar_init(bars + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < stages && s < N; s++) {
+    for (int s = 0; s < stages && r0 + s < r1; s++) {
       mbar_expect_tx(bars + s, blk);
-      tma_bulk_g2s(ring + (size_t)s * Mn * Mtp, gblock(s), blk, bars + s);
+      tma_bulk_g2s(ring + (size_t)s * Mn * Mtp, gblock(r0 + s), blk, bars + s);
     }
   }
   for (int t = tid; t < 2 * RW; t += nt) Rb[t] = 0.0;
   __syncthreads();
-  const int i0 = fwd ? 0 : N;
+  const int i0 = fwd ? r0 : N - r0;
   for (int m = tid; m < Mt; m += nt) {
-    const double v = boundary_row(p, f, m, fwd);  // alpha_0 / beta_N
-    Rb[Mn + m] = v;
-    rows[(size_t)i0 * Mt + m] = v;
+    if (r0 == 0) {
+      const double v = boundary_row(p, f, m, fwd);  // alpha_0 / beta_N
+      Rb[Mn + m] = v;
+      row_at(i0)[m] = v;
+    } else {
+      Rb[Mn + m] = row_at(i0)[m];  // resume from the stored, normalised row
+    }
   }
   __syncthreads();
   // alpha gather of state m reads Gamma column j = m - lo - e, e < M_n: all inside [0, M_tau)
   // for m in [m_lo_in, m_hi_in]
   const int m_lo_in = lo + Mn - 1, m_hi_in = Mt - 1 + lo;
   double inv_c = 1.0;  // scale of the current row (any constant: every row is normalised by its sum)
-  for (int step = 0; step < N; step++) {
-    const int stage = kRing ? step % stages : 0;
-    if constexpr (kRing) mbar_wait(bars + stage, (uint32_t)(step / stages) & 1u);
+  for (int step = r0; step < r1; step++) {
+    const int ts = step - r0;
+    const int stage = kRing ? ts % stages : 0;
+    if constexpr (kRing) mbar_wait(bars + stage, (uint32_t)(ts / stages) & 1u);
     const float* G = kRing ? ring + (size_t)stage * Mn * Mtp : gblock(step);
-    const double* cur = Rb + (step & 1) * RW + Mn;
-    double* nxt = Rb + ((step + 1) & 1) * RW + Mn;
+    const double* cur = Rb + (ts & 1) * RW + Mn;
+    double* nxt = Rb + ((ts + 1) & 1) * RW + Mn;
     double ps = 0.0;
     for (int m = tid; m < Mt; m += nt) {
       double a0 = 0.0, a1 = 0.0;
@@ -105,10 +111,10 @@ __global__ void __launch_bounds__(1024) k_alpha_beta_cta(const DecodeParams p, i
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
-    double* pp = part + ((step + 1) & 1) * 32;
+    double* pp = part + ((ts + 1) & 1) * 32;
     if (lane == 0) pp[warp] = ps;
     __syncthreads();  // nxt and the partials are complete; the ring stage is consumed
-    if (kRing && tid == 0 && step + stages < N) {
+    if (kRing && tid == 0 && step + stages < r1) {
       mbar_expect_tx(bars + stage, blk);
       tma_bulk_g2s(ring + (size_t)stage * Mn * Mtp, gblock(step + stages), blk, bars + stage);
     }
@@ -118,14 +124,15 @@ __global__ void __launch_bounds__(1024) k_alpha_beta_cta(const DecodeParams p, i
     if (!(c > 0.0)) {  // all-zero row: Y impossible under the limits (reading R14)
       if (tid == 0) {
         p.status[f] = kFrameUnderflow;
-        for (int t = step + 1; kRing && t < N && t <= step + stages; t++)  // drain issued copies
-          mbar_wait(bars + t % stages, (uint32_t)(t / stages) & 1u);
+        for (int u = ts + 1; kRing && r0 + u < r1 && u <= ts + stages; u++)  // drain issued copies
+          mbar_wait(bars + u % stages, (uint32_t)(u / stages) & 1u);
       }
       return;
     }
     inv_c = 1.0 / c;
     const int r = fwd ? step + 1 : N - 1 - step;
-    for (int m = tid; m < Mt; m += nt) rows[(size_t)r * Mt + m] = nxt[m] * inv_c;  // eqn:alpha_norm
+    double* const out = row_at(r);
+    for (int m = tid; m < Mt; m += nt) out[m] = nxt[m] * inv_c;  // eqn:alpha_norm
   }
 }
 

@@ -45,35 +45,42 @@ __global__ void __launch_bounds__(kAbWarpThreads) k_alpha_beta_warp(const Decode
   float* ring = reinterpret_cast<float*>(base + SPT * 32 * 8);
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + SPT * 32 * 8 + (size_t)kAbStages * MN * Mtp * 4);
   const long task = (long)blockIdx.x * (kAbWarpThreads / 32) + warp;
-  if (task >= 2L * p.F) return;  // warp-uniform
-  const int f = (int)(task >> 1);
-  const bool fwd = (task & 1) == 0;
+  const bool both = p.ab_dir < 0;  // (frame, direction) tasks, or one direction per frame
+  if (task >= (both ? 2L : 1L) * p.F) return;  // warp-uniform
+  const int f = (int)(both ? task >> 1 : task);
+  const bool fwd = both ? (task & 1) == 0 : p.ab_dir == 0;
+  const int r0 = p.ab_r0, r1 = p.ab_r1;  // steps of this launch (the whole recursion: 0, N)
   if (p.status[f] != kFrameOk) return;
-  double* rows_g = (fwd ? p.alpha : p.beta) + (size_t)f * (N + 1) * Mt;
-  const float* Gf = p.Gsum + (size_t)f * N * MN * Mtp;
+  double* const arows = p.alpha + (size_t)f * (N + 1) * Mt;
+  auto row_at = [&](int r) { return fwd ? arows + (size_t)r * Mt : beta_row(p, f, r); };
   const uint32_t blk_bytes = (uint32_t)(MN * Mtp * 4);
-  auto gblock = [&](int step) { return Gf + (size_t)(fwd ? step : N - 1 - step) * MN * Mtp; };
+  auto gblock = [&](int step) { return gsum_block(p, f, fwd ? step : N - 1 - step); };
 
   if (lane == 0) {
     for (int s = 0; s < kAbStages; s++) mbar_init(bars + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < kAbStages && s < N; s++) {
+    for (int s = 0; s < kAbStages && r0 + s < r1; s++) {
       mbar_expect_tx(bars + s, blk_bytes);
-      tma_bulk_g2s(ring + (size_t)s * MN * Mtp, gblock(s), blk_bytes, bars + s);
+      tma_bulk_g2s(ring + (size_t)s * MN * Mtp, gblock(r0 + s), blk_bytes, bars + s);
     }
   }
-  const int i0 = fwd ? 0 : N;
+  const int i0 = fwd ? r0 : N - r0;
 #pragma unroll
   for (int s = 0; s < SPT; s++) {
     const int m = lane + 32 * s;
-    const double v = boundary_row(p, f, m, fwd);  // alpha_0 / beta_N
-    row[m] = v;
-    if (m < Mt) rows_g[(size_t)i0 * Mt + m] = v;
+    if (r0 == 0) {
+      const double v = boundary_row(p, f, m, fwd);  // alpha_0 / beta_N
+      row[m] = v;
+      if (m < Mt) row_at(i0)[m] = v;
+    } else {
+      row[m] = m < Mt ? row_at(i0)[m] : 0.0;  // resume from the stored, normalised row
+    }
   }
   __syncwarp();
-  for (int step = 0; step < N; step++) {
-    const int stage = step % kAbStages;
-    mbar_wait(bars + stage, (uint32_t)(step / kAbStages) & 1u);
+  for (int step = r0; step < r1; step++) {
+    const int t = step - r0;
+    const int stage = t % kAbStages;
+    mbar_wait(bars + stage, (uint32_t)(t / kAbStages) & 1u);
     const float* G = ring + (size_t)stage * MN * Mtp;  // Gamma_i [k][m'] in smem
     double acc[SPT];
     double part = 0.0;
@@ -96,25 +103,26 @@ __global__ void __launch_bounds__(kAbWarpThreads) k_alpha_beta_warp(const Decode
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
     __syncwarp();  // every lane is done with this stage and with the old row
-    if (lane == 0 && step + kAbStages < N) {
+    if (lane == 0 && step + kAbStages < r1) {
       mbar_expect_tx(bars + stage, blk_bytes);
       tma_bulk_g2s(ring + (size_t)stage * MN * Mtp, gblock(step + kAbStages), blk_bytes, bars + stage);
     }
     if (!(part > 0.0)) {  // all-zero row: Y impossible under the limits (reading R14)
       if (lane == 0) p.status[f] = kFrameUnderflow;
       // drain the copies already issued for later steps before the warp's smem can be reused
-      for (int t = step + 1; t < N && t <= step + kAbStages; t++)
-        mbar_wait(bars + t % kAbStages, (uint32_t)(t / kAbStages) & 1u);
+      for (int u = t + 1; r0 + u < r1 && u <= t + kAbStages; u++)
+        mbar_wait(bars + u % kAbStages, (uint32_t)(u / kAbStages) & 1u);
       return;
     }
     const double inv = 1.0 / part;
     const int r = fwd ? step + 1 : N - 1 - step;
+    double* const out = row_at(r);
 #pragma unroll
     for (int s = 0; s < SPT; s++) {
       const int m = lane + 32 * s;
       const double v = acc[s] * inv;
       row[m] = v;
-      if (m < Mt) rows_g[(size_t)r * Mt + m] = v;
+      if (m < Mt) out[m] = v;
     }
     __syncwarp();
   }

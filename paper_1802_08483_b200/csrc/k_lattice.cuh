@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_su
   }
   if (G.in) {
     const float sc = p.priors ? 1.f : 1.f / p.q;
-    float* out = p.Gsum + ((size_t)G.f * p.N + i) * MN * p.Mtp + G.mi;
+    float* out = gsum_block(p, G.f, i) + G.mi;
 #pragma unroll
     for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, G, e) ? sc * acc[e] : 0.f;
   }
@@ -182,7 +182,7 @@ template <int MN>
 __device__ __forceinline__ double app_weights(const DecodeParams& p, const LaneGeom& G, int i, float (&bt)[MN]) {
   double bm = 0.0;
   double bv[MN];
-  const double* brow = p.beta + ((size_t)G.f * (p.N + 1) + (i + 1)) * p.Mt;
+  const double* brow = beta_row(p, G.f, i + 1);
 #pragma unroll
   for (int e = 0; e < MN; e++) {
     bv[e] = out_valid(p, G, e) ? brow[G.mi + p.mn_lo + e] : 0.0;

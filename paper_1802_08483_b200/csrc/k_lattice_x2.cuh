@@ -140,12 +140,12 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_
   }
   const float sc = p.priors ? 1.f : 1.f / p.q;
   if (A.in) {
-    float* out = p.Gsum + ((size_t)A.f * p.N + i) * MN * p.Mtp + A.mi;
+    float* out = gsum_block(p, A.f, i) + A.mi;
 #pragma unroll
     for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, A, e) ? sc * lo_of(acc[e]) : 0.f;
   }
   if (B.in) {
-    float* out = p.Gsum + ((size_t)B.f * p.N + i) * MN * p.Mtp + B.mi;
+    float* out = gsum_block(p, B.f, i) + B.mi;
 #pragma unroll
     for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, B, e) ? sc * hi_of(acc[e]) : 0.f;
   }
@@ -177,6 +177,13 @@ __device__ __forceinline__ LaneGeom geom_step(const DecodeParams& p, const WinBa
   G.vmask = valid_mask(p, G);
   return G;
 }
+// Recomputed Gamma (slab schedule, backward sweep, p.askip): a window with alpha_i(m') = 0 contributes
+// nothing weighted by a non-zero alpha (reading R19); a warp none of whose windows has alpha != 0
+// skips the step and leaves its Gamma rows 0 (windows with alpha = 0 in a warp that runs are computed
+// as usual: either value is exact for L).
+__device__ __forceinline__ bool alpha_live(const DecodeParams& p, const WinBase& b, const LaneGeom& G, int i) {
+  return G.active && (!p.askip || p.alpha[((size_t)b.f * (p.N + 1) + i) * p.Mt + b.mi] != 0.0);
+}
 
 // Head tables of pass 1: lattice rows 1..KH depend only on the codeword's first KH bits, so at each
 // symbol index the lane computes them once for the 2^KH prefixes (both windows) and keeps row KH of
@@ -204,8 +211,11 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1C_MINB) k_gamma_sum
   extern __shared__ __align__(128) unsigned char smem[];
   f32x2* s_res = reinterpret_cast<f32x2*>(smem);  // [MN][128] per-lane result (private column, no barrier)
   f32x2* s_head = s_res + MN * kLatticeThreads + threadIdx.x;  // [2^KH][MN - E0][128]: this lane's column
-  const long ga = (long)blockIdx.x * (2 * blockDim.x) + threadIdx.x;
-  const WinBase ba = win_base(p, ga), bb = win_base(p, ga + blockDim.x);
+  // windows g and g + 128 per lane; with the alpha-support skip adjacent windows 2t, 2t + 1, so that
+  // a warp spans 64 consecutive windows and whole warps fall outside the support more often
+  const long g0 = (long)blockIdx.x * (2 * blockDim.x);
+  const long ga = p.askip ? g0 + 2 * threadIdx.x : g0 + threadIdx.x;
+  const WinBase ba = win_base(p, ga), bb = win_base(p, p.askip ? ga + 1 : ga + blockDim.x);
   const int i0 = p.i_base + blockIdx.y * p.i_steps, i1 = min(i0 + p.i_steps, p.i_end);
   Win3 na = win_words(ba, p.n * i0 + ba.mp), nb = win_words(bb, p.n * i0 + bb.mp);
 #pragma unroll 1
@@ -221,7 +231,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1C_MINB) k_gamma_sum
     f32x2 acc[MN];
 #pragma unroll
     for (int e = 0; e < MN; e++) acc[e] = 0ull;
-    if (__any_sync(0xffffffffu, A.active || B.active)) {
+    if (__any_sync(0xffffffffu, alpha_live(p, ba, A, i) || alpha_live(p, bb, B, i))) {
       typename Core::Lane lane;
       Core::init(lane, A.active ? win_bits(wa, A.s) : 0ull, B.active ? win_bits(wb, B.s) : 0ull, p);
       if constexpr (KH > 0) {  // rows 1..KH of every prefix, once per symbol index
@@ -284,12 +294,12 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1C_MINB) k_gamma_sum
     }
     const float sc = p.priors ? 1.f : 1.f / p.q;
     if (A.in) {
-      float* out = p.Gsum + ((size_t)A.f * p.N + i) * MN * p.Mtp + A.mi;
+      float* out = gsum_block(p, A.f, i) + A.mi;
 #pragma unroll
       for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, A, e) ? sc * lo_of(acc[e]) : 0.f;
     }
     if (B.in) {
-      float* out = p.Gsum + ((size_t)B.f * p.N + i) * MN * p.Mtp + B.mi;
+      float* out = gsum_block(p, B.f, i) + B.mi;
 #pragma unroll
       for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, B, e) ? sc * hi_of(acc[e]) : 0.f;
     }
@@ -317,7 +327,7 @@ __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_su
     float acc[MN];
 #pragma unroll
     for (int e = 0; e < MN; e++) acc[e] = 0.f;
-    if (__any_sync(0xffffffffu, G.active)) {
+    if (__any_sync(0xffffffffu, alpha_live(p, wb, G, i))) {
       typename Core::Lane lane;
       Core::init(lane, G.active ? win_bits(ww, G.s) : 0ull, p);
       const float* pri = p.priors ? p.priors + ((size_t)G.f * p.N + i) * p.q : nullptr;
@@ -355,7 +365,7 @@ __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_su
     }
     if (G.in) {
       const float sc = p.priors ? 1.f : 1.f / p.q;
-      float* out = p.Gsum + ((size_t)G.f * p.N + i) * MN * p.Mtp + G.mi;
+      float* out = gsum_block(p, G.f, i) + G.mi;
 #pragma unroll
       for (int e = 0; e < MN; e++) out[(size_t)e * p.Mtp] = out_valid(p, G, e) ? sc * acc[e] : 0.f;
     }
@@ -368,7 +378,7 @@ template <int MN>
 __device__ __forceinline__ double app_weights_p2(const DecodeParams& p, const LaneGeom& G, int i, float (&bt)[MN]) {
   double bv[MN];
   double bm = 0.0;
-  const double* brow = p.beta + ((size_t)G.f * (p.N + 1) + (i + 1)) * p.Mt;
+  const double* brow = beta_row(p, G.f, i + 1);
   const int m0 = G.mi + p.mn_lo;
 #pragma unroll
   for (int e = 0; e < MN; e++) {
@@ -391,7 +401,7 @@ template <int MN>
 __device__ __forceinline__ void app_weights_pair(const DecodeParams& p, const LaneGeom& A, const LaneGeom& B, int i,
                                                  float (&ba)[MN], float (&bb)[MN], double& da, double& db) {
   double bv[MN + 1];
-  const double* brow = p.beta + ((size_t)A.f * (p.N + 1) + (i + 1)) * p.Mt;
+  const double* brow = beta_row(p, A.f, i + 1);
   const int m0 = A.mi + p.mn_lo;
 #pragma unroll
   for (int u = 0; u < MN + 1; u++) bv[u] = __ldg(brow + min(max(m0 + u, 0), p.Mt - 1));

@@ -79,12 +79,13 @@ __global__ void k_extrinsic(const DecodeParams p, float* E) {
 __global__ void k_live(const DecodeParams p) {
   const long row = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (row >= (long)p.F * p.N) return;
-  const int f = (int)(row / p.N), i = (int)(row - (long)f * p.N);
+  const int ni = p.i_end - p.i_base;  // symbol indices [i_base, i_end) of this launch
+  if (row >= (long)p.F * ni) return;
+  const int f = (int)(row / ni), i = p.i_base + (int)(row - (long)f * ni);
   int2 out = make_int2(0, 0);
   if (p.status[f] == kFrameOk) {
     const double* a = p.alpha + ((size_t)f * (p.N + 1) + i) * p.Mt;
-    const double* b = p.beta + ((size_t)f * (p.N + 1) + i) * p.Mt;
+    const double* b = beta_row(p, f, i);
     double s = 0.0;
     for (int m = lane; m < p.Mt; m += 32) s += a[m] * b[m];
 #pragma unroll
@@ -101,7 +102,7 @@ __global__ void k_live(const DecodeParams p) {
     hi = __reduce_max_sync(0xffffffffu, hi);
     if (s > 0.0 && hi >= lo) out = make_int2(lo, (hi - lo + 2) & ~1);
   }
-  if (lane == 0) p.live[row] = out;
+  if (lane == 0) p.live[(size_t)f * p.N + i] = out;
 }
 
 // One warp per (frame, i) row.

@@ -98,27 +98,57 @@ def test_c2_parity(mode):
     assert_parity(L, st, run_oracle(cfg, b))
 
 
-def test_c3_parity():
+# RECOMPUTE's two schedules: the slab schedule (spec cores; slabs of 8 symbol indices here, so the
+# frames span many slabs and a ragged last one) and the paper's per-frame local kernels
+SCHEDS = {"slab": ({"BSIDMAP_SLAB_LEN": "8"}, "recompute-slab"),
+          "local": ({"BSIDMAP_SLAB": "0"}, "recompute-local")}
+
+
+def run_recompute(cfg, b, sched, monkeypatch):
+    env, mode_name = SCHEDS[sched]
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    d, L, st = run_gpu(cfg, b, 2)
+    assert d.plan(len(b.rho))["mode"].startswith(mode_name)
+    if sched == "slab":
+        assert d.plan(len(b.rho))["slab"] == min(8, cfg.N)
+    for k in env:
+        monkeypatch.delenv(k)
+    return d, L, st
+
+
+@pytest.mark.parametrize("sched", ["slab", "local"])
+def test_c3_parity(sched, monkeypatch):
     cfg = small_cfg("C3")
     b = bsidgen.make_batch(cfg, 7, 4)
-    _, L, st = run_gpu(cfg, b, 2)
+    _, L, st = run_recompute(cfg, b, sched, monkeypatch)
     assert_parity(L, st, run_oracle(cfg, b))
 
 
-def test_c4_parity():
+@pytest.mark.parametrize("sched", ["slab", "local"])
+def test_c4_parity(sched, monkeypatch):
     cfg = small_cfg("C4")
     b = bsidgen.make_batch(cfg, 3, 2)
-    _, L, st = run_gpu(cfg, b, 2)
+    _, L, st = run_recompute(cfg, b, sched, monkeypatch)
     assert_parity(L, st, run_oracle(cfg, b))
 
 
-def test_c5_shape_parity_reduced_N():
+@pytest.mark.parametrize("sched", ["slab", "local"])
+def test_c5_shape_parity_reduced_N(sched, monkeypatch):
     """C5's q, n, channel, corridor, M_tau and non-uniform priors, N cut to 60 so the
     oracle finishes in seconds (full-N C5 is checked by sampled gamma + properties)."""
     full = bsidgen.configs()["C5"]
     cfg = small_cfg("C5", N=60, mn=full.mn, mt=full.mt)
     b = bsidgen.make_batch(cfg, 0, 2)
-    _, L, st = run_gpu(cfg, b, 2)
+    _, L, st = run_recompute(cfg, b, sched, monkeypatch)
+    assert_parity(L, st, run_oracle(cfg, b))
+
+
+@pytest.mark.parametrize("sched", ["slab", "local"])
+def test_c2_recompute_parity(sched, monkeypatch):
+    cfg = small_cfg("C2")
+    b = bsidgen.make_batch(cfg, 1000, 48)   # N = 100: twelve slabs of 8 and a ragged one of 4
+    _, L, st = run_recompute(cfg, b, sched, monkeypatch)
     assert_parity(L, st, run_oracle(cfg, b))
 
 
@@ -286,7 +316,7 @@ def test_app_two_folded_rows(name, frames, monkeypatch):
     assert_parity(L2, st2, run_oracle(cfg, b))
 
 
-def test_modes_agree_and_plan():
+def test_modes_agree_and_plan(monkeypatch):
     cfg = small_cfg("C2")
     b = bsidgen.make_batch(cfg, 0, 16)
     _, Ls, sts = run_gpu(cfg, b, 1)
@@ -296,17 +326,26 @@ def test_modes_agree_and_plan():
     np.testing.assert_array_equal(sts, stg)
     np.testing.assert_allclose(Ls, Lr, rtol=2e-5, atol=1e-30)
     np.testing.assert_allclose(Lg, Lr, rtol=2e-5, atol=1e-30)
-    assert d.plan(65536)["mode"] == "recompute-local" and d.plan(64)["core"] == "spec"
+    # RECOMPUTE on a spec core: the slab schedule (Gamma for two slabs of symbol indices, alpha and
+    # beta rows); memory estimate at the bench batch: stored gamma > Gamma-sum > slab
+    assert d.plan(65536)["mode"] == "recompute-slab" and d.plan(64)["core"] == "spec"
     assert _dec().from_config(cfg, b.C, mode=0, device=0).plan(64)["mode"] == "recompute-gammasum"
-    # memory estimate: stored gamma > Gamma-sum > local (alpha rows only)
-    assert d.workspace_bytes(16, 1) > d.workspace_bytes(16, 3) > d.workspace_bytes(16, 2)
-    assert d.workspace_bytes(16, 2) == 16 * (cfg.N + 1) * cfg.Mt * 8 or d.workspace_bytes(16, 2) < 16 * (cfg.N + 1) * cfg.Mt * 8 + 512
-    # M_tau > 64: RECOMPUTE runs the local schedule with one CTA per frame (alpha rows only);
-    # AUTO the Gamma-sum schedule
+    assert d.workspace_bytes(65536, 1) > d.workspace_bytes(65536, 3) > 3 * d.workspace_bytes(65536, 2)
+    # BSIDMAP_SLAB=0: the paper's per-frame local kernels (alpha rows only), one warp per frame for
+    # M_tau <= 64 and one CTA per frame above; AUTO the Gamma-sum schedule
+    monkeypatch.setenv("BSIDMAP_SLAB", "0")
+    dl, Ll, stl = run_gpu(cfg, b, 2)
+    assert dl.plan(65536)["mode"] == "recompute-local"
+    np.testing.assert_array_equal(stl, stg)
+    np.testing.assert_allclose(Ll, Lr, rtol=2e-5, atol=1e-30)
+    assert d.workspace_bytes(16, 1) > d.workspace_bytes(16, 3) > dl.workspace_bytes(16, 2)
+    assert dl.workspace_bytes(16, 2) < 16 * (cfg.N + 1) * cfg.Mt * 8 + 512
     c3 = small_cfg("C3")
     d3 = _dec().from_config(c3, bsidgen.codebook(c3), mode=2, device=0)
     assert d3.plan(8)["mode"] == "recompute-local-cta"
     assert d3.workspace_bytes(8, 2) < 8 * (c3.N + 1) * c3.Mt * 8 + 512
+    monkeypatch.delenv("BSIDMAP_SLAB")
+    assert _dec().from_config(c3, bsidgen.codebook(c3), mode=2, device=0).plan(8)["mode"] == "recompute-slab"
     assert _dec().from_config(c3, bsidgen.codebook(c3), mode=0, device=0).plan(8)["mode"] == "recompute-gammasum"
 
 
@@ -326,7 +365,7 @@ def test_alpha_beta_states_vs_oracle():
             assert np.all(np.abs(g[~big] - o[~big]) <= 1e-4 * 1e-12 + 1e-16)
 
 
-def test_full_c5_frame_properties():
+def test_full_c5_frame_properties(monkeypatch):
     """Full-size C5 frames (N = 10^4, tau = 120000): the oracle cannot decode them in
     seconds, so check properties that hold at any size: status OK, rows sum to 1,
     APP calibration (among symbols decided with max_D L > 1 - eps the error rate is
@@ -354,13 +393,19 @@ def test_full_c5_frame_properties():
     _, L2, st2 = run_gpu(cfg, b2, 0)
     assert (st2 == 0).all()
     np.testing.assert_allclose(L2, L, rtol=1e-5, atol=1e-30)
-    # the paper's local schedule (one CTA per frame, gamma recomputed in the alpha pass and in the
-    # combined beta + L pass) on the same full-size frames agrees with the Gamma-sum one
+    # the memory-reduced schedules on the same full-size frames agree with the Gamma-sum one: the
+    # slab schedule (RECOMPUTE's default on the spec cores) and the paper's per-frame local schedule
+    # (one CTA per frame, gamma recomputed in the alpha pass and in the combined beta + L pass,
+    # P:483-627)
     d3, L3, st3 = run_gpu(cfg, b, 2)
-    assert d3.plan(2)["mode"] == "recompute-local-cta"
-    np.testing.assert_array_equal(st3, st)
+    assert d3.plan(2)["mode"] == "recompute-slab"
+    monkeypatch.setenv("BSIDMAP_SLAB", "0")
+    d4, L4, st4 = run_gpu(cfg, b, 2)
+    assert d4.plan(2)["mode"] == "recompute-local-cta"
     big = L > 1e-20
-    np.testing.assert_allclose(L3[big], L[big], rtol=2e-4)
+    for Lx, sx in ((L3, st3), (L4, st4)):
+        np.testing.assert_array_equal(sx, st)
+        np.testing.assert_allclose(Lx[big], L[big], rtol=2e-4)
 
 
 # ----------------------------------------------- bench launch configuration, full sizes
@@ -391,14 +436,15 @@ def test_bench_batch_sampled_parity(name, frames, picks):
 
 
 @pytest.mark.slow
-def test_full_c5_frame_vs_oracle():
+def test_full_c5_frame_vs_oracle(monkeypatch):
     """BASELINE's C5 at full length (q=64, n=12, N=10^4, tau=120000, Pi=Pd=0.02, non-uniform
     priors), decoded end to end on the GPU and compared element by element with the FP64 oracle
     (eqn:L) at the north-star gate: max relative error 1e-4 on every L_i(D), hard
     decisions equal where the oracle's top-two gap exceeds 1e-3.  The GPU decodes the C5 per-GPU
     batch of the 8-GPU config (32 frames) three ways: AUTO with the default geometry (Gamma-sum,
     alpha/beta overlapped on two sub-batches), AUTO chunked in two by a workspace limit (the checked
-    frame sits in the second chunk), and RECOMPUTE (the paper's local schedule).  The
+    frame sits in the second chunk), RECOMPUTE (the slab schedule) and RECOMPUTE with
+    BSIDMAP_SLAB=0 (the paper's per-frame local schedule).  The
     oracle decodes the checked frame with its m' loops on every host core (bit-identical to the
     serial oracle, test_threaded_oracle_bit_identical) while the GPU runs."""
     import threading
@@ -426,8 +472,12 @@ def test_full_c5_frame_vs_oracle():
     assert d2.plan(frames)["chunks"] == 2
     runs["auto-chunked"] = (L2, st2)
     d3, L3, st3 = run_gpu(cfg, b, 2)
-    assert d3.plan(frames)["mode"] == "recompute-local-cta"
-    runs["recompute"] = (L3, st3)
+    assert d3.plan(frames)["mode"] == "recompute-slab"
+    runs["recompute-slab"] = (L3, st3)
+    monkeypatch.setenv("BSIDMAP_SLAB", "0")
+    d4, L4, st4 = run_gpu(cfg, b, 2)
+    assert d4.plan(frames)["mode"] == "recompute-local-cta"
+    runs["recompute-local"] = (L4, st4)
     th.join()
     r = box["r"]
     assert r["status"] == oracle.OK
