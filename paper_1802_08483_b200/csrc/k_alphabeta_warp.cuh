@@ -29,21 +29,30 @@ constexpr int kAbWarpThreads = BSIDMAP_AB_WARP_THREADS;
 #endif
 constexpr int kAbStages = BSIDMAP_AB_STAGES;
 
-// shared memory per warp: row[SPT*32] doubles | ring[kStages][MN][Mtp] floats | bars[kStages]
+// shared memory per warp: row[MN + SPT*32 + MN] doubles (the state row with M_n zero entries on
+// both sides and zeros at m >= M_tau) | ring[kStages][MN][Mtp] floats | bars[kStages]
+__host__ __device__ __forceinline__ size_t ab_warp_row_bytes(int SPT, int MN) {
+  return ((size_t)(SPT * 32 + 2 * MN) * 8 + 15) & ~(size_t)15;  // the TMA ring stays 16-byte aligned
+}
 __host__ __device__ __forceinline__ size_t ab_warp_smem(int SPT, int MN, int Mtp) {
   // rounded to 16 bytes: the next warp's TMA ring must stay 16-byte aligned
-  return ((size_t)SPT * 32 * 8 + (size_t)kAbStages * MN * Mtp * 4 + kAbStages * 8 + 15) & ~(size_t)15;
+  return (ab_warp_row_bytes(SPT, MN) + (size_t)kAbStages * MN * Mtp * 4 + kAbStages * 8 + 15) & ~(size_t)15;
 }
 
+// The state row lives in shared memory with M_n zero entries on both sides and zeros for m >= M_tau,
+// so the gathers need no bounds tests: beta reads row[m + k] (k = m_n^- + e) and Gamma column m, always
+// inside [0, M_tau) for m < M_tau; alpha reads row[j] and Gamma column j = m - k, which is clamped into
+// [0, M_tau) (its row factor is then 0).  Lanes with m >= M_tau compute a discarded value.
 template <int SPT, int MN>
 __global__ void __launch_bounds__(kAbWarpThreads) k_alpha_beta_warp(const DecodeParams p) {
   extern __shared__ __align__(128) unsigned char s_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Mt = p.Mt, Mtp = p.Mtp, N = p.N, lo = p.mn_lo;
   unsigned char* base = s_raw + (size_t)warp * ab_warp_smem(SPT, MN, Mtp);
-  double* row = reinterpret_cast<double*>(base);
-  float* ring = reinterpret_cast<float*>(base + SPT * 32 * 8);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + SPT * 32 * 8 + (size_t)kAbStages * MN * Mtp * 4);
+  double* const rowx = reinterpret_cast<double*>(base);  // [MN + SPT*32 + MN]
+  double* const row = rowx + MN;                         // row[m], m in [-MN, SPT*32 + MN)
+  float* ring = reinterpret_cast<float*>(base + ab_warp_row_bytes(SPT, MN));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + ab_warp_row_bytes(SPT, MN) + (size_t)kAbStages * MN * Mtp * 4);
   const long task = (long)blockIdx.x * (kAbWarpThreads / 32) + warp;
   const bool both = p.ab_dir < 0;  // (frame, direction) tasks, or one direction per frame
   if (task >= (both ? 2L : 1L) * p.F) return;  // warp-uniform
@@ -64,16 +73,20 @@ __global__ void __launch_bounds__(kAbWarpThreads) k_alpha_beta_warp(const Decode
       tma_bulk_g2s(ring + (size_t)s * MN * Mtp, gblock(r0 + s), blk_bytes, bars + s);
     }
   }
+  for (int t = lane; t < SPT * 32 + 2 * MN; t += 32) rowx[t] = 0.0;
+  __syncwarp();
   const int i0 = fwd ? r0 : N - r0;
 #pragma unroll
   for (int s = 0; s < SPT; s++) {
     const int m = lane + 32 * s;
-    if (r0 == 0) {
-      const double v = boundary_row(p, f, m, fwd);  // alpha_0 / beta_N
-      row[m] = v;
-      if (m < Mt) row_at(i0)[m] = v;
-    } else {
-      row[m] = m < Mt ? row_at(i0)[m] : 0.0;  // resume from the stored, normalised row
+    if (m < Mt) {
+      if (r0 == 0) {
+        const double v = boundary_row(p, f, m, fwd);  // alpha_0 / beta_N
+        row[m] = v;
+        row_at(i0)[m] = v;
+      } else {
+        row[m] = row_at(i0)[m];  // resume from the stored, normalised row
+      }
     }
   }
   __syncwarp();
@@ -88,16 +101,24 @@ __global__ void __launch_bounds__(kAbWarpThreads) k_alpha_beta_warp(const Decode
     for (int s = 0; s < SPT; s++) {
       const int m = lane + 32 * s;
       double a0 = 0.0, a1 = 0.0;
+      if (fwd) {  // alpha'(m) = sum_e alpha(j) Gamma(j, k), j = m - k, k = m_n^- + e
+        const int j0 = m - lo;
 #pragma unroll
-      for (int e = 0; e < MN; e++) {
-        const int idx = fwd ? m - lo - e : m;         // Gamma_i column read by this term
-        const int j = fwd ? m - lo - e : m + lo + e;  // neighbouring state of the previous row
-        const bool ok = m < Mt && idx >= 0 && idx < Mt && j >= 0 && j < Mt;
-        const double r = ok ? row[min(max(j, 0), Mt - 1)] : 0.0;
-        const double gv = ok ? (double)G[e * Mtp + min(max(idx, 0), Mt - 1)] : 0.0;
-        if (e & 1) a1 = fma(r, gv, a1); else a0 = fma(r, gv, a0);
+        for (int e = 0; e < MN; e++) {
+          const int j = j0 - e;
+          const double g = (double)G[e * Mtp + min(max(j, 0), Mt - 1)];
+          if (e & 1) a1 = fma(row[j], g, a1); else a0 = fma(row[j], g, a0);
+        }
+      } else {    // beta'(m) = sum_e Gamma(m, k) beta(m + k)
+        const double* c0 = row + m + lo;
+        const float* g0 = G + min(m, Mt - 1);
+#pragma unroll
+        for (int e = 0; e < MN; e++) {
+          const double g = (double)g0[e * Mtp];
+          if (e & 1) a1 = fma(g, c0[e], a1); else a0 = fma(g, c0[e], a0);
+        }
       }
-      acc[s] = a0 + a1;
+      acc[s] = m < Mt ? a0 + a1 : 0.0;
       part += acc[s];
     }
 #pragma unroll
@@ -121,7 +142,7 @@ __global__ void __launch_bounds__(kAbWarpThreads) k_alpha_beta_warp(const Decode
     for (int s = 0; s < SPT; s++) {
       const int m = lane + 32 * s;
       const double v = acc[s] * inv;
-      row[m] = v;
+      row[m] = v;  // 0 for m >= M_tau
       if (m < Mt) out[m] = v;
     }
     __syncwarp();

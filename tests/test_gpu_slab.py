@@ -45,16 +45,22 @@ def test_slab_lengths_parity(name, frames, lengths, monkeypatch):
 
 def test_slab_chunked_bit_identical(monkeypatch):
     """Chunking the batch does not change the arithmetic at a fixed slab length (and a fixed number
-    of frames per APP warp, whose FP64 association otherwise follows the launch size)."""
+    of frames per APP warp, whose FP64 association otherwise follows the launch size) when every
+    window is recomputed; with the alpha-support skip the skipped warps follow the packing of frames
+    into warps, which changes beta only where alpha = 0 (R19): L equal up to rounding."""
     monkeypatch.setenv("BSIDMAP_APP_G", "1")
     cfg = small_cfg("C4")
     b = bsidgen.make_batch(cfg, 4, 6)
-    d, L1, st1 = _slab(monkeypatch, cfg, b, 16)
-    per = d.workspace_bytes(1, 2)
-    d2, L2, st2 = _slab(monkeypatch, cfg, b, 16, ws_limit=per * 2 + per // 2)
-    assert d2.plan(6)["chunks"] == 3
-    np.testing.assert_array_equal(st1, st2)
-    np.testing.assert_array_equal(L1, L2)
+    for askip in (False, True):
+        d, L1, st1 = _slab(monkeypatch, cfg, b, 16, askip)
+        per = d.workspace_bytes(1, 2)
+        d2, L2, st2 = _slab(monkeypatch, cfg, b, 16, askip, ws_limit=per * 2 + per // 2)
+        assert d2.plan(6)["chunks"] == 3
+        np.testing.assert_array_equal(st1, st2)
+        if askip:
+            np.testing.assert_allclose(L1, L2, rtol=2e-5, atol=1e-30)
+        else:
+            np.testing.assert_array_equal(L1, L2)
     assert_parity(L1, st1, run_oracle(cfg, b, [0, 5]), [0, 5])
 
 
