@@ -350,10 +350,14 @@ def main():
     ph = np.array(phases)  # [steps][6]: init, pass 1, exposed alpha/beta, pass 2, finalize, alpha/beta busy
     mean_ph = ph.mean(0)
     dominant = 1 if mean_ph[1] >= mean_ph[3] else 3
+    slab = plan["mode"] == "recompute-slab"
+    if slab:  # phases: [1] forward sweep (every pass-1 slab, alpha overlapped), [3] backward sweep
+        dominant = 1
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     peak_tf, peak_basis = fp32_peak(sms)
     achieved = flops_pass / (mean_ph[dominant] / 1e3) / 1e12
-    prof = ncu_profile(cfg, "lattice_pass1" if dominant == 1 else "lattice_pass2", count, plan)
+    prof = ({"ncu": "not captured for the slab schedule (the ncu entries are the Gamma-sum kernels)"} if slab else
+            ncu_profile(cfg, "lattice_pass1" if dominant == 1 else "lattice_pass2", count, plan))
     if "executed_flops_per_launch" in prof:  # executed work over the same live launch time
         prof["executed_achieved"] = prof["executed_flops_per_launch"] / (mean_ph[dominant] / 1e3) / 1e12
         prof["frac_executed"] = prof["executed_achieved"] / peak_tf
@@ -422,7 +426,8 @@ def main():
             "symbols_per_s": value * cfg.N,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf, "traffic": prof.get("traffic"),
-                         "kernel": "lattice pass 1 (k_gamma_sum)" if dominant == 1 else "lattice pass 2 (k_app)",
+                         "kernel": ("slab forward sweep (pass 1 of every slab, alpha overlapped)" if slab else
+                                    "lattice pass 1 (k_gamma_sum)" if dominant == 1 else "lattice pass 2 (k_app)"),
                          "peak_basis": peak_basis,
                          "flops_per_launch": flops_pass, "launch_ms": float(mean_ph[dominant]),
                          "frames_per_launch": int(min(plan["chunk"], count)),
@@ -436,7 +441,10 @@ def main():
             "phase_ms": {"init": float(mean_ph[0]), "lattice_pass1": float(mean_ph[1]),
                          "alpha_beta": float(mean_ph[2]), "lattice_pass2": float(mean_ph[3]),
                          "finalize": float(mean_ph[4]),
-                         "alpha_beta_busy": float(mean_ph[5]) if len(mean_ph) > 5 else float(mean_ph[2])},
+                         "alpha_beta_busy": float(mean_ph[5]) if len(mean_ph) > 5 else float(mean_ph[2]),
+                         **({"note": "slab schedule: lattice_pass1 = forward sweep (pass 1 + alpha per slab), "
+                                     "lattice_pass2 = backward sweep (pass 1 where alpha != 0, beta, live APP)"}
+                            if slab else {})},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
