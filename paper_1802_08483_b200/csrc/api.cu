@@ -26,6 +26,9 @@ __global__ void k_finalize(const DecodeParams p);
 __global__ void k_zero_failed(const DecodeParams p);
 __global__ void k_extrinsic(const DecodeParams p, float* E);
 __global__ void k_live(const DecodeParams p);
+__global__ void k_alpha_support(const DecodeParams p);
+__global__ void k_support_pack1(const DecodeParams p);
+__global__ void k_support_pack2(const DecodeParams p, int nblk);
 struct McParams {
   uint64_t seed;
   long first;
@@ -134,7 +137,7 @@ int cuda_fail(bsidmap_decoder* d, cudaError_t e, const char* what) {
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t gsum, gamma, alpha, beta, lacc, live, total;
+  size_t gsum, gamma, alpha, beta, lacc, live, spack, sblk, total;
 };
 
 
@@ -150,14 +153,17 @@ struct Layout {
 // for two slabs in flight.
 enum Sched { kSchedStored = 1, kSchedLocal = 2, kSchedGammaSum = 3, kSchedLocalCta = 4, kSchedSlab = 5 };
 
-// Windows per Gamma slab: pass 1 of one slab is ~8 waves of 3 CTAs (256 windows x 8 symbol indices
-// each) on every SM; the slab length is a multiple of the pass-1 CTA's 8 symbol indices.  Measured
-// (C5, 32 frames; tools/exp_slab.py): slabs of 64 / 128 / 256 symbol indices 375 / 362 / 348 ms.
-constexpr long kSlabWindows = 8L * 3 * 256 * 8 * 148;
+// Windows per Gamma slab: pass 1 of one slab is ~16 waves of 3 CTAs (256 windows x 8 symbol indices
+// each) on every SM; the slab length is a multiple of the pass-1 CTA's 8 symbol indices, and the
+// two-slab ring at most a quarter of the Gamma-sum schedule's Gamma (slabs of <= N/8).  Measured (C5,
+// 32 frames; tools/exp_slab.py): slabs of 64 / 128 / 256 / 512 symbol indices 375 / 362 / 311 / 299 ms
+// (the last two with the packed backward sweep); C2 (65536 frames): 8 / 100 indices 125.8 / 126.5 ms.
+constexpr long kSlabWindows = 16L * 3 * 256 * 8 * 148;
 int slab_len(const bsidmap_decoder* d, long F) {
   if (d->slab_fixed > 0) return std::min(d->slab_fixed, d->N);  // BSIDMAP_SLAB_LEN (tests: many slabs at small N)
   const long per_i = std::max(1L, F * d->Mt);
   long B = (kSlabWindows + per_i - 1) / per_i;
+  B = std::min(B, std::max(8L, (long)d->N / 8));
   B = (B + 7) / 8 * 8;
   return (int)std::max(1L, std::min<long>(B, d->N));
 }
@@ -215,7 +221,10 @@ Layout layout(const bsidmap_decoder* d, long F, int sched) {
   const bool live = uses_live_app(d, sched);
   l.lacc = (local || live) ? 0 : align_up((size_t)F * d->N * d->q * sizeof(double));
   l.live = live ? align_up((size_t)F * d->N * sizeof(int2)) : 0;
-  l.total = l.gsum + l.gamma + l.alpha + l.beta + l.lacc + l.live;
+  // slab backward sweep: packed alpha-support windows, (F + 1) entries per symbol-index group
+  l.spack = sched == kSchedSlab ? align_up(((size_t)F + 1) * slab_len(d, F) * sizeof(int2)) : 0;
+  l.sblk = sched == kSchedSlab ? align_up((size_t)((F + 255) / 256) * slab_len(d, F) * sizeof(int)) : 0;
+  l.total = l.gsum + l.gamma + l.alpha + l.beta + l.lacc + l.live + l.spack + l.sblk;
   return l;
 }
 
@@ -454,6 +463,10 @@ void bind_ws(const bsidmap_decoder* d, const Layout& l, DecodeParams* p) {
   p->Lacc = l.lacc ? reinterpret_cast<double*>(b) : nullptr;
   b += l.lacc;
   p->live = l.live ? reinterpret_cast<int2*>(b) : nullptr;
+  b += l.live;
+  p->spack = l.spack ? reinterpret_cast<int2*>(b) : nullptr;
+  b += l.spack;
+  p->spack_blk = l.sblk ? reinterpret_cast<int*>(b) : nullptr;
 }
 
 void record(bsidmap_decoder* d, int k, cudaStream_t s) {
@@ -513,17 +526,27 @@ void (*pass1_kernel(const bsidmap_decoder* d, const Plan& P, bool priors))(const
   return l1;
 }
 
-void launch_pass1(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s, int ib = 0, int ie = -1) {
-  if (ie < 0) ie = d->N;  // symbol indices [ib, ie)
-  const long lanes = (long)p.F * d->Mt;
-  const unsigned gx_flat = (unsigned)((lanes + kLatticeThreads - 1) / kLatticeThreads);
-  auto l1 = pass1_kernel(d, P, p.priors != nullptr);
-  // the class kernels walk up to kL1Steps symbol indices per CTA -- fewer where the grid would
-  // not fill the GPU (small batches: single-frame latency)
+// Pass-1 grid: x over the windows of F frames, y over groups of `steps` symbol indices of [ib, ie).
+// The class kernels walk up to kL1Steps symbol indices per CTA -- fewer where the grid would not fill
+// the GPU (small batches: single-frame latency).
+unsigned pass1_gx(const bsidmap_decoder* d, long F) {
+  const long lanes = F * d->Mt;
+  return d->kern.l1_W == 2 ? (unsigned)((lanes + 2 * kLatticeThreads - 1) / (2 * kLatticeThreads))
+                           : (unsigned)((lanes + kLatticeThreads - 1) / kLatticeThreads);
+}
+int pass1_steps(const bsidmap_decoder* d, const Plan& P, long F, int ib, int ie) {
   const bool multi = P.mode != kSchedStored && d->kern.l1_steps;
-  const unsigned gx1 = d->kern.l1_W == 2 ? (unsigned)((lanes + 2 * kLatticeThreads - 1) / (2 * kLatticeThreads)) : gx_flat;
+  const unsigned gx1 = pass1_gx(d, F);
   int steps = multi ? kL1Steps : 1;
   while (steps > 1 && (long)gx1 * ((ie - ib + steps - 1) / steps) < 8L * d->num_sms) steps >>= 1;
+  return steps;
+}
+
+void launch_pass1(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_t s, int ib = 0, int ie = -1) {
+  if (ie < 0) ie = d->N;  // symbol indices [ib, ie)
+  auto l1 = pass1_kernel(d, P, p.priors != nullptr);
+  const unsigned gx1 = pass1_gx(d, p.F);
+  const int steps = pass1_steps(d, P, p.F, ib, ie);
   p.i_steps = steps;
   for_i_slices(ie - ib, [&](int i0, int ni) {
     p.i_base = ib + i0;
@@ -612,6 +635,22 @@ int run_chunk_slab(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream
     const int i0 = b * B, i1 = std::min(N, i0 + B);
     DecodeParams q = slab_params(b, d->slab_askip);
     if (b + 2 < nsl) cudaStreamWaitEvent(s, d->ev_ab[b & 1], 0);  // beta of slab b + 2 read this half
+    if (q.askip) {  // alpha support of the slab's rows (p.live; k_live reuses the rows after beta)
+      if (d->kern.l1_W != 2) {
+        q.askip = 0;  // the pair core's pass 1 packs the windows with alpha != 0; others recompute all
+      } else {
+        DecodeParams r = q;
+        r.i_base = i0;
+        r.i_end = i1;
+        r.i_steps = pass1_steps(d, P, p.F, i0, i1);  // the pass-1 CTA rows' symbol-index groups
+        const unsigned groups = (unsigned)((i1 - i0 + r.i_steps - 1) / r.i_steps);
+        const int nblk = (p.F + 255) / 256;
+        k_alpha_support<<<(unsigned)(((long)p.F * (i1 - i0) + 7) / 8), 256, 0, s>>>(r);
+        k_support_pack1<<<dim3(groups, nblk), 256, 0, s>>>(r);
+        k_support_pack2<<<groups, 256, 0, s>>>(r, nblk);
+        d->launches += 3;
+      }
+    }
     launch_pass1(d, P, q, s, i0, i1);
     cudaEventRecord(d->ev_p1[b & 1], s);
     cudaStreamWaitEvent(d->s_ab, d->ev_p1[b & 1], 0);

@@ -89,12 +89,27 @@ struct DecodeParams {
   // range that does not start at step 0 resumes from the stored, normalised row
   int ab_r0, ab_r1, ab_dir;
   int beta_rows;              // beta rows kept per frame: N + 1, or a ring of 3 slabs (row i at i % beta_rows)
+  int2* spack;                // slab backward sweep: packed alpha-support windows per symbol-index group
+  int* spack_blk;             //   its per-block scan totals (k_support_pack1/2)
   LatticeConst lc;
 };
 
 // beta_i of frame f (the whole recursion, or the slab schedule's ring of three slabs of rows).
 __device__ __forceinline__ double* beta_row(const DecodeParams& p, int f, int i) {
-  return p.beta + ((size_t)f * p.beta_rows + (size_t)(i % p.beta_rows)) * p.Mt;
+  const int r = i < p.beta_rows ? i : i % p.beta_rows;  // no division for the whole recursion (k_live: 0.5 ms)
+  return p.beta + ((size_t)f * p.beta_rows + (size_t)r) * p.Mt;
+}
+// (frame, i) of row `row` of a launch over symbol indices [i_base, i_base + ni) (32-bit division
+// where the row count allows: the per-row kernels are short)
+__device__ __forceinline__ void row_fi(long row, int ni, int i_base, int* f, int* i) {
+  if (row < 0x7fffffffL) {
+    const unsigned r = (unsigned)row, q = r / (unsigned)ni;
+    *f = (int)q;
+    *i = i_base + (int)(r - q * (unsigned)ni);
+  } else {
+    *f = (int)(row / ni);
+    *i = i_base + (int)(row - (long)*f * ni);
+  }
 }
 
 // Gamma_i block of frame f (M_n x Mtp floats) in the Gamma-sum array or the current slab.
@@ -146,6 +161,44 @@ __device__ __forceinline__ WinBase win_base(const DecodeParams& p, long g) {
   b.rho = b.in ? p.rho[b.f] : 0;
   b.ok = b.in && p.status[b.f] == kFrameOk;
   b.w = p.rx + (b.in ? p.rx_off[b.f] : 0);
+  b.nwords = (b.rho + 31) >> 5;
+  return b;
+}
+
+// The slab schedule's backward sweep (p.askip): the windows with alpha != 0 are packed across frames.
+// For symbol-index group g (the i_steps indices of one pass-1 CTA row), p.spack[g][f] = (offset of
+// frame f's windows in the packed list, first window lo_f) and p.spack[g][F].x = total T; frame f
+// contributes the windows [lo_f, hi_f] holding every alpha_i(m') != 0 of the group (k_support_pack*).
+// Slots [0, T) are these windows (the largest f whose offset is <= slot); slots [T, F M_tau) are the
+// other windows in frame order (frame f's start at f M_tau - offset_f), which only write their Gamma
+// rows as 0.
+__device__ __forceinline__ WinBase win_base_packed(const DecodeParams& p, long slot, int g) {
+  const int2* pk = p.spack + (size_t)g * (p.F + 1);
+  const long T = pk[p.F].x, Mt = p.Mt;
+  WinBase b;
+  b.in = slot < (long)p.F * Mt;
+  const bool live = slot < T;
+  const long d = live ? slot : slot - T;  // index in the live or the dead list
+  int f = 0;
+  if (b.in) {
+    int lo = 0, hi = p.F - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      const long start = live ? (long)pk[mid].x : (long)mid * Mt - pk[mid].x;
+      if (start <= d) lo = mid; else hi = mid - 1;
+    }
+    f = lo;
+  }
+  const int2 e = pk[f];
+  const long start = live ? (long)e.x : (long)f * Mt - e.x;
+  const int idx = (int)(d - start);
+  const int w = (f + 1 < p.F ? pk[f + 1].x : (int)T) - e.x;  // frame f's live windows
+  b.f = f;
+  b.mi = !b.in ? 0 : live ? e.y + idx : (idx < e.y ? idx : idx + w);
+  b.mp = p.mt_lo + b.mi;
+  b.rho = b.in ? p.rho[f] : 0;
+  b.ok = b.in && live && p.status[f] == kFrameOk;  // dead windows: Gamma rows written as 0
+  b.w = p.rx + (b.in ? p.rx_off[f] : 0);
   b.nwords = (b.rho + 31) >> 5;
   return b;
 }

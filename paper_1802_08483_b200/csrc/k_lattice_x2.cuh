@@ -181,8 +181,8 @@ __device__ __forceinline__ LaneGeom geom_step(const DecodeParams& p, const WinBa
 // nothing weighted by a non-zero alpha (reading R19); a warp none of whose windows has alpha != 0
 // skips the step and leaves its Gamma rows 0 (windows with alpha = 0 in a warp that runs are computed
 // as usual: either value is exact for L).
-__device__ __forceinline__ bool alpha_live(const DecodeParams& p, const WinBase& b, const LaneGeom& G, int i) {
-  return G.active && (!p.askip || p.alpha[((size_t)b.f * (p.N + 1) + i) * p.Mt + b.mi] != 0.0);
+__device__ __forceinline__ bool alpha_live(const DecodeParams& p, bool askip, const WinBase& b, const LaneGeom& G, int i) {
+  return G.active && (!askip || p.alpha[((size_t)b.f * (p.N + 1) + i) * p.Mt + b.mi] != 0.0);
 }
 
 // Head tables of pass 1: lattice rows 1..KH depend only on the codeword's first KH bits, so at each
@@ -211,12 +211,17 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1C_MINB) k_gamma_sum
   extern __shared__ __align__(128) unsigned char smem[];
   f32x2* s_res = reinterpret_cast<f32x2*>(smem);  // [MN][128] per-lane result (private column, no barrier)
   f32x2* s_head = s_res + MN * kLatticeThreads + threadIdx.x;  // [2^KH][MN - E0][128]: this lane's column
-  // windows g and g + 128 per lane; with the alpha-support skip adjacent windows 2t, 2t + 1, so that
-  // a warp spans 64 consecutive windows and whole warps fall outside the support more often
-  const long g0 = (long)blockIdx.x * (2 * blockDim.x);
-  const long ga = p.askip ? g0 + 2 * threadIdx.x : g0 + threadIdx.x;
-  const WinBase ba = win_base(p, ga), bb = win_base(p, p.askip ? ga + 1 : ga + blockDim.x);
+  // windows g and g + 128 per lane; with the alpha-support skip (slab backward sweep) the packed
+  // windows with alpha != 0 of this CTA's symbol indices first, adjacent slots 2t, 2t + 1
+  // (win_base_packed): the CTAs past them only write zero rows.  Packing only where it skips more
+  // than 1/8 of the windows (C2-C4 have alpha > 0 on 96-98 % of them: the plain geometry, no test).
   const int i0 = p.i_base + blockIdx.y * p.i_steps, i1 = min(i0 + p.i_steps, p.i_end);
+  const long g0 = (long)blockIdx.x * (2 * blockDim.x);
+  const bool askip = p.askip && 8L * p.spack[(size_t)blockIdx.y * (p.F + 1) + p.F].x < 7L * p.F * p.Mt;
+  const long ga = askip ? g0 + 2 * threadIdx.x : g0 + threadIdx.x;
+  const long gb = askip ? ga + 1 : ga + blockDim.x;
+  const WinBase ba = askip ? win_base_packed(p, ga, blockIdx.y) : win_base(p, ga);
+  const WinBase bb = askip ? win_base_packed(p, gb, blockIdx.y) : win_base(p, gb);
   Win3 na = win_words(ba, p.n * i0 + ba.mp), nb = win_words(bb, p.n * i0 + bb.mp);
 #pragma unroll 1
   for (int i = i0; i < i1; i++) {
@@ -231,7 +236,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1C_MINB) k_gamma_sum
     f32x2 acc[MN];
 #pragma unroll
     for (int e = 0; e < MN; e++) acc[e] = 0ull;
-    if (__any_sync(0xffffffffu, alpha_live(p, ba, A, i) || alpha_live(p, bb, B, i))) {
+    if (__any_sync(0xffffffffu, alpha_live(p, askip, ba, A, i) || alpha_live(p, askip, bb, B, i))) {
       typename Core::Lane lane;
       Core::init(lane, A.active ? win_bits(wa, A.s) : 0ull, B.active ? win_bits(wb, B.s) : 0ull, p);
       if constexpr (KH > 0) {  // rows 1..KH of every prefix, once per symbol index
@@ -327,7 +332,7 @@ __global__ void __launch_bounds__(kLatticeThreads, kLatticeMinBlocks) k_gamma_su
     float acc[MN];
 #pragma unroll
     for (int e = 0; e < MN; e++) acc[e] = 0.f;
-    if (__any_sync(0xffffffffu, alpha_live(p, wb, G, i))) {
+    if (__any_sync(0xffffffffu, alpha_live(p, false, wb, G, i))) {
       typename Core::Lane lane;
       Core::init(lane, G.active ? win_bits(ww, G.s) : 0ull, p);
       const float* pri = p.priors ? p.priors + ((size_t)G.f * p.N + i) * p.q : nullptr;

@@ -81,7 +81,8 @@ __global__ void k_live(const DecodeParams p) {
   const int lane = threadIdx.x & 31;
   const int ni = p.i_end - p.i_base;  // symbol indices [i_base, i_end) of this launch
   if (row >= (long)p.F * ni) return;
-  const int f = (int)(row / ni), i = p.i_base + (int)(row - (long)f * ni);
+  int f, i;
+  row_fi(row, ni, p.i_base, &f, &i);
   int2 out = make_int2(0, 0);
   if (p.status[f] == kFrameOk) {
     const double* a = p.alpha + ((size_t)f * (p.N + 1) + i) * p.Mt;
@@ -103,6 +104,88 @@ __global__ void k_live(const DecodeParams p) {
     if (s > 0.0 && hi >= lo) out = make_int2(lo, (hi - lo + 2) & ~1);
   }
   if (lane == 0) p.live[(size_t)f * p.N + i] = out;
+}
+
+// The slab schedule's backward sweep: per (frame, i) row of symbol indices [i_base, i_end), the state
+// range [first, first + count) holding every alpha_i(m') != 0 (count 0: none), into p.live (which the
+// live-window APP's k_live overwrites for the same rows afterwards).  One warp per row.
+__global__ void k_alpha_support(const DecodeParams p) {
+  const long row = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int ni = p.i_end - p.i_base;
+  if (row >= (long)p.F * ni) return;
+  int f, i;
+  row_fi(row, ni, p.i_base, &f, &i);
+  int lo = 0x7fffffff, hi = -1;
+  if (p.status[f] == kFrameOk) {
+    const double* a = p.alpha + ((size_t)f * (p.N + 1) + i) * p.Mt;
+    for (int m = lane; m < p.Mt; m += 32) {
+      if (a[m] != 0.0) {
+        lo = min(lo, m);
+        hi = max(hi, m);
+      }
+    }
+  }
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  if (lane == 0) p.live[(size_t)f * p.N + i] = hi >= lo ? make_int2(lo, hi - lo + 1) : make_int2(0, 0);
+}
+
+// Packing of the slab backward sweep's pass 1 (win_base_packed), per symbol-index group g (p.i_steps
+// indices from p.i_base): per frame the union [lo, hi] of the group's alpha-support rows
+// (k_alpha_support), its width, and the exclusive scan of the widths over frames, in two passes --
+// pack1: grid (groups, ceil(F / 256)), a block scan of 256 frames, block totals to spack_blk;
+// pack2: one block per group, scans the block totals, adds them, writes the total at [F].
+__device__ __forceinline__ int block_scan_incl(int v, int* s_w) {  // blockDim.x = 256
+  s_w[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+    const int t = threadIdx.x >= (unsigned)o ? s_w[threadIdx.x - o] : 0;
+    __syncthreads();
+    s_w[threadIdx.x] += t;
+    __syncthreads();
+  }
+  return s_w[threadIdx.x];
+}
+__global__ void __launch_bounds__(256) k_support_pack1(const DecodeParams p) {
+  __shared__ int s_w[256];
+  const int g = blockIdx.x, f = blockIdx.y * 256 + threadIdx.x;
+  const int i0 = p.i_base + g * p.i_steps, i1 = min(i0 + p.i_steps, p.i_end);
+  int lo = 0x7fffffff, hi = -1;
+  if (f < p.F) {
+    for (int i = i0; i < i1; i++) {
+      const int2 r = p.live[(size_t)f * p.N + i];
+      if (r.y > 0) {
+        lo = min(lo, r.x);
+        hi = max(hi, r.x + r.y - 1);
+      }
+    }
+  }
+  const int w = hi >= lo ? hi - lo + 1 : 0;
+  const int incl = block_scan_incl(w, s_w);
+  if (f < p.F) p.spack[(size_t)g * (p.F + 1) + f] = make_int2(incl - w, w > 0 ? lo : 0);
+  if (threadIdx.x == blockDim.x - 1) p.spack_blk[(size_t)g * gridDim.y + blockIdx.y] = incl;
+}
+__global__ void __launch_bounds__(256) k_support_pack2(const DecodeParams p, int nblk) {
+  __shared__ int s_w[256];
+  __shared__ int s_carry;
+  const int g = blockIdx.x;
+  int2* pk = p.spack + (size_t)g * (p.F + 1);
+  int* bt = p.spack_blk + (size_t)g * nblk;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < nblk; b0 += blockDim.x) {  // exclusive scan of the block totals
+    const int b = b0 + threadIdx.x;
+    const int v = b < nblk ? bt[b] : 0;
+    const int incl = block_scan_incl(v, s_w);
+    const int carry = s_carry;
+    __syncthreads();
+    if (b < nblk) bt[b] = carry + incl - v;
+    if (threadIdx.x == blockDim.x - 1) s_carry = carry + incl;
+    __syncthreads();
+  }
+  for (int f = threadIdx.x; f < p.F; f += blockDim.x) pk[f].x += bt[f >> 8];
+  if (threadIdx.x == 0) pk[p.F] = make_int2(s_carry, 0);
 }
 
 // One warp per (frame, i) row.
