@@ -25,7 +25,9 @@ __global__ void k_frame_init(const DecodeParams p);
 __global__ void k_finalize(const DecodeParams p);
 __global__ void k_zero_failed(const DecodeParams p);
 __global__ void k_extrinsic(const DecodeParams p, float* E);
-__global__ void k_live(const DecodeParams p);
+__global__ void k_live8(const DecodeParams p);
+__global__ void k_live16(const DecodeParams p);
+__global__ void k_live32(const DecodeParams p);
 __global__ void k_alpha_support(const DecodeParams p);
 __global__ void k_support_pack1(const DecodeParams p);
 __global__ void k_support_pack2(const DecodeParams p, int nblk);
@@ -56,7 +58,7 @@ using namespace bsidmap;
 
 namespace {
 constexpr int kPhases = 5;
-constexpr int kHostSub = 8;  // sub-batches of the host-buffer pipeline
+constexpr int kHostSub = 12;  // sub-batches of the host-buffer pipeline (at most 8 + 3)
 constexpr int kMaxAbSub = 4;  // sub-batches of the alpha/beta-overlapped Gamma-sum pipeline
 std::string g_err;  // failures without a decoder (create)
 }  // namespace
@@ -86,7 +88,7 @@ struct bsidmap_decoder {
   void* hs = nullptr;
   size_t hs_bytes = 0;
   cudaStream_t s_copy = nullptr;
-  cudaEvent_t ev_sub[8] = {};
+  cudaEvent_t ev_sub[kHostSub] = {};
   // host-side caches: the free-memory query and the smem opt-ins cost ~1 ms per call,
   // which would dominate single-frame latency (C1)
   size_t budget_cache = 0;
@@ -572,7 +574,13 @@ void launch_pass2(bsidmap_decoder* d, const Plan& P, DecodeParams p, cudaStream_
     const long rows = (long)p.F * (ie - ib);
     p.i_base = ib;
     p.i_end = ie;
-    k_live<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(p);
+    // k_live: 8 / 16 / 32 lanes per row for M_tau <= 64 / 128 / more (rows per 256-thread block: 32 / 16 / 8)
+    if (d->Mt <= 64)
+      k_live8<<<(unsigned)((rows + 31) / 32), 256, 0, s>>>(p);
+    else if (d->Mt <= 128)
+      k_live16<<<(unsigned)((rows + 15) / 16), 256, 0, s>>>(p);
+    else
+      k_live32<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(p);
     d->launches++;
     p.app_G = P.app_G;
     const unsigned gx = (unsigned)(((p.F + P.app_G - 1) / P.app_G + kX2Warps - 1) / kX2Warps);
@@ -1031,11 +1039,21 @@ int bsidmap_decode_batch_host(bsidmap_decoder* d, int F, const uint32_t* rx, siz
   cudaMemcpyAsync(d_off, off, (size_t)F * 8, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(d_rho, rho, (size_t)F * 4, cudaMemcpyHostToDevice, s);
   if (priors) cudaMemcpyAsync(d_pri, priors, nL * 4, cudaMemcpyHostToDevice, s);
-  const int nsub = std::max(1, std::min(kHostSub, F / 8192));
+  // sub-batches: up to 8 equal ones; the last of them split in halves down to 1/8 (4/2/1/1 eighths),
+  // so the D2H left after the last decode is small (C2: 6.5 MB instead of 52 MB)
+  const int neq = std::max(1, std::min(8, F / 8192));
+  std::vector<int> cut;
+  for (int k = 0; k < neq; k++) cut.push_back((int)((long)F * k / neq));
+  if (neq >= 2) {
+    const int last = cut.back(), len = F - last;
+    for (int part : {4, 6, 7}) cut.push_back(last + (int)((long)len * part / 8));
+  }
+  cut.push_back(F);
+  const int nsub = (int)cut.size() - 1;
   const size_t row = (size_t)d->N * d->q;
   long launches = 0;
   for (int k = 0; k < nsub; k++) {
-    const int f0 = (int)((long)F * k / nsub), f1 = (int)((long)F * (k + 1) / nsub);
+    const int f0 = cut[k], f1 = cut[k + 1];
     if ((rc = bsidmap_decode_batch(d, f1 - f0, d_rx, d_off + f0, d_rho + f0, d_pri ? d_pri + f0 * row : nullptr,
                                    d_L + f0 * row, d_st + f0, stream)))
       return rc;

@@ -76,35 +76,46 @@ __global__ void k_extrinsic(const DecodeParams p, float* E) {
 // < 1e-35, far below the 1e-4 relative gate at its 1e-30 floor; eps = 0 skips exact zeros only).
 // Writes the smallest state range holding every live window, its length rounded up to even (the pair
 // core runs two adjacent windows per lane).  One warp per (frame, i) row.
-__global__ void k_live(const DecodeParams p) {
-  const long row = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+template <int LPR>
+__device__ __forceinline__ void live_body(const DecodeParams& p) {
+  // LPR lanes per (frame, i) row, 32 / LPR rows per warp (M_tau <= 64: 8 lanes, so the reductions and
+  // the per-row index work serve four rows at once; the kernel is issue-bound)
+  constexpr int RPW = 32 / LPR;
+  const int lane = threadIdx.x & 31, sl = lane % LPR;
+  const long row = ((long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * RPW + lane / LPR;
   const int ni = p.i_end - p.i_base;  // symbol indices [i_base, i_end) of this launch
-  if (row >= (long)p.F * ni) return;
-  int f, i;
-  row_fi(row, ni, p.i_base, &f, &i);
-  int2 out = make_int2(0, 0);
-  if (p.status[f] == kFrameOk) {
-    const double* a = p.alpha + ((size_t)f * (p.N + 1) + i) * p.Mt;
-    const double* b = beta_row(p, f, i);
-    double s = 0.0;
-    for (int m = lane; m < p.Mt; m += 32) s += a[m] * b[m];
+  const bool valid = row < (long)p.F * ni;
+  int f = 0, i = p.i_base;
+  if (valid) row_fi(row, ni, p.i_base, &f, &i);
+  const bool ok = valid && p.status[f] == kFrameOk;
+  const double* a = p.alpha + ((size_t)f * (p.N + 1) + i) * p.Mt;
+  const double* b = beta_row(p, f, i);
+  double s = 0.0;
+  if (ok)
+    for (int m = sl; m < p.Mt; m += LPR) s += a[m] * b[m];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    const double thr = s * p.live_eps;
-    int lo = 0x7fffffff, hi = -1;
-    for (int m = lane; m < p.Mt; m += 32) {
+  for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);  // within the row's lanes
+  const double thr = s * p.live_eps;
+  int lo = 0x7fffffff, hi = -1;
+  if (ok) {
+    for (int m = sl; m < p.Mt; m += LPR) {
       if (a[m] * b[m] > thr) {
         lo = min(lo, m);
         hi = max(hi, m);
       }
     }
-    lo = __reduce_min_sync(0xffffffffu, lo);
-    hi = __reduce_max_sync(0xffffffffu, hi);
-    if (s > 0.0 && hi >= lo) out = make_int2(lo, (hi - lo + 2) & ~1);
   }
-  if (lane == 0) p.live[(size_t)f * p.N + i] = out;
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if (valid && sl == 0)
+    p.live[(size_t)f * p.N + i] = (ok && s > 0.0 && hi >= lo) ? make_int2(lo, (hi - lo + 2) & ~1) : make_int2(0, 0);
 }
+__global__ void __launch_bounds__(256) k_live8(const DecodeParams p) { live_body<8>(p); }
+__global__ void __launch_bounds__(256) k_live16(const DecodeParams p) { live_body<16>(p); }
+__global__ void __launch_bounds__(256) k_live32(const DecodeParams p) { live_body<32>(p); }
 
 // The slab schedule's backward sweep: per (frame, i) row of symbol indices [i_base, i_end), the state
 // range [first, first + count) holding every alpha_i(m') != 0 (count 0: none), into p.live (which the
