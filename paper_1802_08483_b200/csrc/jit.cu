@@ -198,6 +198,9 @@ bool jit_spec_kernels(int n, int lo, int Mn, CoreKernels* out, std::string* err,
   const bool scalar_app = !minb3 && Mn <= 20;
   const std::string sh = std::to_string(n) + ", " + std::to_string(lo) + ", " + std::to_string(Mn) + ">";
   const std::string px = "bsidmap::SpecCoreX2<" + sh, sc = "bsidmap::SpecCore<" + sh, m = std::to_string(Mn);
+  // the pair APP runs the core on 64-bit pairs (lattice_x2.cuh)
+  const std::string pxa = "bsidmap::SpecCoreX2<" + std::to_string(n) + ", " + std::to_string(lo) + ", " +
+                          std::to_string(Mn) + ", unsigned long long>";
   // slots, in the order of the units below
   std::vector<Unit> units(5);
   auto add = [&](int g, const std::string& e) { units[g].exprs.push_back(e); };
@@ -211,7 +214,7 @@ bool jit_spec_kernels(int n, int lo, int Mn, CoreKernels* out, std::string* err,
   const int kps[4] = {0, 2, 3, 4};
   for (int ks = 1; ks <= 2; ks++)
     for (int k = 0; k < 4; k++)
-      add(ks, std::string(scalar_app ? "bsidmap::k_app_live_x1<" + sc : "bsidmap::k_app_live_x2<" + px) + ", " +
+      add(ks, std::string(scalar_app ? "bsidmap::k_app_live_x1<" + sc : "bsidmap::k_app_live_x2<" + pxa) + ", " +
                   std::to_string(kps[k] <= n - 2 ? kps[k] : 0) + ", " + std::to_string(ks) + ">");
   for (int spt : {1, 2, 4}) add(3, "bsidmap::k_alpha_beta_warp<" + std::to_string(spt) + ", " + m + ">");
   add(3, "bsidmap::k_alpha_beta_cta<" + m + ">");

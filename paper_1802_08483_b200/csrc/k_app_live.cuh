@@ -118,6 +118,7 @@ __device__ __forceinline__ void live_write_rows(const DecodeParams& p, const dou
 template <class Core, int KP, int KS = 1>
 __global__ void __launch_bounds__(kLatticeThreads, KS == 2 ? BSIDMAP_APP_MINB_KS2 : BSIDMAP_LIVE_MINB)
     k_app_live_x2(const DecodeParams p) {
+  using f32x2 = typename Core::P2;
   constexpr int MN = Core::Mn;
   constexpr int NT = 2 << (KS - 1);  // weight tables per lane
   constexpr int RL = Core::NNr - KS;  // last lattice row run per symbol
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(kLatticeThreads, KS == 2 ? BSIDMAP_APP_MINB_KS
       float ba[MN], bb[MN];
       app_weights_pair<MN>(p, A, B, i, ba, bb, da, db);
 #pragma unroll
-      for (int u = 0; u < MN; u++) bt[u] = pk(ba[u], bb[u]);
+      for (int u = 0; u < MN; u++) bt[u] = Core::pk(ba[u], bb[u]);
     }
     sg[lane] = in ? g : -1;  // the frame's lanes stay one segment (a window of weight 0 adds 0.0)
     if (__any_sync(0xffffffffu, da > 0.0 || db > 0.0)) {
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(kLatticeThreads, KS == 2 ? BSIDMAP_APP_MINB_KS
         f32x2 w1[MN], w0[MN], wi[MN];
         Core::last_row_weights(lane_t, [&](int u) { return bt[u]; }, [&](int u) -> f32x2& { return w1[u]; },
                                [&](int u) -> f32x2& { return w0[u]; });
-        const f32x2 a2 = pk(p.lc.a, p.lc.a);
+        const f32x2 a2 = Core::pk(p.lc.a, p.lc.a);
         Core::template row_transpose<Core::NNr - 1>(w1, wi, lane_t.q1, a2);  // (x_{n-1}, x_n) = (1, 1)
 #pragma unroll
         for (int u = 0; u < MN; u++) wt[u * 32] = wi[u];
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(kLatticeThreads, KS == 2 ? BSIDMAP_APP_MINB_KS
         // t(m', D) = sum_k G_n(m', k, D) bt(m', k) = sum_e G_{n-KS}[e] w[e]  (two chains)
         const f32x2* W = KS == 1 ? wt + (((x >> nb) & 1u) ? 0 : MN * 32)
                                  : wt + (size_t)((((x >> nb) & 1u) ? 0 : 2) + (((x >> (nb - 1)) & 1u) ? 0 : 1)) * MN * 32;
-        f32x2 t0 = 0ull, t1 = 0ull;
+        f32x2 t0 = Core::f2z(), t1 = Core::f2z();
         auto dot = [&](const f32x2 (&gg)[MN]) {
 #pragma unroll
           for (int u = 0; u < MN; u += 2) {

@@ -89,6 +89,7 @@ __device__ __forceinline__ int exp2_of(double x) {  // floor(log2 x) for normal 
 #endif
 template <class Core, bool kStoreGamma>
 __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_x2(const DecodeParams p) {
+  using f32x2 = typename Core::P2;
   constexpr int MN = Core::Mn;
   extern __shared__ uint32_t s_C[];
   const int i = blockIdx.y + p.i_base;
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_
   const LaneGeom A = lane_geom_at(p, i, ga), B = lane_geom_at(p, i, ga + blockDim.x);
   f32x2 acc[MN];
 #pragma unroll
-  for (int e = 0; e < MN; e++) acc[e] = 0ull;
+  for (int e = 0; e < MN; e++) acc[e] = Core::f2z();
 
   if (__any_sync(0xffffffffu, A.active || B.active)) {
     typename Core::Lane lane;
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1_MINB) k_gamma_sum_
     const float* pb = p.priors ? p.priors + ((size_t)B.f * p.N + i) * p.q : nullptr;
     const float usc = 1.f / p.q;
     for (int D = 0; D < p.q; D++) {
-      const f32x2 P = pa ? pk(__ldg(pa + D), __ldg(pb + D)) : pk(1.f, 1.f);
+      const f32x2 P = pa ? Core::pk(__ldg(pa + D), __ldg(pb + D)) : Core::pk(1.f, 1.f);
       f32x2 fo[MN];
       Core::template run<BSIDMAP_L1_GROUP>(lane, s_C[D], p, fo);
 #pragma unroll
@@ -204,6 +205,7 @@ __host__ __device__ constexpr int l1_head_rows(int NN, int LO, int MN, int K, in
 
 template <class Core, int K, bool kPri = true>
 __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1C_MINB) k_gamma_sum_x2_cls(const DecodeParams p) {
+  using f32x2 = typename Core::P2;
   constexpr int MN = Core::Mn;
   constexpr int NC = 1 << K;
   constexpr int KH = l1_head_rows(Core::NNr, Core::Lo, MN, K, BSIDMAP_L1C_MINB);
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1C_MINB) k_gamma_sum
     const uint16_t* Di = p.Ds[K - 2] + (size_t)i * p.q;
     f32x2 acc[MN];
 #pragma unroll
-    for (int e = 0; e < MN; e++) acc[e] = 0ull;
+    for (int e = 0; e < MN; e++) acc[e] = Core::f2z();
     if (__any_sync(0xffffffffu, alpha_live(p, askip, ba, A, i) || alpha_live(p, askip, bb, B, i))) {
       typename Core::Lane lane;
       Core::init(lane, A.active ? win_bits(wa, A.s) : 0ull, B.active ? win_bits(wb, B.s) : 0ull, p);
@@ -265,16 +267,16 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1C_MINB) k_gamma_sum
           for (int e = 0; e < MN; e++) {
             if (!first) acc[e] = fadd2(acc[e], res[e * kLatticeThreads]);
             res[e * kLatticeThreads] = acc[e];
-            acc[e] = 0ull;
+            acc[e] = Core::f2z();
           }
           first = false;
           cur = c;
         }
         f32x2 fo[MN];
-        f32x2 P = 0ull;
+        f32x2 P = Core::f2z();
         if constexpr (kPri) {  // P(D_i = D) of the two windows' frames
           const int D = Di[k];
-          P = pk(__ldg(pa + D), __ldg(pb + D));
+          P = Core::pk(__ldg(pa + D), __ldg(pb + D));
         }
         auto add = [&](const f32x2 (&g)[MN]) {
 #pragma unroll
@@ -285,7 +287,7 @@ __global__ void __launch_bounds__(kLatticeThreads, BSIDMAP_L1C_MINB) k_gamma_sum
         if constexpr (KH > 0) {
           const f32x2* hp = s_head + (x & ((1u << KH) - 1u)) * (MN - E0) * kLatticeThreads;
 #pragma unroll
-          for (int e = 0; e < MN; e++) fo[e] = e < E0 ? 0ull : hp[(e < E0 ? 0 : e - E0) * kLatticeThreads];
+          for (int e = 0; e < MN; e++) fo[e] = e < E0 ? Core::f2z() : hp[(e < E0 ? 0 : e - E0) * kLatticeThreads];
           Core::template run_from_then<KH + 1, Core::NNr - K, BSIDMAP_L1_GROUP>(lane, x, p, fo, add);
         } else {
           Core::template run_prefix_then<K, BSIDMAP_L1_GROUP>(lane, x, p, fo, add);
@@ -450,6 +452,7 @@ __host__ __device__ __forceinline__ int app_prefix_bits(int q, int n) {
 
 template <class Core>
 __global__ void __launch_bounds__(kLatticeThreads) k_gamma_dump_x2(const DecodeParams p) {
+  using f32x2 = typename Core::P2;
   constexpr int MN = Core::Mn;
   extern __shared__ uint32_t s_C[];
   const int i = p.dbg_i;
@@ -499,14 +502,14 @@ CoreKernels make_core_kernels_x2_base(long nodes) {
   // one folded row on the pair core: two (four smem weight tables per lane) measured slower with the
   // live-window APP (C4 pass 2 33.7 vs 23.7 ms, C2 29.4 vs 26.1; tools/exp_appkpks.sh)
   k.app_ks_auto = 1;
-  k.app_live[0][0] = k_app_live_x2<Core, 0, 1>;
-  k.app_live[0][1] = k_app_live_x2<Core, 2, 1>;
-  k.app_live[0][2] = k_app_live_x2<Core, 3, 1>;
-  k.app_live[0][3] = k_app_live_x2<Core, 4, 1>;
-  k.app_live[1][0] = k_app_live_x2<Core, 0, 2>;
-  k.app_live[1][1] = k_app_live_x2<Core, 2, 2>;
-  k.app_live[1][2] = k_app_live_x2<Core, 3, 2>;
-  k.app_live[1][3] = k_app_live_x2<Core, 4, 2>;
+  k.app_live[0][0] = k_app_live_x2<typename Core::AsmCore, 0, 1>;
+  k.app_live[0][1] = k_app_live_x2<typename Core::AsmCore, 2, 1>;
+  k.app_live[0][2] = k_app_live_x2<typename Core::AsmCore, 3, 1>;
+  k.app_live[0][3] = k_app_live_x2<typename Core::AsmCore, 4, 1>;
+  k.app_live[1][0] = k_app_live_x2<typename Core::AsmCore, 0, 2>;
+  k.app_live[1][1] = k_app_live_x2<typename Core::AsmCore, 2, 2>;
+  k.app_live[1][2] = k_app_live_x2<typename Core::AsmCore, 3, 2>;
+  k.app_live[1][3] = k_app_live_x2<typename Core::AsmCore, 4, 2>;
   k.app_live_W = 2;
   {
     using Core_ = Core;

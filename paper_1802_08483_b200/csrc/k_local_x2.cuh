@@ -33,6 +33,7 @@ __host__ __device__ __forceinline__ size_t local_warp_smem(int Mn, int q) {
 
 template <class Core>
 __global__ void __launch_bounds__(kLocalWarps * 32, Core::kMinBlocks) k_local_fwd(const DecodeParams p) {
+  using f32x2 = typename Core::P2;
   constexpr int MN = Core::Mn;
   extern __shared__ __align__(128) unsigned char s_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -60,7 +61,7 @@ __global__ void __launch_bounds__(kLocalWarps * 32, Core::kMinBlocks) k_local_fw
     const LaneGeom A = geom_fm(p, i, f, ma, ma < Mt), B = geom_fm(p, i, f, mb, mb < Mt);
     f32x2 acc[MN];
 #pragma unroll
-    for (int e = 0; e < MN; e++) acc[e] = 0ull;
+    for (int e = 0; e < MN; e++) acc[e] = Core::f2z();
     if (__any_sync(0xffffffffu, A.active || B.active)) {
       typename Core::Lane lt;
       Core::init(lt, A.active ? load_window(p, f, A.s, A.rho) : 0ull, B.active ? load_window(p, f, B.s, B.rho) : 0ull,
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(kLocalWarps * 32, Core::kMinBlocks) k_local_fw
         const float P = pri ? __ldg(pri + D) : 1.f;
         f32x2 fo[MN];
         Core::template run<true>(lt, sC[D], p, fo);
-        const f32x2 P2 = pk(P, P);
+        const f32x2 P2 = Core::pk(P, P);
 #pragma unroll
         for (int e = 0; e < MN; e++) acc[e] = ffma2(P2, fo[e], acc[e]);
       }
@@ -110,6 +111,7 @@ __global__ void __launch_bounds__(kLocalWarps * 32, Core::kMinBlocks) k_local_fw
 // 5 CTAs/SM where the pair core allows 3 (as the round-1 tiled APP kernel it derives from)
 template <class Core>
 __global__ void __launch_bounds__(kLocalWarps * 32, Core::kMinBlocks > 2 ? 5 : 2) k_local_bwd(const DecodeParams p) {
+  using f32x2 = typename Core::P2;
   constexpr int MN = Core::Mn;
   extern __shared__ __align__(128) unsigned char s_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(kLocalWarps * 32, Core::kMinBlocks > 2 ? 5 : 2
         const int j = ma + lo + e;
         const double va = ((A.vmask >> e) & 1u) ? row[min(max(j, 0), 63)] : 0.0;
         const double vb = ((B.vmask >> e) & 1u) ? row[min(max(j + 1, 0), 63)] : 0.0;
-        bt[e] = pk((float)(va * sa), (float)(vb * sb));
+        bt[e] = Core::pk((float)(va * sa), (float)(vb * sb));
       }
       da = (A.active && bm_a > 0.0) ? alpha_f[(size_t)i * Mt + ma] * pow2d(Ea) : 0.0;
       db = (B.active && bm_b > 0.0) ? alpha_f[(size_t)i * Mt + mb] * pow2d(Eb) : 0.0;
@@ -176,7 +178,7 @@ __global__ void __launch_bounds__(kLocalWarps * 32, Core::kMinBlocks > 2 ? 5 : 2
       for (int D = 0; D < p.q; D++) {
         f32x2 fo[MN];
         Core::template run<BSIDMAP_APP_GROUP>(lt, sC[D], p, fo);
-        f32x2 t0 = 0ull, t1 = 0ull;
+        f32x2 t0 = Core::f2z(), t1 = Core::f2z();
 #pragma unroll
         for (int e = 0; e < MN; e += 2) {
           t0 = ffma2(fo[e], bt[e], t0);

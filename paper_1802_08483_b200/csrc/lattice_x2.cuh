@@ -15,32 +15,56 @@
 
 namespace bsidmap {
 
-typedef unsigned long long f32x2;
+// A pair of FP32 values (lo = window a, hi = window b) and the sm_100 packed FP32 arithmetic
+// (fma.rn.f32x2 / add.rn.f32x2 / mul.rn.f32x2), in two representations with the same results:
+//  - float2 through the CUDA builtins: the compiler sees two 32-bit registers (fewer moves; pass 1
+//    C3-C5 2-4 % faster than the 64-bit form, tools/gpu_quick2.sh r02 q3);
+//  - one 64-bit register through inline PTX: the pair live-window APP keeps it (with float2 its C2
+//    instance spills 228 B and runs 26.0 -> 29.7 ms).
+// A core picks one (SpecCoreX2<..., P2T>); the kernels take the type from their core.
+typedef float2 f32x2;
+typedef unsigned long long u64x2;
 
-__device__ __forceinline__ f32x2 pk(float lo, float hi) {
-  return (f32x2)__float_as_uint(lo) | ((f32x2)__float_as_uint(hi) << 32);
-}
-__device__ __forceinline__ float lo_of(f32x2 v) { return __uint_as_float((unsigned)v); }
-__device__ __forceinline__ float hi_of(f32x2 v) { return __uint_as_float((unsigned)(v >> 32)); }
+__device__ __forceinline__ float lo_of(float2 v) { return v.x; }
+__device__ __forceinline__ float hi_of(float2 v) { return v.y; }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 
-__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
-  f32x2 d;
+__device__ __forceinline__ float lo_of(u64x2 v) { return __uint_as_float((unsigned)v); }
+__device__ __forceinline__ float hi_of(u64x2 v) { return __uint_as_float((unsigned)(v >> 32)); }
+__device__ __forceinline__ u64x2 ffma2(u64x2 a, u64x2 b, u64x2 c) {
+  u64x2 d;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
   return d;
 }
-__device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b) {
-  f32x2 d;
+__device__ __forceinline__ u64x2 fadd2(u64x2 a, u64x2 b) {
+  u64x2 d;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
-__device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
-  f32x2 d;
+__device__ __forceinline__ u64x2 fmul2(u64x2 a, u64x2 b) {
+  u64x2 d;
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
 
-template <int NN, int LO, int MN>
+template <class P2>
+__device__ __forceinline__ P2 pair_of(float lo, float hi);
+template <>
+__device__ __forceinline__ float2 pair_of<float2>(float lo, float hi) { return make_float2(lo, hi); }
+template <>
+__device__ __forceinline__ u64x2 pair_of<u64x2>(float lo, float hi) {
+  return (u64x2)__float_as_uint(lo) | ((u64x2)__float_as_uint(hi) << 32);
+}
+
+template <int NN, int LO, int MN, class P2T = float2>
 struct SpecCoreX2 {
+  using P2 = P2T;                                       // the pair representation of this core
+  using f32x2 = P2T;
+  using AsmCore = SpecCoreX2<NN, LO, MN, u64x2>;        // the same core on 64-bit pairs (pair APP)
+  __device__ __forceinline__ static P2 pk(float lo, float hi) { return pair_of<P2>(lo, hi); }
+  __device__ __forceinline__ static P2 f2z() { return pair_of<P2>(0.f, 0.f); }
   static constexpr int Mn = MN;
   static constexpr int NNr = NN;  // lattice rows n
   static constexpr int Lo = LO;   // m_n^-
@@ -71,12 +95,12 @@ struct SpecCoreX2 {
   __device__ __forceinline__ static void row_from(f32x2 (&d)[MN], const f32x2 (&s)[MN], const f32x2 (&Q)[J + 1],
                                                   f32x2 a2) {
     constexpr bool kLast = (R == NN);
-    f32x2 prev = 0ull;
+    f32x2 prev = f2z();
 #pragma unroll
     for (int e = 0; e < MN; e++) {
       const int j = R + LO + e;
       if (j < 0) {  // structurally zero
-        if constexpr (!kInPlace) d[e] = 0ull;
+        if constexpr (!kInPlace) d[e] = f2z();
         continue;
       }
       f32x2 v;
@@ -288,12 +312,12 @@ struct SpecCoreX2 {
       const int j = R + LO + e;
       const int jn = j + 1;  // column of node e + 1
       const bool chain_next = (e + 1 < MN) && (jn >= 1) && (e + 1 > 0);
-      dv[e] = (j < 0) ? 0ull : (chain_next ? ffma2(a2, dv[e + 1 < MN ? e + 1 : e], w[e]) : w[e]);
+      dv[e] = (j < 0) ? f2z() : (chain_next ? ffma2(a2, dv[e + 1 < MN ? e + 1 : e], w[e]) : w[e]);
     }
 #pragma unroll
     for (int e = 0; e < MN; e++) {
       const int j = R + LO + e;
-      const f32x2 left = (e >= 1 && j - 1 >= 0) ? dv[e >= 1 ? e - 1 : 0] : 0ull;
+      const f32x2 left = (e >= 1 && j - 1 >= 0) ? dv[e >= 1 ? e - 1 : 0] : f2z();
       wi[e] = (j >= 1) ? ffma2(dv[e], Q[j < 1 ? 1 : j], left) : left;
     }
   }
@@ -306,7 +330,7 @@ struct SpecCoreX2 {
 #pragma unroll
     for (int e = 0; e < MN; e++) {
       const int j = NN + LO + e;
-      const f32x2 del = (e >= 1) ? bt(e - 1) : 0ull;
+      const f32x2 del = (e >= 1) ? bt(e - 1) : f2z();
       if constexpr (NN + LO >= 1) {  // every last-row column is >= 1
         w1(e) = ffma2(bt(e), L.q1[j], del);
         w0(e) = ffma2(bt(e), L.q0[j], del);
