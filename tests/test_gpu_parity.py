@@ -271,6 +271,27 @@ def test_chunked_equals_unchunked_and_host_path():
     np.testing.assert_allclose(L3.numpy(), L1, rtol=1e-5, atol=1e-30)
 
 
+@pytest.mark.parametrize("frames", [16384 + 17, 8 * 8192 + 5])
+def test_host_path_subbatches(frames):
+    """bsidmap_decode_batch_host splits the batch into up to 8 equal sub-batches and the last one
+    again into 1/2, 1/4, 1/8, 1/8 (host path): with C1 frames (small) at 2 and 8 equal
+    sub-batches plus the split tail, every frame's status equals and its L agrees (1e-5) with the
+    device-buffer decode of the same frames in one call, and sampled frames match the oracle."""
+    cfg = small_cfg("C1")
+    b = bsidgen.make_batch(cfg, 3, frames)
+    d, L1, st1 = run_gpu(cfg, b, 3)
+    rx = torch.from_numpy(b.rx.ravel().copy()).pin_memory()
+    off = torch.from_numpy(b.offsets).pin_memory()
+    rho = torch.from_numpy(b.rho).pin_memory()
+    L3 = torch.empty((frames, cfg.N, cfg.q), dtype=torch.float32).pin_memory()
+    st3 = torch.empty(frames, dtype=torch.int32).pin_memory()
+    d.decode_host(rx, off, rho, None, L3, st3)
+    np.testing.assert_array_equal(st3.numpy(), st1)
+    np.testing.assert_allclose(L3.numpy(), L1, rtol=1e-5, atol=1e-30)
+    picks = [0, frames // 2, frames - 1]
+    assert_parity(L3.numpy().astype(np.float64), st3.numpy(), run_oracle(cfg, b, picks), picks)
+
+
 @pytest.mark.parametrize("name,frames", [("C2", 37), ("C3", 5)])
 def test_alpha_beta_overlap_subbatches_bit_identical(name, frames, monkeypatch):
     """The alpha/beta-overlapped sub-batch pipeline (side stream) changes only
